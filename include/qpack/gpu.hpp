@@ -1,0 +1,46 @@
+// Batched GPU entry points of qpack-b200 (C++ face of include/qpack_b200.h).
+//
+// The reference's per-word calls (redq_residues_into, dqt_mul_poly, fgdp_dot
+// on length-1 vectors, GfqField::mul) cannot be accelerated one word at a
+// time; these overloads take whole batches and run the sm_100a kernels.
+// Pointers are HOST memory; results are visible on return, exactly like the
+// reference.  Errors throw the reference's exception types.
+#pragma once
+
+#include <cstdint>
+#include <span>
+
+#include "qpack/counters.hpp"
+#include "qpack/gfq.hpp"
+#include "qpack/params.hpp"
+#include "qpack/redq.hpp"
+
+namespace qpack::gpu {
+
+// redq_residues_into over words given as exact doubles; out has n*(d+1)
+// residues (p <= 256).  (redq.hpp:73-74)
+void redq_residues_batch(std::span<const double> words, const RedqPlan& plan, std::span<std::uint8_t> out,
+                         CostReport* cost = nullptr);
+
+// n products of degree-<k polynomials (records of k coefficients) -> n*(2k-1)
+// residues, via pack -> fp64 product -> REDQ.  (dqt_mul_poly dqt.hpp:46,
+// fqt_mul single chunk polymul.hpp:42)
+void polymul_batch(std::span<const std::uint8_t> a, std::span<const std::uint8_t> b, const QadicParams& params,
+                   std::span<std::uint8_t> out, CostReport* cost = nullptr);
+
+enum class GfqPath { packed = 0, dlog = 1 };
+
+// elementwise GF(p^k) products of coefficient records (k bytes each)
+void gfq_mul_batch(std::span<const std::uint8_t> a, std::span<const std::uint8_t> b, const GfqField& field,
+                   std::span<std::uint8_t> out, GfqPath path = GfqPath::packed);
+
+// elementwise GfqField::mul over reps
+void gfq_mul_batch(std::span<const GfqElt> a, std::span<const GfqElt> b, const GfqField& field,
+                   std::span<GfqElt> out);
+
+// C = A*B of coefficient records: A is m x K x k, B is K x n x k, C m x n x k
+void gfq_matmul_coeffs(std::span<const std::uint8_t> A, std::span<const std::uint8_t> B, std::size_t m,
+                       std::size_t K, std::size_t n, const GfqField& field, std::span<std::uint8_t> C,
+                       std::uint32_t chunk = 0, CostReport* cost = nullptr);
+
+}  // namespace qpack::gpu

@@ -1,0 +1,117 @@
+// K1 pack kernels (coefficient records and dlog reps -> q-adic doubles) and
+// the K4 launch dispatcher; the K4 kernel templates are in gfq_matmul.cuh.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "device_common.cuh"
+#include "kernels.hpp"
+
+namespace qpk {
+
+cudaError_t matmul_launch_k1(const GfqMatmulParams&, const double*, const double*, uint64_t, uint64_t, uint64_t,
+                             uint64_t, uint64_t, uint8_t*, uint32_t*, cudaStream_t);
+cudaError_t matmul_launch_k2(const GfqMatmulParams&, const double*, const double*, uint64_t, uint64_t, uint64_t,
+                             uint64_t, uint64_t, uint8_t*, uint32_t*, cudaStream_t);
+cudaError_t matmul_launch_k3(const GfqMatmulParams&, const double*, const double*, uint64_t, uint64_t, uint64_t,
+                             uint64_t, uint64_t, uint8_t*, uint32_t*, cudaStream_t);
+cudaError_t matmul_launch_k4(const GfqMatmulParams&, const double*, const double*, uint64_t, uint64_t, uint64_t,
+                             uint64_t, uint64_t, uint8_t*, uint32_t*, cudaStream_t);
+
+namespace {
+
+// ---------------------------------------------------------------- K1 packs
+// 32x32 tiles through shared memory so both the record reads and the
+// (possibly transposed) double writes are coalesced.
+__global__ void pack_coeffs_kernel(uint32_t p, uint32_t k, double qd, const uint8_t* __restrict__ src, uint64_t rows,
+                                   uint64_t cols, double* __restrict__ dst, uint64_t ld, bool transpose) {
+    __shared__ double tile[32][33];
+    const uint64_t r0 = uint64_t(blockIdx.y) * 32, c0 = uint64_t(blockIdx.x) * 32;
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    for (int i = ty; i < 32; i += 8) {
+        const uint64_t r = r0 + i, c = c0 + tx;
+        double v = 0.0;
+        if (r < rows && c < cols) {
+            const uint8_t* e = src + (r * cols + c) * k;
+            for (int t = static_cast<int>(k) - 1; t >= 0; --t) v = fma(v, qd, static_cast<double>(e[t] % p));
+        }
+        tile[i][tx] = v;
+    }
+    __syncthreads();
+    for (int i = ty; i < 32; i += 8) {
+        if (transpose) {
+            const uint64_t c = c0 + i, r = r0 + tx;
+            if (r < rows && c < cols) dst[c * ld + r] = tile[tx][i];
+        } else {
+            const uint64_t r = r0 + i, c = c0 + tx;
+            if (r < rows && c < cols) dst[r * ld + c] = tile[i][tx];
+        }
+    }
+}
+
+__global__ void pack_reps_kernel(const double* __restrict__ fval, uint32_t order, const uint32_t* __restrict__ src,
+                                 uint64_t rows, uint64_t cols, double* __restrict__ dst, uint64_t ld, bool transpose) {
+    extern __shared__ double s_fval[];
+    __shared__ double tile[32][33];
+    for (uint32_t i = threadIdx.y * 32 + threadIdx.x; i < order; i += 256) s_fval[i] = fval[i];
+    __syncthreads();
+    const uint64_t r0 = uint64_t(blockIdx.y) * 32, c0 = uint64_t(blockIdx.x) * 32;
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    for (int i = ty; i < 32; i += 8) {
+        const uint64_t r = r0 + i, c = c0 + tx;
+        double v = 0.0;
+        if (r < rows && c < cols) {
+            const uint32_t rep = src[r * cols + c];
+            v = rep < order ? s_fval[rep] : 0.0;
+        }
+        tile[i][tx] = v;
+    }
+    __syncthreads();
+    for (int i = ty; i < 32; i += 8) {
+        if (transpose) {
+            const uint64_t c = c0 + i, r = r0 + tx;
+            if (r < rows && c < cols) dst[c * ld + r] = tile[tx][i];
+        } else {
+            const uint64_t r = r0 + i, c = c0 + tx;
+            if (r < rows && c < cols) dst[r * ld + c] = tile[i][tx];
+        }
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_gfq_matmul(const GfqMatmulParams& P, const double* at, const double* b, uint64_t m, uint64_t n,
+                              uint64_t K_pad, uint64_t m_pad, uint64_t n_pad, uint8_t* out_coeffs,
+                              uint32_t* out_reps, cudaStream_t s) {
+    if (m == 0 || n == 0) return cudaSuccess;
+    if (m_pad % 128 || n_pad % 128 || K_pad % 16) return cudaErrorInvalidValue;
+    switch (P.k) {
+        case 1: return matmul_launch_k1(P, at, b, m, n, K_pad, m_pad, n_pad, out_coeffs, out_reps, s);
+        case 2: return matmul_launch_k2(P, at, b, m, n, K_pad, m_pad, n_pad, out_coeffs, out_reps, s);
+        case 3: return matmul_launch_k3(P, at, b, m, n, K_pad, m_pad, n_pad, out_coeffs, out_reps, s);
+        case 4: return matmul_launch_k4(P, at, b, m, n, K_pad, m_pad, n_pad, out_coeffs, out_reps, s);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+cudaError_t launch_pack_coeffs(uint32_t p, uint32_t k, double qd, const uint8_t* src, uint64_t rows, uint64_t cols,
+                               double* dst, uint64_t ld, bool transpose, cudaStream_t s) {
+    if (rows == 0 || cols == 0) return cudaSuccess;
+    dim3 grid(static_cast<unsigned>((cols + 31) / 32), static_cast<unsigned>((rows + 31) / 32));
+    pack_coeffs_kernel<<<grid, dim3(32, 8), 0, s>>>(p, k, qd, src, rows, cols, dst, ld, transpose);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pack_reps(const double* fval, uint32_t order, const uint32_t* src, uint64_t rows, uint64_t cols,
+                             double* dst, uint64_t ld, bool transpose, cudaStream_t s) {
+    if (rows == 0 || cols == 0) return cudaSuccess;
+    dim3 grid(static_cast<unsigned>((cols + 31) / 32), static_cast<unsigned>((rows + 31) / 32));
+    const size_t smem = size_t(order) * 8;
+    if (smem > 200 * 1024) return cudaErrorInvalidValue;
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(pack_reps_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    pack_reps_kernel<<<grid, dim3(32, 8), smem, s>>>(fval, order, src, rows, cols, dst, ld, transpose);
+    return cudaGetLastError();
+}
+
+}  // namespace qpk

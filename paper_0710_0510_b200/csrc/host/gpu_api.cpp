@@ -1,0 +1,488 @@
+// GPU layer of qpack-b200: device mirrors of plans and fields, the batched
+// qpack::gpu entry points and the gfq_matmul drop-in.  No CPU fallback: every
+// entry point here runs the sm_100a kernels or throws.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <tuple>
+
+#include "device_state.hpp"
+#include "gpu_internal.hpp"
+#include "qpack/gpu.hpp"
+#include "qpack/polymul.hpp"
+
+namespace qpack::gpu {
+
+void check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw device_error(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+void require_device() {
+    int n = 0;
+    const cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0)
+        throw device_error(std::string("qpack-b200: no CUDA device available (") + cudaGetErrorString(e) + ")");
+}
+
+DevBuf::~DevBuf() {
+    if (ptr) cudaFree(ptr);
+}
+
+void* DevBuf::ensure(std::size_t n) {
+    if (n <= bytes && ptr) return ptr;
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    bytes = 0;
+    check(cudaMalloc(&ptr, std::max<std::size_t>(n, 16)), "cudaMalloc");
+    bytes = std::max<std::size_t>(n, 16);
+    return ptr;
+}
+
+Staging::Staging() {
+    for (auto& s : streams) check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "cudaStreamCreate");
+}
+
+Staging::~Staging() {
+    for (auto& s : streams)
+        if (s) cudaStreamDestroy(s);
+}
+
+}  // namespace qpack::gpu
+
+namespace qpack::detail {
+
+using gpu::check;
+
+qpk::RedqParams make_redq_params(const RedqPlan& plan, gpu::DevBuf* table) {
+    if (plan.p > 256) throw std::invalid_argument("qpack-b200 REDQ: residues are emitted as uint8, p must be <= 256");
+    if (plan.d + 1 > static_cast<unsigned>(qpk::kMaxDigits))
+        throw std::invalid_argument("qpack-b200 REDQ: at most 64 digits per word");
+    qpk::RedqParams P{};
+    P.p = static_cast<uint32_t>(plan.p);
+    P.d = plan.d;
+    P.qbits = is_pow2(plan.q) ? bit_width_u128(plan.q) - 1 : 0;
+    P.neg_q = static_cast<uint32_t>(plan.neg_q_mod_p);
+    P.mod_magic = static_cast<uint32_t>(((u64(1) << 32) + plan.p - 1) / plan.p);
+    P.float_mode = plan.mode == RedqMode::float_premul;
+    P.inv_p = plan.inv_p.inv_up;
+    P.r_max = static_cast<double>(plan.inv_p.r_max);
+    P.q = plan.q;
+    // words must lie below min(q^(d+1), 2^53)
+    const u128 two53 = u128(1) << 53;
+    P.limit = (pow_fits_u128(plan.q, plan.d + 1) && checked_pow_u128(plan.q, plan.d + 1) < two53)
+                  ? static_cast<double>(static_cast<u64>(checked_pow_u128(plan.q, plan.d + 1)))
+                  : 9007199254740992.0;
+    u128 pw = 1;
+    for (unsigned i = 0; i <= plan.d; ++i) {
+        const bool small = pw < two53;
+        P.qpow[i] = small ? static_cast<uint64_t>(pw) : (uint64_t(1) << 63);
+        P.inv_q[i] = small ? ReciprocalDivisor::make(static_cast<u64>(pw)).inv_up : 0.0;  // r < 2^53 <= q^i -> 0
+        if (pw < two53) pw *= plan.q;
+    }
+    // tabulated correction on the device when the window table fits shared memory
+    P.window = 0;
+    if (plan.neg_q_mod_p != 0 && plan.correction && plan.d > 0) {
+        const CorrectionTable& t = *plan.correction;
+        if (t.k_window >= 2 && t.k_window <= 4 && t.entries.size() <= 16384 && table) {
+            std::vector<uint32_t> packed(t.entries.size());
+            for (std::size_t idx = 0; idx < t.entries.size(); ++idx) {
+                u64 e = t.entries[idx];
+                uint32_t w = 0;
+                for (u32 j = 0; j < t.k_window; ++j, e /= t.radix) w |= static_cast<uint32_t>(e % t.radix) << (8 * j);
+                packed[idx] = w;
+            }
+            table->ensure(packed.size() * 4);
+            check(cudaMemcpy(table->ptr, packed.data(), packed.size() * 4, cudaMemcpyHostToDevice), "table upload");
+            P.window = t.k_window;
+            P.radix = static_cast<uint32_t>(t.radix);
+            P.n_entries = static_cast<uint32_t>(t.entries.size());
+            P.table = table->as<uint32_t>();
+        }
+        // otherwise: direct correction on the device (identical residues,
+        // test_redq.cpp "correction table reproduces the direct formula")
+    }
+    return P;
+}
+
+DevicePlanCache& device_plan(const RedqPlan& plan) {
+    if (!plan.device) {
+        gpu::require_device();
+        auto c = std::make_shared<DevicePlanCache>();
+        c->prm = make_redq_params(plan, &c->table);
+        c->status.ensure(4);
+        check(cudaMemset(c->status.ptr, 0, 4), "status init");
+        plan.device = std::move(c);
+    }
+    return *plan.device;
+}
+
+CostReport redq_batch_cost(const RedqPlan& plan, u64 n) {
+    CostReport c;
+    c.divisions = n;
+    c.reduction_calls = n;
+    if (plan.neg_q_mod_p != 0 && plan.correction && plan.d > 0) {
+        const u64 w = plan.correction->k_window;
+        c.table_accesses = n * ((plan.d + w - 2) / (w - 1));
+    }
+    return c;
+}
+
+DeviceFieldCache& device_field(const GfqField& f) {
+    auto& slot = FieldAccess::device(f);
+    if (slot) return *slot;
+    gpu::require_device();
+    const u64 p = f.p();
+    const u32 k = f.k();
+    if (p > 255 || k > static_cast<u32>(qpk::kMaxGfqK))
+        throw std::invalid_argument("qpack-b200 GF(p^k): device path needs p < 256 and k <= 4");
+    auto c = std::make_shared<DeviceFieldCache>();
+    const u64 lh = FieldAccess::lh_radix(f);
+    u64 nlh = 1;
+    for (u32 i = 0; i < k; ++i) nlh *= lh;
+    const u64 order = f.order();
+    const u64 words = 2 * nlh + 2 * order;
+    if (words * 4 > 96 * 1024)
+        throw std::invalid_argument("qpack-b200 GF(p^k): field tables exceed the shared-memory budget");
+    // coefficient-form tables: rep -> packed coefficient bytes
+    auto bytes_of = [&](u32 rep) {
+        uint32_t w = 0;
+        const std::vector<u64> cf = f.to_coeffs(GfqElt{rep});
+        for (u32 i = 0; i < k; ++i) w |= static_cast<uint32_t>(cf[i]) << (8 * i);
+        return w;
+    };
+    std::vector<uint32_t> host(words);
+    for (u64 i = 0; i < nlh; ++i) {
+        host[i] = bytes_of(FieldAccess::low(f)[i]);
+        host[nlh + i] = bytes_of(FieldAccess::high(f)[i]);
+    }
+    for (u64 i = 0; i < order; ++i) {
+        host[2 * nlh + i] = FieldAccess::log(f)[i];
+        host[2 * nlh + order + i] = bytes_of(static_cast<u32>(i));
+    }
+    c->tables.ensure(words * 4);
+    check(cudaMemcpy(c->tables.ptr, host.data(), words * 4, cudaMemcpyHostToDevice), "field tables upload");
+    c->fval.ensure(order * 8);
+    check(cudaMemcpy(c->fval.ptr, FieldAccess::fval(f).data(), order * 8, cudaMemcpyHostToDevice), "fval upload");
+    c->nlh = static_cast<uint32_t>(nlh);
+
+    const RedqPlan digits = RedqPlan::build(p, FieldAccess::q(f), 2 * k - 2, RedqMode::integer);
+    const qpk::RedqParams rq = make_redq_params(digits, nullptr);
+    const uint32_t* tb = c->tables.as<uint32_t>();
+    qpk::GfqElemParams& E = c->elem;
+    E.rq = rq;
+    E.k = k;
+    E.p = static_cast<uint32_t>(p);
+    E.order = static_cast<uint32_t>(order);
+    E.group = static_cast<uint32_t>(order - 1);
+    E.lh_radix = static_cast<uint32_t>(lh);
+    E.qd = static_cast<double>(FieldAccess::q(f));
+    E.lc = tb;
+    E.hc = tb + nlh;
+    E.log = tb + 2 * nlh;
+    E.alog = tb + 2 * nlh + order;
+    E.tables_words = static_cast<uint32_t>(words);
+    qpk::GfqMatmulParams& M = c->mm;
+    M.rq = rq;
+    M.k = k;
+    M.p = E.p;
+    M.order = E.order;
+    M.group = E.group;
+    M.lh_radix = E.lh_radix;
+    M.qd = E.qd;
+    M.lc = E.lc;
+    M.hc = E.hc;
+    M.log = E.log;
+    M.fval = c->fval.as<double>();
+    slot = std::move(c);
+    return *slot;
+}
+
+}  // namespace qpack::detail
+
+namespace qpack::gpu {
+
+using detail::DeviceFieldCache;
+using detail::DevicePlanCache;
+
+uint32_t take_status(DevicePlanCache& dp, cudaStream_t s) {
+    check(cudaStreamSynchronize(s), "stream sync");
+    uint32_t st = 0;
+    check(cudaMemcpy(&st, dp.status.ptr, 4, cudaMemcpyDeviceToHost), "status read");
+    if (st) check(cudaMemset(dp.status.ptr, 0, 4), "status clear");
+    return st;
+}
+
+void raise_status(uint32_t st) {
+    if (st & qpk::kErrDomain) throw std::domain_error("redq: input exceeds q^(d+1), digits are not all below q");
+    if (st & qpk::kErrOutOfRange) throw std::out_of_range("floor_div_premul: numerator exceeds guaranteed range r_max");
+}
+
+void redq_device(DevicePlanCache& dp, const double* d_words, u64 n, uint8_t* d_out, cudaStream_t s) {
+    check(qpk::launch_redq_f64(dp.prm, d_words, n, d_out, dp.status.as<uint32_t>(), s), "redq launch");
+}
+
+// Host buffers in, host buffers out: H2D / kernel / D2H of consecutive
+// chunks on three streams so the copies of one chunk overlap the others.
+void redq_host(DevicePlanCache& dp, const double* h_words, u64 n, uint8_t* h_out) {
+    std::lock_guard<std::mutex> lock(dp.mu);
+    if (!dp.staging) dp.staging = std::make_unique<Staging>();
+    Staging& S = *dp.staging;
+    const u64 nd = dp.prm.d + 1;
+    const u64 chunk = u64(1) << 22;
+    for (u64 off = 0, c = 0; off < n; off += chunk, ++c) {
+        const int si = static_cast<int>(c % Staging::kStreams);
+        cudaStream_t s = S.streams[si];
+        const u64 cnt = std::min(chunk, n - off);
+        double* din = static_cast<double*>(S.in0[si].ensure(chunk * 8));
+        uint8_t* dout = static_cast<uint8_t*>(S.out[si].ensure(chunk * nd));
+        check(cudaMemcpyAsync(din, h_words + off, cnt * 8, cudaMemcpyHostToDevice, s), "H2D");
+        redq_device(dp, din, cnt, dout, s);
+        check(cudaMemcpyAsync(h_out + off * nd, dout, cnt * nd, cudaMemcpyDeviceToHost, s), "D2H");
+    }
+    for (auto s : S.streams) check(cudaStreamSynchronize(s), "sync");
+    raise_status(take_status(dp, S.streams[0]));
+}
+
+void redq_residues_batch(std::span<const double> words, const RedqPlan& plan, std::span<std::uint8_t> out,
+                         CostReport* cost) {
+    if (out.size() < words.size() * (plan.d + 1))
+        throw std::invalid_argument("redq_residues_batch: output span holds fewer than n*(d+1) residues");
+    DevicePlanCache& dp = detail::device_plan(plan);
+    redq_host(dp, words.data(), words.size(), out.data());
+    if (cost) *cost += detail::redq_batch_cost(plan, words.size());
+}
+
+// ------------------------------------------------------------ polymul plans
+PolymulPlan::PolymulPlan(const QadicParams& pr) : params(pr) {
+    const ValidationResult vr = validate(pr);
+    if (!vr.ok()) throw std::invalid_argument("dqt_mul_poly: " + vr.detail);
+    if (pr.k > static_cast<u32>(qpk::kMaxGfqK))
+        throw std::invalid_argument("qpack-b200 polymul: device path packs at most k = 4 coefficients");
+    if (pr.p > 256) throw std::invalid_argument("qpack-b200 polymul: residues are uint8, p must be <= 256");
+    redq = fqt_reduction_plan(pr, pr.k - 1);
+    DevicePlanCache& dp = detail::device_plan(redq);
+    P.rq = dp.prm;
+    P.k = pr.k;
+}
+
+void polymul_device(PolymulPlan& pl, const uint8_t* a, const uint8_t* b, u64 n, uint8_t* out, cudaStream_t s) {
+    DevicePlanCache& dp = detail::device_plan(pl.redq);
+    check(qpk::launch_polymul(pl.P, a, b, n, out, dp.status.as<uint32_t>(), s), "polymul launch");
+}
+
+void polymul_host(PolymulPlan& pl, const uint8_t* a, const uint8_t* b, u64 n, uint8_t* out) {
+    DevicePlanCache& dp = detail::device_plan(pl.redq);
+    std::lock_guard<std::mutex> lock(dp.mu);
+    if (!dp.staging) dp.staging = std::make_unique<Staging>();
+    Staging& S = *dp.staging;
+    const u64 k = pl.params.k, ko = 2 * k - 1, chunk = u64(1) << 22;
+    for (u64 off = 0, c = 0; off < n; off += chunk, ++c) {
+        const int si = static_cast<int>(c % Staging::kStreams);
+        cudaStream_t s = S.streams[si];
+        const u64 cnt = std::min(chunk, n - off);
+        auto* da = static_cast<uint8_t*>(S.in0[si].ensure(chunk * k));
+        auto* db = static_cast<uint8_t*>(S.in1[si].ensure(chunk * k));
+        auto* dout = static_cast<uint8_t*>(S.out[si].ensure(chunk * ko));
+        check(cudaMemcpyAsync(da, a + off * k, cnt * k, cudaMemcpyHostToDevice, s), "H2D");
+        check(cudaMemcpyAsync(db, b + off * k, cnt * k, cudaMemcpyHostToDevice, s), "H2D");
+        polymul_device(pl, da, db, cnt, dout, s);
+        check(cudaMemcpyAsync(out + off * ko, dout, cnt * ko, cudaMemcpyDeviceToHost, s), "D2H");
+    }
+    for (auto s : S.streams) check(cudaStreamSynchronize(s), "sync");
+    raise_status(take_status(dp, S.streams[0]));
+}
+
+CostReport polymul_cost(const PolymulPlan& pl, u64 n) {
+    // fqt_mul with one chunk per operand: one product, one REDQ per pair
+    CostReport c = detail::redq_batch_cost(pl.redq, n);
+    c.mul_add = n;
+    return c;
+}
+
+void polymul_batch(std::span<const std::uint8_t> a, std::span<const std::uint8_t> b, const QadicParams& params,
+                   std::span<std::uint8_t> out, CostReport* cost) {
+    static std::mutex mu;
+    static std::map<std::tuple<u64, u64, u32, u32, u32>, std::unique_ptr<PolymulPlan>> cache;
+    PolymulPlan* pl;
+    {
+        std::lock_guard<std::mutex> lock(mu);
+        auto& slot = cache[{params.p, params.q, params.k, params.n_q, params.m}];
+        if (!slot) slot = std::make_unique<PolymulPlan>(params);
+        pl = slot.get();
+    }
+    const u64 n = a.size() / params.k;
+    if (a.size() != b.size() || a.size() % params.k || out.size() < n * (2 * params.k - 1))
+        throw std::invalid_argument("polymul_batch: spans do not hold n records of k coefficients / 2k-1 residues");
+    polymul_host(*pl, a.data(), b.data(), n, out.data());
+    if (cost) *cost += polymul_cost(*pl, n);
+}
+
+// ------------------------------------------------------------------ GF(p^k)
+void gfq_mul_device(DeviceFieldCache& F, const uint8_t* a, const uint8_t* b, u64 n, uint8_t* out, int path,
+                    cudaStream_t s) {
+    qpk::GfqElemParams E = F.elem;
+    E.mode = path;
+    check(qpk::launch_gfq_elem(E, a, b, n, out, s), "gfq_mul launch");
+}
+
+void gfq_mul_host(DeviceFieldCache& F, const uint8_t* a, const uint8_t* b, u64 n, uint8_t* out, int path) {
+    std::lock_guard<std::mutex> lock(F.mu);
+    if (!F.staging) F.staging = std::make_unique<Staging>();
+    Staging& S = *F.staging;
+    const u64 k = F.elem.k, chunk = u64(1) << 22;
+    for (u64 off = 0, c = 0; off < n; off += chunk, ++c) {
+        const int si = static_cast<int>(c % Staging::kStreams);
+        cudaStream_t s = S.streams[si];
+        const u64 cnt = std::min(chunk, n - off);
+        auto* da = static_cast<uint8_t*>(S.in0[si].ensure(chunk * k));
+        auto* db = static_cast<uint8_t*>(S.in1[si].ensure(chunk * k));
+        auto* dout = static_cast<uint8_t*>(S.out[si].ensure(chunk * k));
+        check(cudaMemcpyAsync(da, a + off * k, cnt * k, cudaMemcpyHostToDevice, s), "H2D");
+        check(cudaMemcpyAsync(db, b + off * k, cnt * k, cudaMemcpyHostToDevice, s), "H2D");
+        gfq_mul_device(F, da, db, cnt, dout, path, s);
+        check(cudaMemcpyAsync(out + off * k, dout, cnt * k, cudaMemcpyDeviceToHost, s), "D2H");
+    }
+    for (auto s : S.streams) check(cudaStreamSynchronize(s), "sync");
+}
+
+void gfq_mul_batch(std::span<const std::uint8_t> a, std::span<const std::uint8_t> b, const GfqField& field,
+                   std::span<std::uint8_t> out, GfqPath path) {
+    const u64 k = field.k();
+    if (a.size() != b.size() || a.size() % k || out.size() < a.size())
+        throw std::invalid_argument("gfq_mul_batch: spans do not hold n records of k coefficients");
+    gfq_mul_host(detail::device_field(field), a.data(), b.data(), a.size() / k, out.data(), static_cast<int>(path));
+}
+
+void gfq_mul_rep_host(DeviceFieldCache& F, const uint32_t* a, const uint32_t* b, u64 n, uint32_t* out) {
+    std::lock_guard<std::mutex> lock(F.mu);
+    DevBuf& da = F.io_a;
+    DevBuf& db = F.io_b;
+    DevBuf& dc = F.io_c;
+    da.ensure(n * 4);
+    db.ensure(n * 4);
+    dc.ensure(n * 4);
+    check(cudaMemcpy(da.ptr, a, n * 4, cudaMemcpyHostToDevice), "H2D");
+    check(cudaMemcpy(db.ptr, b, n * 4, cudaMemcpyHostToDevice), "H2D");
+    check(qpk::launch_gfq_mul_rep(F.elem.group, da.as<uint32_t>(), db.as<uint32_t>(), n, dc.as<uint32_t>(), 0),
+          "gfq_mul_rep launch");
+    check(cudaMemcpy(out, dc.ptr, n * 4, cudaMemcpyDeviceToHost), "D2H");
+}
+
+void gfq_mul_batch(std::span<const GfqElt> a, std::span<const GfqElt> b, const GfqField& field,
+                   std::span<GfqElt> out) {
+    if (a.size() != b.size() || out.size() < a.size()) throw std::invalid_argument("gfq_mul_batch: length mismatch");
+    if (a.empty()) return;
+    for (const auto* v : {&a, &b})
+        for (const GfqElt& e : *v)
+            if (e.rep >= field.order()) throw std::out_of_range("gfq_mul_batch: rep outside the field");
+    gfq_mul_rep_host(detail::device_field(field), reinterpret_cast<const uint32_t*>(a.data()),
+                     reinterpret_cast<const uint32_t*>(b.data()), a.size(), reinterpret_cast<uint32_t*>(out.data()));
+}
+
+// ---- matmul ----
+namespace {
+u64 round_up(u64 v, u64 m) { return (v + m - 1) / m * m; }
+}  // namespace
+
+uint32_t resolve_chunk(const DeviceFieldCache& F, const GfqField& field, u64 K, uint32_t chunk) {
+    const u64 p = field.p(), k = field.k(), q = field.params().q;
+    const u64 unit = k * (p - 1) * (p - 1);
+    // after a re-pack every digit is <= p-1; `safe` more products keep it < q
+    const u64 safe = unit ? (q - 1 - (p - 1)) / unit : K;
+    (void)F;
+    if (chunk == 0) {
+        if (K <= field.params().n_q) return 0;  // one accumulation group: never reduce
+        chunk = static_cast<uint32_t>(std::min<u64>(safe, 1u << 30));
+    }
+    if (chunk > safe)
+        throw std::invalid_argument("gfq_matmul: chunk " + std::to_string(chunk) + " lets digit sums reach q (max " +
+                                    std::to_string(safe) + ")");
+    chunk -= chunk % 4;  // the kernel re-packs at 4-step granularity
+    if (chunk == 0) throw std::invalid_argument("gfq_matmul: field admits fewer than 4 products between reductions");
+    return chunk;
+}
+
+// A, B, C device pointers: coefficient records (reps when `reps`)
+void gfq_matmul_device(DeviceFieldCache& F, const GfqField& field, const void* A, const void* B, u64 m, u64 K, u64 n,
+                       uint32_t chunk, void* C, bool reps, cudaStream_t s) {
+    if (m == 0 || n == 0) return;
+    const u64 mp = round_up(m, 128), np = round_up(n, 128), kp = round_up(std::max<u64>(K, 1), 16);
+    auto* at = static_cast<double*>(F.ws_a.ensure(kp * mp * 8));
+    auto* bt = static_cast<double*>(F.ws_b.ensure(kp * np * 8));
+    if (mp != m || kp != K) check(cudaMemsetAsync(at, 0, kp * mp * 8, s), "memset");
+    if (np != n || kp != K) check(cudaMemsetAsync(bt, 0, kp * np * 8, s), "memset");
+    if (reps) {
+        check(qpk::launch_pack_reps(F.mm.fval, F.mm.order, static_cast<const uint32_t*>(A), m, K, at, mp, true, s),
+              "pack A");
+        check(qpk::launch_pack_reps(F.mm.fval, F.mm.order, static_cast<const uint32_t*>(B), K, n, bt, np, false, s),
+              "pack B");
+    } else {
+        check(qpk::launch_pack_coeffs(F.mm.p, F.mm.k, F.mm.qd, static_cast<const uint8_t*>(A), m, K, at, mp, true, s),
+              "pack A");
+        check(qpk::launch_pack_coeffs(F.mm.p, F.mm.k, F.mm.qd, static_cast<const uint8_t*>(B), K, n, bt, np, false, s),
+              "pack B");
+    }
+    qpk::GfqMatmulParams M = F.mm;
+    M.chunk = resolve_chunk(F, field, K, chunk);
+    check(qpk::launch_gfq_matmul(M, at, bt, m, n, kp, mp, np, reps ? nullptr : static_cast<uint8_t*>(C),
+                                 reps ? static_cast<uint32_t*>(C) : nullptr, s),
+          "gfq_matmul launch");
+}
+
+void gfq_matmul_host(DeviceFieldCache& F, const GfqField& field, const void* A, const void* B, u64 m, u64 K, u64 n,
+                     uint32_t chunk, void* C, bool reps) {
+    std::lock_guard<std::mutex> lock(F.mu);
+    const u64 es = reps ? 4 : field.k();
+    auto* da = F.io_a.ensure(m * K * es);
+    auto* db = F.io_b.ensure(K * n * es);
+    auto* dc = F.io_c.ensure(m * n * es);
+    check(cudaMemcpy(da, A, m * K * es, cudaMemcpyHostToDevice), "H2D");
+    check(cudaMemcpy(db, B, K * n * es, cudaMemcpyHostToDevice), "H2D");
+    gfq_matmul_device(F, field, da, db, m, K, n, chunk, dc, reps, 0);
+    check(cudaMemcpy(C, dc, m * n * es, cudaMemcpyDeviceToHost), "D2H");
+}
+
+CostReport matmul_cost(const GfqField& field, u64 m, u64 K, u64 n) {
+    // reference grouping (gfq.cpp:346-385): ceil(K/n_q) groups per entry;
+    // table_accesses counts the operand and L/H lookups, not the Zech adds
+    // whose count depends on intermediate zeros
+    const u64 groups = K ? (K + field.params().n_q - 1) / field.params().n_q : 0;
+    CostReport c;
+    c.mul_add = m * n * K;
+    c.divisions = c.reduction_calls = m * n * groups;
+    c.table_accesses = 2 * m * n * K + 2 * m * n * groups;
+    return c;
+}
+
+void gfq_matmul_coeffs(std::span<const std::uint8_t> A, std::span<const std::uint8_t> B, std::size_t m, std::size_t K,
+                       std::size_t n, const GfqField& field, std::span<std::uint8_t> C, std::uint32_t chunk,
+                       CostReport* cost) {
+    const u64 k = field.k();
+    if (A.size() != m * K * k || B.size() != K * n * k || C.size() < m * n * k)
+        throw std::invalid_argument("gfq_matmul_coeffs: span sizes do not match m x K x k / K x n x k / m x n x k");
+    gfq_matmul_host(detail::device_field(field), field, A.data(), B.data(), m, K, n, chunk, C.data(), false);
+    if (cost) *cost += matmul_cost(field, m, K, n);
+}
+
+}  // namespace qpack::gpu
+
+namespace qpack {
+
+GfqMatrix gfq_matmul(const GfqMatrix& a, const GfqMatrix& b, const GfqField& field, CostReport* cost) {
+    if (a.cols != b.rows) throw std::invalid_argument("gfq_matmul: inner dimensions differ");
+    GfqMatrix c = GfqMatrix::zero(field, a.rows, b.cols);
+    if (a.rows == 0 || b.cols == 0) return c;
+    if (a.cols == 0) return c;
+    for (const auto* mtx : {&a, &b})
+        for (const GfqElt& e : mtx->data)
+            if (e.rep >= field.order()) throw std::out_of_range("gfq_matmul: rep outside the field");
+    gpu::gfq_matmul_host(detail::device_field(field), field, a.data.data(), b.data.data(), a.rows, a.cols, b.cols, 0,
+                         c.data.data(), true);
+    if (cost) *cost += gpu::matmul_cost(field, a.rows, a.cols, b.cols);
+    return c;
+}
+
+}  // namespace qpack

@@ -1,0 +1,45 @@
+// Internal GPU entry points shared by the C++ API (gpu_api.cpp) and the
+// C-ABI (capi.cpp).  Device-pointer variants are asynchronous on `s`;
+// *_host variants take host buffers and return when results are visible.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "device_state.hpp"
+#include "qpack/counters.hpp"
+#include "qpack/gfq.hpp"
+#include "qpack/params.hpp"
+#include "qpack/redq.hpp"
+
+namespace qpack::gpu {
+
+uint32_t take_status(detail::DevicePlanCache& dp, cudaStream_t s);
+void raise_status(uint32_t st);
+
+void redq_device(detail::DevicePlanCache& dp, const double* d_words, u64 n, uint8_t* d_out, cudaStream_t s);
+void redq_host(detail::DevicePlanCache& dp, const double* h_words, u64 n, uint8_t* h_out);
+
+// fqt_mul / dqt_mul_poly over a batch of single-chunk pairs
+struct PolymulPlan {
+    QadicParams params;
+    RedqPlan redq;  // fqt_reduction_plan(params, k-1)
+    qpk::PolymulParams P{};
+    explicit PolymulPlan(const QadicParams& pr);
+};
+void polymul_device(PolymulPlan& pl, const uint8_t* a, const uint8_t* b, u64 n, uint8_t* out, cudaStream_t s);
+void polymul_host(PolymulPlan& pl, const uint8_t* a, const uint8_t* b, u64 n, uint8_t* out);
+CostReport polymul_cost(const PolymulPlan& pl, u64 n);
+
+void gfq_mul_device(detail::DeviceFieldCache& F, const uint8_t* a, const uint8_t* b, u64 n, uint8_t* out, int path,
+                    cudaStream_t s);
+void gfq_mul_host(detail::DeviceFieldCache& F, const uint8_t* a, const uint8_t* b, u64 n, uint8_t* out, int path);
+void gfq_mul_rep_host(detail::DeviceFieldCache& F, const uint32_t* a, const uint32_t* b, u64 n, uint32_t* out);
+
+uint32_t resolve_chunk(const detail::DeviceFieldCache& F, const GfqField& field, u64 K, uint32_t chunk);
+void gfq_matmul_device(detail::DeviceFieldCache& F, const GfqField& field, const void* A, const void* B, u64 m, u64 K,
+                       u64 n, uint32_t chunk, void* C, bool reps, cudaStream_t s);
+void gfq_matmul_host(detail::DeviceFieldCache& F, const GfqField& field, const void* A, const void* B, u64 m, u64 K,
+                     u64 n, uint32_t chunk, void* C, bool reps);
+CostReport matmul_cost(const GfqField& field, u64 m, u64 K, u64 n);
+
+}  // namespace qpack::gpu

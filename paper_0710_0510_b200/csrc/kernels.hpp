@@ -1,0 +1,114 @@
+// Host-visible parameter blocks and launchers for the sm_100a kernels.
+// Everything here is plain data: the C-ABI (capi.cpp) fills these from the
+// host-side plan/field objects and calls the launchers.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace qpk {
+
+constexpr int kMaxFastDigits = 8;   // templated fast path: d+1 <= 8
+constexpr int kMaxDigits = 64;      // generic path
+constexpr int kMaxGfqK = 4;         // coefficient records up to 4 bytes
+
+// status bits OR-ed into a device word by the kernels
+enum : uint32_t {
+    kErrDomain = 1u,      // word outside [0, min(q^(d+1), 2^53))  (redq.cpp:22-29, dqt.cpp:96-97)
+    kErrOutOfRange = 2u,  // premultiplied floor outside r_max     (fpdiv.cpp:133-135)
+};
+
+// One REDQ plan as the device sees it (RedqPlan, redq.hpp:46-61).
+struct RedqParams {
+    uint32_t p;
+    uint32_t d;           // highest digit index
+    uint32_t qbits;       // log2(q) when q is a power of two, else 0
+    uint32_t neg_q;       // (p - q mod p) mod p
+    uint32_t window;      // 0 = direct/identity correction, else table window (2..4)
+    uint32_t radix;       // table index radix (p or 2^ceil(log2 p))
+    uint32_t n_entries;   // radix^window
+    uint32_t mod_magic;   // ceil(2^32 / p), exact mod for t < 2^16 when p <= 256
+    uint32_t float_mode;  // RedqMode::float_premul
+    double inv_p;         // ReciprocalDivisor(p).inv_up
+    double r_max;         // premul exactness bound (as an exact double)
+    double limit;         // min(q^(d+1), 2^53): words must lie below
+    uint64_t q;
+    uint64_t qpow[kMaxDigits];
+    double inv_q[kMaxDigits];  // ReciprocalDivisor(q^i).inv_up, general q
+    const uint32_t* table;     // device table, byte-packed windows (mu_j in byte j)
+};
+
+// Batched small polynomial product (config 1): pack, fp64 product, REDQ.
+struct PolymulParams {
+    RedqParams rq;  // d = 2k-2
+    uint32_t k;
+};
+
+// GF(p^k) elementwise product (config 3).
+struct GfqElemParams {
+    RedqParams rq;          // d = 2k-2, mode float
+    uint32_t k, p, order, group, lh_radix;
+    double qd;              // q as double (Horner)
+    const uint32_t* lc;     // lh^k: corrected low half  -> coefficient bytes
+    const uint32_t* hc;     // lh^k: corrected high half -> coefficient bytes (reduced by the modulus)
+    const uint32_t* log;    // p^k: coefficient index -> rep
+    const uint32_t* alog;   // p^k: rep -> coefficient bytes (sentinel -> 0)
+    uint32_t tables_words;  // lc+hc+log+alog total (for smem staging)
+    int mode;               // 0 packed (DQT/REDQ/L-H), 1 dlog/Zech
+};
+
+// GF(p^k) matrix product (configs 4/5).
+struct GfqMatmulParams {
+    RedqParams rq;        // d = 2k-2, digits of one accumulated word
+    uint32_t k, p, order, group, lh_radix;
+    uint32_t chunk;       // delayed REDQ re-pack every `chunk` K-steps (0 = never)
+    double qd;
+    const uint32_t* lc;   // as GfqElemParams
+    const uint32_t* hc;
+    const uint32_t* log;  // for rep output
+    const double* fval;   // rep -> q-adic evaluation (float_eval, gfq.cpp:194-207)
+};
+
+// ---- launchers (return cudaError_t of the launch) ----
+cudaError_t launch_redq_f64(const RedqParams& P, const double* words, uint64_t n, uint8_t* out,
+                            uint32_t* status, cudaStream_t s);
+cudaError_t launch_polymul(const PolymulParams& P, const uint8_t* a, const uint8_t* b, uint64_t n,
+                           uint8_t* out, uint32_t* status, cudaStream_t s);
+cudaError_t launch_gfq_elem(const GfqElemParams& P, const uint8_t* a, const uint8_t* b, uint64_t n,
+                            uint8_t* out, cudaStream_t s);
+cudaError_t launch_gfq_mul_rep(uint32_t group, const uint32_t* a, const uint32_t* b, uint64_t n, uint32_t* out,
+                               cudaStream_t s);
+
+// DQT pack of coefficient records into q-adic doubles (K1a): src is
+// rows x cols x k bytes; dst element (r, c) goes to dst[c*ld + r] when
+// `transpose`, else dst[r*ld + c].  dst must be pre-zeroed for padding.
+cudaError_t launch_pack_coeffs(uint32_t p, uint32_t k, double qd, const uint8_t* src, uint64_t rows,
+                               uint64_t cols, double* dst, uint64_t ld, bool transpose, cudaStream_t s);
+// Zech/dlog tabulated pack (K1b): reps -> float_eval(rep) via a smem table.
+cudaError_t launch_pack_reps(const double* fval, uint32_t order, const uint32_t* src, uint64_t rows,
+                             uint64_t cols, double* dst, uint64_t ld, bool transpose, cudaStream_t s);
+
+// K4: C = A*B on packed operands.  at is K x m_pad (A transposed), b is
+// K x n_pad, both zero padded (m_pad, n_pad multiples of 128, K_pad of 16).
+// Output either coefficient bytes (m x n x k) or reps (m x n u32).
+cudaError_t launch_gfq_matmul(const GfqMatmulParams& P, const double* at, const double* b, uint64_t m,
+                              uint64_t n, uint64_t K_pad, uint64_t m_pad, uint64_t n_pad, uint8_t* out_coeffs,
+                              uint32_t* out_reps, cudaStream_t s);
+
+// Synthetic inputs: out[i] = SplitMix64(seed) draw (start+i+1) mod bound.
+cudaError_t launch_gen_draws(uint64_t seed, uint64_t start, uint64_t count, uint32_t bound, uint8_t* out,
+                             cudaStream_t s);
+// q-adic words: word i = sum_j draw(i*(d+1)+j+1 mod q) * q^(d-j) (first draw = top digit)
+cudaError_t launch_gen_words(uint64_t seed, uint64_t n, uint64_t q, uint32_t d, double* out, cudaStream_t s);
+// record pairs: a[i] = draws 2k*i+1..2k*i+k, b[i] = the next k
+cudaError_t launch_gen_pairs(uint64_t seed, uint64_t n, uint32_t k, uint32_t bound, uint8_t* a, uint8_t* b,
+                             cudaStream_t s);
+
+// fp64 peak probes (roofline denominators): returns flop count per launch
+cudaError_t launch_probe_dfma(double* sink, int iters, uint64_t* flops, cudaStream_t s);
+cudaError_t launch_probe_dmma(double* sink, int iters, uint64_t* flops, cudaStream_t s);
+
+int num_sms();
+
+}  // namespace qpk

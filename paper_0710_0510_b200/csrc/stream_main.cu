@@ -1,0 +1,181 @@
+// Non-templated streaming kernels (generic-width REDQ, input generators,
+// rep products), the launch dispatchers, and the device SM count.  The
+// templated TMA pipeline lives in stream_kernels.cuh and is instantiated in
+// stream_inst.cu.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+
+#include "device_common.cuh"
+#include "kernels.hpp"
+#include "stream_inst.hpp"
+
+namespace qpk {
+
+namespace {
+
+int g_num_sms = 0;
+
+__device__ __forceinline__ uint32_t mod_small_g(uint32_t t, uint32_t p, uint32_t magic) {
+    return t - p * __umulhi(t, magic);
+}
+
+__device__ __forceinline__ void report_g(uint32_t err, uint32_t* status) {
+    err = __reduce_or_sync(0xffffffffu, err);
+    if (err && (threadIdx.x & 31) == 0 && status) atomicOr(status, err);
+}
+
+// Generic REDQ for d+1 > kMaxFastDigits: one word per thread, runtime loops.
+__global__ void redq_generic_kernel(const RedqParams P, const double* __restrict__ words, uint64_t n,
+                                    uint8_t* __restrict__ out, uint32_t* status) {
+    uint32_t err = 0;
+    const uint32_t nd = P.d + 1;
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
+        const double w = words[i];
+        double r = trunc(w);
+        if (!(w >= 0.0 && r < P.limit)) {
+            err |= kErrDomain;
+            r = 0.0;
+        }
+        const bool premul = r <= P.r_max;
+        const uint64_t rb = __double2ull_rz(r);
+        const uint64_t rop = premul ? floor_div_premul(r, P.inv_p) : rb / P.p;
+        uint32_t u[kMaxDigits];
+        for (uint32_t j = 0; j < nd; ++j) {
+            uint64_t x, y;
+            if (P.qbits) {
+                x = rb >> (P.qbits * j);
+                y = rop >> (P.qbits * j);
+            } else {
+                x = rb / P.qpow[j];
+                y = rop / P.qpow[j];
+            }
+            u[j] = static_cast<uint32_t>(x) - P.p * static_cast<uint32_t>(y);
+        }
+        // direct correction (results equal the tabulated one, redq tests)
+        if (P.neg_q)
+            for (uint32_t j = 0; j + 1 < nd; ++j) u[j] = mod_small_g(u[j] + P.neg_q * u[j + 1], P.p, P.mod_magic);
+        for (uint32_t j = 0; j < nd; ++j) out[i * nd + j] = static_cast<uint8_t>(u[j]);
+    }
+    report_g(err, status);
+}
+
+__global__ void gfq_mul_rep_kernel(uint32_t group, const uint32_t* __restrict__ a, const uint32_t* __restrict__ b,
+                                   uint64_t n, uint32_t* __restrict__ out) {
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
+        const uint32_t x = a[i], y = b[i];
+        uint32_t r = x + y;
+        if (r >= group) r -= group;
+        out[i] = (x == group || y == group) ? group : r;
+    }
+}
+
+// ------------------------------------------------------------- generators
+__global__ void gen_draws_kernel(uint64_t seed, uint64_t start, uint64_t count, uint32_t bound, uint8_t* out) {
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
+         i += uint64_t(gridDim.x) * blockDim.x)
+        out[i] = static_cast<uint8_t>(splitmix_at(seed, start + i + 1) % bound);
+}
+
+__global__ void gen_words_kernel(uint64_t seed, uint64_t n, uint64_t q, uint32_t d, double* out) {
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
+        uint64_t r = 0;
+        for (uint32_t j = 0; j <= d; ++j) r = r * q + splitmix_at(seed, i * (d + 1) + j + 1) % q;
+        out[i] = static_cast<double>(r);
+    }
+}
+
+__global__ void gen_pairs_kernel(uint64_t seed, uint64_t n, uint32_t k, uint32_t bound, uint8_t* a, uint8_t* b) {
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n * k;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t rec = i / k, c = i % k;
+        a[i] = static_cast<uint8_t>(splitmix_at(seed, rec * 2 * k + c + 1) % bound);
+        b[i] = static_cast<uint8_t>(splitmix_at(seed, rec * 2 * k + k + c + 1) % bound);
+    }
+}
+
+unsigned grid_for(uint64_t n) {
+    return static_cast<unsigned>(std::min<uint64_t>((n + 255) / 256, uint64_t(num_sms()) * 16));
+}
+
+}  // namespace
+
+int num_sms() {
+    if (!g_num_sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+        if (g_num_sms <= 0) g_num_sms = 148;
+    }
+    return g_num_sms;
+}
+
+cudaError_t launch_redq_f64(const RedqParams& P, const double* words, uint64_t n, uint8_t* out, uint32_t* status,
+                            cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    switch (P.d + 1) {
+        case 1: return redq_launch_nd1(P, words, n, out, status, s);
+        case 2: return redq_launch_nd2(P, words, n, out, status, s);
+        case 3: return redq_launch_nd3(P, words, n, out, status, s);
+        case 4: return redq_launch_nd4(P, words, n, out, status, s);
+        case 5: return redq_launch_nd5(P, words, n, out, status, s);
+        case 6: return redq_launch_nd6(P, words, n, out, status, s);
+        case 7: return redq_launch_nd7(P, words, n, out, status, s);
+        case 8: return redq_launch_nd8(P, words, n, out, status, s);
+        default:
+            redq_generic_kernel<<<grid_for(n), 256, 0, s>>>(P, words, n, out, status);
+            return cudaGetLastError();
+    }
+}
+
+cudaError_t launch_polymul(const PolymulParams& P, const uint8_t* a, const uint8_t* b, uint64_t n, uint8_t* out,
+                           uint32_t* status, cudaStream_t s) {
+    switch (P.k) {
+        case 1: return polymul_launch_k1(P, a, b, n, out, status, s);
+        case 2: return polymul_launch_k2(P, a, b, n, out, status, s);
+        case 3: return polymul_launch_k3(P, a, b, n, out, status, s);
+        case 4: return polymul_launch_k4(P, a, b, n, out, status, s);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+cudaError_t launch_gfq_elem(const GfqElemParams& P, const uint8_t* a, const uint8_t* b, uint64_t n, uint8_t* out,
+                            cudaStream_t s) {
+    switch (P.k) {
+        case 1: return gfq_elem_launch_k1(P, a, b, n, out, s);
+        case 2: return gfq_elem_launch_k2(P, a, b, n, out, s);
+        case 3: return gfq_elem_launch_k3(P, a, b, n, out, s);
+        case 4: return gfq_elem_launch_k4(P, a, b, n, out, s);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+cudaError_t launch_gfq_mul_rep(uint32_t group, const uint32_t* a, const uint32_t* b, uint64_t n, uint32_t* out,
+                               cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    gfq_mul_rep_kernel<<<grid_for(n), 256, 0, s>>>(group, a, b, n, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_gen_draws(uint64_t seed, uint64_t start, uint64_t count, uint32_t bound, uint8_t* out,
+                             cudaStream_t s) {
+    if (count == 0) return cudaSuccess;
+    gen_draws_kernel<<<grid_for(count), 256, 0, s>>>(seed, start, count, bound, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_gen_words(uint64_t seed, uint64_t n, uint64_t q, uint32_t d, double* out, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    gen_words_kernel<<<grid_for(n), 256, 0, s>>>(seed, n, q, d, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_gen_pairs(uint64_t seed, uint64_t n, uint32_t k, uint32_t bound, uint8_t* a, uint8_t* b,
+                             cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    gen_pairs_kernel<<<grid_for(n * k), 256, 0, s>>>(seed, n, k, bound, a, b);
+    return cudaGetLastError();
+}
+
+}  // namespace qpk
