@@ -1,0 +1,409 @@
+#!/usr/bin/env python
+"""Benchmark of the q-adic transform pipeline on B200 (one JSON line).
+
+Headline workload (BASELINE.json configs[1], "C2"): batched REDQ of 2^26 fp64
+words (7 digits at q = 2^7, p = 5, float_premul + window-4 correction table)
+per GPU per step -> 7 residues/word as uint8.  Multi-GPU: one process per GPU,
+each rank reduces its own 2^26-word shard of the seeded stream (weak scaling,
+no data-path collective); time = max over ranks.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+value     residues/s over all ranks, inputs resident in HBM (CUDA events on
+          the launching stream, K back-to-back steps, barrier + sync around)
+e2e       same metric through the C-ABI host entry point
+          (qpk_redq_residues_f64_host): pinned host words in, H2D + kernel +
+          D2H inside the timed region every step
+roofline  HBM: 15 B/word algorithmic (8 in + 7 out) / kernel time vs the
+          measured copy bandwidth in MEASURED_PEAKS.json
+cpu_baseline  the reference's own CPU path (oracle/_ref, built from
+          /root/reference unmodified) on a bounded sample, all host threads
+secondary the other BASELINE configs (C1, C3 both paths, C4, C5) measured
+          the same way with their own rooflines (N = 1 only)
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "redq_residues_per_s"
+UNIT = "residues/s"
+N_WORDS = 1 << 26
+ND = 7
+ALGO_BYTES_PER_WORD = 8 + ND
+WORKLOAD = "C2 batched REDQ: 2^26 fp64 words/GPU, p=5, q=2^7, d=6, float_premul + window-4 table -> 7 uint8 residues/word"
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(kernel_key):
+    """dram bytes per launch of `kernel_key` from the committed ncu summary."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+            s = json.load(f)
+        return s[kernel_key]["dram_bytes_per_launch"]
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed regions."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self.proc = None
+        self.active = False
+        self.t = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.t = threading.Thread(target=self._read, daemon=True)
+        self.t.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            if self.active:
+                self.samples.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > i + 2 and s[i + 2].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------- reference
+def run_reference(args, rank):
+    """The reference's own CPU implementation (oracle/_ref when built here,
+    else the C restatement) on the host cores, same metric/config."""
+    import numpy as np
+
+    import oracle as O
+
+    threads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    use_ref = O.ref() is not None
+    kind = "reference" if use_ref else "port"
+
+    def words_for(n):
+        dr = O.draws(0x07100510 + 2, n * ND, 128).reshape(n, ND).astype(np.uint64)
+        w = np.zeros(n, np.uint64)
+        for j in range(ND):
+            w = w * np.uint64(128) + dr[:, j]
+        return w.astype(np.float64)
+
+    def run(words):
+        if use_ref:
+            out, ns, _ = O.ref_redq_f64(5, 128, 6, words, float_mode=True, window=4, threads=threads)
+            return ns * 1e-9
+        t0 = time.perf_counter()
+        O.redq_f64(5, 128, 6, words, float_mode=True, window=4)
+        return time.perf_counter() - t0
+
+    # size each step to ~1.5 s of wall time so K+W steps end within minutes
+    probe = words_for(1 << 18)
+    rate = (1 << 18) / max(run(probe), 1e-6)
+    sample = int(min(N_WORDS, max(1 << 16, rate * 1.5)))
+    words = words_for(sample)
+    for _ in range(args.warmup):
+        run(words)
+    ts = [run(words) for _ in range(args.steps)]
+    t = sum(ts) / len(ts)
+    value = ND * sample / t
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded SplitMix64)",
+        "config": {"workload": WORKLOAD, "sample_words_per_step": sample},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads if use_ref else 1, "kind": kind,
+                         "sample": f"{sample} words of the C2 stream per step (redq_residues_into, float_premul + "
+                                   f"window-4 table; -O2 asserts armed as shipped)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+def cpu_baseline_leg():
+    """Reference CPU path on the host cores, bounded sample (~5 s)."""
+    import numpy as np
+
+    import oracle as O
+    threads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    if O.ref() is None:
+        kind, threads_used = "port", 1
+    else:
+        kind, threads_used = "reference", threads
+
+    def words_for(n):
+        dr = O.draws(0x07100510 + 2, n * ND, 128).reshape(n, ND).astype(np.uint64)
+        w = np.zeros(n, np.uint64)
+        for j in range(ND):
+            w = w * np.uint64(128) + dr[:, j]
+        return w.astype(np.float64)
+
+    def run(words):
+        if kind == "reference":
+            _, ns, _ = O.ref_redq_f64(5, 128, 6, words, float_mode=True, window=4, threads=threads_used)
+            return ns * 1e-9
+        t0 = time.perf_counter()
+        O.redq_f64(5, 128, 6, words, float_mode=True, window=4)
+        return time.perf_counter() - t0
+
+    rate = (1 << 18) / max(run(words_for(1 << 18)), 1e-6)
+    sample = int(min(N_WORDS, max(1 << 16, rate * 4.0)))
+    t = run(words_for(sample))
+    return {"value": ND * sample / t, "unit": UNIT, "cores": threads_used, "kind": kind,
+            "sample": f"{sample} words of the C2 stream (redq_residues_into, float_premul + window-4 table, "
+                      f"reference built -O2 with asserts armed as shipped), {threads_used} threads"}
+
+
+# ---------------------------------------------------------------------- ours
+def run_ours(args, rank, world, local_rank):
+    import numpy as np
+    import torch
+
+    import paper_0710_0510_b200 as Q
+
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier(device_ids=[local_rank])
+
+    from paper_0710_0510_b200.sharding import max_over_ranks as _mor
+    from paper_0710_0510_b200.sharding import weak_shard
+
+    def max_over_ranks(x):
+        return _mor(x, dist, dev)
+
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+
+    # inputs: this rank's shard of the seeded C2 stream, generated on device
+    first, count = weak_shard(rank, N_WORDS)
+    w = torch.empty(count, dtype=torch.float64, device=dev)
+    Q.gen_words(Q.C2.seed, count, 128, 6, w, first=first)
+    out = torch.empty((N_WORDS, ND), dtype=torch.uint8, device=dev)
+    plan = Q.RedqPlan(5, 128, 6, Q.FLOAT_PREMUL).attach_correction(4)
+
+    # ---- value: resident inputs, one REDQ kernel per step
+    for _ in range(args.warmup):
+        plan.residues(w, out=out)
+    plan.sync()
+    barrier()
+    clocks.active = True
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        plan.residues(w, out=out)
+    e1.record()
+    barrier()
+    clocks.active = False
+    plan.sync()
+    ms_total = max_over_ranks(e0.elapsed_time(e1))
+    ms_step = ms_total / args.steps
+    value = world * N_WORDS * ND / (ms_step * 1e-3)
+    kernel_ms = e0.elapsed_time(e1) / args.steps  # this rank's kernel (1 launch / step)
+
+    # ---- e2e: host buffers through the C-ABI host entry point
+    hw = torch.empty(N_WORDS, dtype=torch.float64, pin_memory=True)
+    hw.copy_(w)
+    ho = torch.empty((N_WORDS, ND), dtype=torch.uint8, pin_memory=True)
+    hw_np, ho_np = hw.numpy(), ho.numpy()
+    e2e_steps = max(3, min(args.steps, 10))
+    for _ in range(max(1, min(args.warmup, 3))):
+        plan.residues(hw_np, out=ho_np)
+    barrier()
+    clocks.active = True
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        plan.residues(hw_np, out=ho_np)
+    t_e2e = time.perf_counter() - t0
+    clocks.active = False
+    t_e2e = max_over_ranks(t_e2e) / e2e_steps
+    e2e_value = world * N_WORDS * ND / t_e2e
+    # the e2e output must equal the resident run's
+    assert np.array_equal(ho_np[:1 << 20], out[:1 << 20].cpu().numpy()), "e2e output differs from device output"
+
+    peak, peak_src = measured_peaks()
+    achieved = ALGO_BYTES_PER_WORD * N_WORDS / (kernel_ms * 1e-3) / 1e9
+    traffic = ncu_traffic("redq_c2")
+
+    secondary = None
+    if world == 1 and not args.no_secondary:
+        clocks.active = True
+        secondary = measure_secondary(Q, torch, dev)
+        clocks.active = False
+    del w, out, hw, ho
+    clocks.stop()
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded SplitMix64, generated on device)",
+        "config": {"workload": WORKLOAD, "words_per_gpu": N_WORDS, "global_words": world * N_WORDS,
+                   "l2": "inputs larger than L2 (512 MiB in + 448 MiB out per GPU per step)",
+                   "parallelism": f"dp{world} (independent word shards, no collective)"},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": world * N_WORDS * 8,
+                "d2h_bytes_per_step": world * N_WORDS * ND, "steps": e2e_steps,
+                "path": "qpk_redq_residues_f64_host (pinned host buffers, 3-stream chunked H2D/kernel/D2H)"},
+        "gpu_launches": args.steps,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "peak_source": peak_src,
+                     "frac_of_nominal_8TBps": achieved / 8000.0,
+                     "kernel": "stream_tma_kernel<RedqOp<7,pow2,w4>>",
+                     "algorithmic_bytes_per_launch": ALGO_BYTES_PER_WORD * N_WORDS},
+        "clocks": clocks.summary(),
+    }
+    if secondary is not None:
+        line["secondary"] = secondary
+    return line
+
+
+def measure_secondary(Q, torch, dev):
+    """C1, C3 (both paths), C4, C5 on one GPU; CUDA-event timed."""
+    res = {}
+    peak_hbm, _ = measured_peaks()
+    fp64_peak = Q.probe_fp64(1, 8192)
+    res["fp64_peaks_tflops"] = {"dmma_probe": fp64_peak, "dfma_probe": Q.probe_fp64(0, 8192), "nominal": 37.0}
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def time_it(fn, reps, warm=3, cold=True):
+        for _ in range(warm):
+            fn()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(reps):
+            if cold:
+                flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn()
+            e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        return statistics.median(ts)
+
+    # C1: 2^20 polynomial pairs, 15.7 MB (L2-resident when hot)
+    n1 = Q.C1.n
+    a1 = torch.empty(n1 * 4, dtype=torch.uint8, device=dev)
+    b1 = torch.empty_like(a1)
+    Q.gen_pairs(Q.C1.seed, n1, 4, 3, a1, b1)
+    o1 = torch.empty((n1, 7), dtype=torch.uint8, device=dev)
+    pm = Q.PolymulPlan(3, 32, 4, 1)
+    cold = time_it(lambda: pm(a1, b1, out=o1), 20)
+    hot = time_it(lambda: pm(a1, b1, out=o1), 20, cold=False)
+    pm.sync()
+    res["c1_polymul"] = {"pairs_per_s_cold": n1 / (cold * 1e-3), "ms_cold": cold, "ms_hot": hot,
+                         "GBps_cold": 15 * n1 / (cold * 1e-3) / 1e9, "frac_hbm_cold": 15 * n1 / (cold * 1e-3) / 1e9 / peak_hbm}
+    # C3: 2^24 GF(7^3) products
+    n3 = Q.C3.n
+    a3 = torch.empty(n3 * 3, dtype=torch.uint8, device=dev)
+    b3 = torch.empty_like(a3)
+    Q.gen_pairs(Q.C3.seed, n3, 3, 7, a3, b3)
+    o3 = torch.empty((n3, 3), dtype=torch.uint8, device=dev)
+    f3 = Q.GfqField(7, 3, 256)
+    for path, name in ((0, "packed"), (1, "dlog")):
+        ms = time_it(lambda: f3.mul_batch(a3, b3, path, out=o3), 20)
+        gbs = 9 * n3 / (ms * 1e-3) / 1e9
+        res[f"c3_gfq_mul_{name}"] = {"products_per_s": n3 / (ms * 1e-3), "ms": ms, "GBps": gbs,
+                                     "frac_hbm": gbs / peak_hbm}
+    del a3, b3, o3
+    # C4, C5: GF(p^k) matrix products (pack + contraction), GF ops/s = 2 n^3 / t
+    for cfg in (Q.C4, Q.C5):
+        nn, k = cfg.n, cfg.k
+        A = torch.empty(nn * nn * k, dtype=torch.uint8, device=dev)
+        B = torch.empty_like(A)
+        Q.gen_draws(cfg.seed, nn * nn * k, 3, A, start=0)
+        Q.gen_draws(cfg.seed, nn * nn * k, 3, B, start=nn * nn * k)
+        f = Q.GfqField(3, k, cfg.q)
+        Cm = torch.empty((nn, nn, k), dtype=torch.uint8, device=dev)
+        ms = time_it(lambda: f.matmul(A, B, nn, nn, nn, cfg.chunk, out=Cm), 5, warm=2, cold=False)
+        tf = 2 * nn ** 3 / (ms * 1e-3) / 1e12
+        res[f"c{cfg.cid}_gfq_matmul"] = {"gf_ops_per_s": 2 * nn ** 3 / (ms * 1e-3), "ms": ms, "tflops": tf,
+                                          "frac_dmma_probe": tf / fp64_peak, "frac_nominal_37": tf / 37.0,
+                                          "n": nn, "chunk": cfg.chunk}
+        del A, B, Cm
+    return res
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-secondary", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        if rank == 0:
+            run_reference(args, rank)
+        return
+
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    line = run_ours(args, rank, world, local_rank)
+    if rank == 0:
+        if world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline_leg()
+        print(json.dumps(line))
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

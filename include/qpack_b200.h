@@ -147,9 +147,11 @@ QPK_API qpk_status qpk_gfq_matmul_rep_host(qpk_field f, const uint32_t* A, const
 /* out[i] = SplitMix64(seed): draw number start+i+1, mod bound (below()) */
 QPK_API qpk_status qpk_gen_draws(uint64_t seed, uint64_t start, uint64_t count, uint32_t bound, uint8_t* out,
                                  void* stream);
-/* word i = sum_j below(q) * q^(d-j), draws i*(d+1)+1 .. (first draw = top digit;
- * the acceptance suite's random_digit_safe_word, acceptance.cpp:52-56) */
-QPK_API qpk_status qpk_gen_words(uint64_t seed, uint64_t n, uint64_t q, uint32_t d, double* out, void* stream);
+/* out[i] = word first+i, word w = sum_j below(q) * q^(d-j) over draws
+ * w*(d+1)+1 .. (first draw = top digit; the acceptance suite's
+ * random_digit_safe_word, acceptance.cpp:52-56) */
+QPK_API qpk_status qpk_gen_words(uint64_t seed, uint64_t first, uint64_t n, uint64_t q, uint32_t d, double* out,
+                                 void* stream);
 /* record pairs: a[i] = draws 2k*i+1..2k*i+k, b[i] = the next k, each below(bound) */
 QPK_API qpk_status qpk_gen_pairs(uint64_t seed, uint64_t n, uint32_t k, uint32_t bound, uint8_t* a, uint8_t* b,
                                  void* stream);

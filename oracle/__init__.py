@@ -77,6 +77,7 @@ def oracle():
             _sig(lib, "qo_correction_table", I, [U64, U64, U32, I, U64, C.POINTER(PU64), PU64, PU64])
             _sig(lib, "qo_redq_run_f64", I, [U64, U64, U32, I, U32, I, f64p, U64, u8p])
             _sig(lib, "qo_redq_run_u64", I, [U64, U64, U32, I, U32, I, u64p, U64, u64p])
+            _sig(lib, "qo_redq_trace", I, [U64, U64, U32, U64, U64, PU64, PU64, u64p, u64p])
             _sig(lib, "qo_polymul_batch", I, [U64, U32, u8p, u8p, U64, u8p])
             _sig(lib, "qo_fqt_mul", I, [U64, U32, U64, U32, u64p, U64, u64p, U64, u64p, u64p])
             _sig(lib, "qo_field_build", VP, [U64, U32, U64, I])

@@ -922,3 +922,18 @@ u64 qo_fold_checksum_u64(const u64* data, u64 n) {
         }
     return h;
 }
+
+/* redq_trace (redq.cpp:184-195) for u128 words given as two halves, integer
+ * mode plan (p, q, d) without table: rop, raw digits u, residues mu. */
+int qo_redq_trace(u64 p, u64 q, u32 d, u64 r_lo, u64 r_hi, u64* rop_lo, u64* rop_hi, u64* u, u64* mu) {
+    qo_redq_plan pl;
+    int rc = qo_redq_plan_build(p, q, d, 0, &pl);
+    if (rc) return rc;
+    u128 r = ((u128)r_hi << 64) | r_lo;
+    u128 rop = r / p;
+    *rop_lo = (u64)rop;
+    *rop_hi = (u64)(rop >> 64);
+    rc = qo_redq_word(&pl, r, u, mu);
+    qo_redq_plan_free(&pl);
+    return rc;
+}

@@ -77,6 +77,8 @@ int qo_redq_batch_f64(const qo_redq_plan* plan, const double* words, uint64_t n,
 /* convenience: build plan + run, for ctypes */
 int qo_redq_run_f64(uint64_t p, uint64_t q, uint32_t d, int float_mode, uint32_t window, int binary_shift,
                     const double* words, uint64_t n, uint8_t* out);
+int qo_redq_trace(uint64_t p, uint64_t q, uint32_t d, uint64_t r_lo, uint64_t r_hi, uint64_t* rop_lo,
+                  uint64_t* rop_hi, uint64_t* u, uint64_t* mu);
 int qo_redq_run_u64(uint64_t p, uint64_t q, uint32_t d, int float_mode, uint32_t window, int binary_shift,
                     const uint64_t* words, uint64_t n, uint64_t* out);
 

@@ -117,7 +117,7 @@ SIGNATURES = {
     "qpk_gfq_matmul_rep": (I, [VP, VP, VP, U64, U64, U64, VP, VP]),
     "qpk_gfq_matmul_rep_host": (I, [VP, VP, VP, U64, U64, U64, VP, PCost]),
     "qpk_gen_draws": (I, [U64, U64, U64, U32, VP, VP]),
-    "qpk_gen_words": (I, [U64, U64, U64, U32, VP, VP]),
+    "qpk_gen_words": (I, [U64, U64, U64, U64, U32, VP, VP]),
     "qpk_gen_pairs": (I, [U64, U64, U32, U32, VP, VP, VP]),
     "qpk_probe_fp64": (I, [I, I, PD]),
 }
@@ -334,6 +334,8 @@ class GfqField:
     def fgdp_dot(self, v1, v2):
         v1 = _host(v1, np.uint32).reshape(-1)
         v2 = _host(v2, np.uint32).reshape(-1)
+        if v1.size != v2.size:
+            raise InvalidArgument("fgdp_dot: vector length mismatch")  # gfq.cpp:337
         out = C.c_uint32()
         cost = Cost()
         _check(lib().qpk_fgdp_dot(self._h, _ptr(v1), _ptr(v2), v1.size, C.byref(out), C.byref(cost)))
@@ -406,8 +408,8 @@ def gen_draws(seed, count, bound, out, start=0):
     return out
 
 
-def gen_words(seed, n, q, d, out):
-    _check(lib().qpk_gen_words(seed, n, q, d, _ptr(out), _stream()))
+def gen_words(seed, n, q, d, out, first=0):
+    _check(lib().qpk_gen_words(seed, first, n, q, d, _ptr(out), _stream()))
     return out
 
 

@@ -389,14 +389,15 @@ qpk_status qpk_gen_draws(uint64_t seed, uint64_t start, uint64_t count, uint32_t
     });
 }
 
-qpk_status qpk_gen_words(uint64_t seed, uint64_t n, uint64_t q, uint32_t d, double* out, void* stream) {
+qpk_status qpk_gen_words(uint64_t seed, uint64_t first, uint64_t n, uint64_t q, uint32_t d, double* out,
+                         void* stream) {
     return guard([&] {
         need(q >= 2, "q must be >= 2");
         need(qpack::pow_fits_u128(q, d + 1) && qpack::checked_pow_u128(q, d + 1) <= (qpack::u128(1) << 53),
              "q^(d+1) must not exceed 2^53");
         need(n == 0 || out, "null buffer");
         qpack::gpu::require_device();
-        qpack::gpu::check(qpk::launch_gen_words(seed, n, q, d, out, as_stream(stream)), "gen_words");
+        qpack::gpu::check(qpk::launch_gen_words(seed, first, n, q, d, out, as_stream(stream)), "gen_words");
     });
 }
 

@@ -99,8 +99,9 @@ cudaError_t launch_gfq_matmul(const GfqMatmulParams& P, const double* at, const 
 // Synthetic inputs: out[i] = SplitMix64(seed) draw (start+i+1) mod bound.
 cudaError_t launch_gen_draws(uint64_t seed, uint64_t start, uint64_t count, uint32_t bound, uint8_t* out,
                              cudaStream_t s);
-// q-adic words: word i = sum_j draw(i*(d+1)+j+1 mod q) * q^(d-j) (first draw = top digit)
-cudaError_t launch_gen_words(uint64_t seed, uint64_t n, uint64_t q, uint32_t d, double* out, cudaStream_t s);
+// q-adic words: out[i] = word first+i, word w = sum_j (draw w*(d+1)+j+1 mod q) * q^(d-j)
+cudaError_t launch_gen_words(uint64_t seed, uint64_t first, uint64_t n, uint64_t q, uint32_t d, double* out,
+                             cudaStream_t s);
 // record pairs: a[i] = draws 2k*i+1..2k*i+k, b[i] = the next k
 cudaError_t launch_gen_pairs(uint64_t seed, uint64_t n, uint32_t k, uint32_t bound, uint8_t* a, uint8_t* b,
                              cudaStream_t s);

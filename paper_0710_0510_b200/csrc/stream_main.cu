@@ -78,10 +78,10 @@ __global__ void gen_draws_kernel(uint64_t seed, uint64_t start, uint64_t count, 
         out[i] = static_cast<uint8_t>(splitmix_at(seed, start + i + 1) % bound);
 }
 
-__global__ void gen_words_kernel(uint64_t seed, uint64_t n, uint64_t q, uint32_t d, double* out) {
+__global__ void gen_words_kernel(uint64_t seed, uint64_t first, uint64_t n, uint64_t q, uint32_t d, double* out) {
     for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
         uint64_t r = 0;
-        for (uint32_t j = 0; j <= d; ++j) r = r * q + splitmix_at(seed, i * (d + 1) + j + 1) % q;
+        for (uint32_t j = 0; j <= d; ++j) r = r * q + splitmix_at(seed, (first + i) * (d + 1) + j + 1) % q;
         out[i] = static_cast<double>(r);
     }
 }
@@ -165,9 +165,10 @@ cudaError_t launch_gen_draws(uint64_t seed, uint64_t start, uint64_t count, uint
     return cudaGetLastError();
 }
 
-cudaError_t launch_gen_words(uint64_t seed, uint64_t n, uint64_t q, uint32_t d, double* out, cudaStream_t s) {
+cudaError_t launch_gen_words(uint64_t seed, uint64_t first, uint64_t n, uint64_t q, uint32_t d, double* out,
+                             cudaStream_t s) {
     if (n == 0) return cudaSuccess;
-    gen_words_kernel<<<grid_for(n), 256, 0, s>>>(seed, n, q, d, out);
+    gen_words_kernel<<<grid_for(n), 256, 0, s>>>(seed, first, n, q, d, out);
     return cudaGetLastError();
 }
 
