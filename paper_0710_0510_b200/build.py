@@ -30,7 +30,7 @@ CXX_FLAGS = f"-std=c++20 -O2 -fPIC -Wall -Wextra -I{CSRC} -I{ROOT}/include -I{CU
 
 CU_UNITS = [("stream_main.cu", None), ("gfq_matmul_main.cu", None), ("probe.cu", None)]
 CU_UNITS += [("stream_inst.cu", i) for i in range(1, 9)]
-CU_UNITS += [("gfq_matmul_inst.cu", k) for k in range(1, 5)]
+CU_UNITS += [("gfq_matmul_inst.cu", (k, 0)) for k in range(1, 5)] + [("gfq_matmul_inst.cu", (k, 1)) for k in (2, 3)]
 CXX_UNITS = ["capi.cpp"] + [f"host/{f}" for f in
                             ("common.cpp", "params.cpp", "fpdiv.cpp", "dqt.cpp", "redq.cpp", "polymul.cpp",
                              "gfq.cpp", "gpu_api.cpp")]
@@ -38,7 +38,8 @@ CXX_UNITS = ["capi.cpp"] + [f"host/{f}" for f in
 
 def _ninja_text() -> str:
     hdrs_cu = " ".join(os.path.join(CSRC, h) for h in
-                       ("device_common.cuh", "kernels.hpp", "stream_kernels.cuh", "stream_inst.hpp", "gfq_matmul.cuh"))
+                       ("device_common.cuh", "kernels.hpp", "stream_kernels.cuh", "stream_inst.hpp", "gfq_matmul.cuh",
+                        "redq_core.cuh"))
     lines = [
         f"nvcc = {NVCC}",
         f"nvflags = {NVCC_FLAGS}",
@@ -57,11 +58,14 @@ def _ninja_text() -> str:
     ]
     objs = []
     for src, inst in CU_UNITS:
-        base = os.path.splitext(src)[0] + (f"_{inst}" if inst else "")
-        obj = os.path.join(BUILD, base + ".o")
+        if isinstance(inst, tuple):
+            tag, defs = f"_{inst[0]}_v{inst[1]}", f"-DQPK_INST={inst[0]} -DQPK_VARIANT={inst[1]}"
+        else:
+            tag, defs = (f"_{inst}", f"-DQPK_INST={inst}") if inst else ("", "")
+        obj = os.path.join(BUILD, os.path.splitext(src)[0] + tag + ".o")
         lines.append(f"build {obj}: nvcc {os.path.join(CSRC, src)} | {hdrs_cu}")
-        if inst:
-            lines.append(f"  defs = -DQPK_INST={inst}")
+        if defs:
+            lines.append(f"  defs = {defs}")
         objs.append(obj)
     for src in CXX_UNITS:
         obj = os.path.join(BUILD, src.replace("/", "_").replace(".cpp", ".o"))

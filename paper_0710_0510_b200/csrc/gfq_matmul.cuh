@@ -1,25 +1,27 @@
-// K1 (pack) and K4 (matrix product) of the q-adic pipeline for GF(p^k).
+// K4: GF(p^k) matrix product as an exact fp64 contraction on q-packed
+// operands (reference gfq.cpp:389-404 -> fgdp_dot, gfq.cpp:335-387; paper
+// Alg. 4 and Theorem 3).
 //
-// K1a  DQT/Horner pack: coefficient records (k bytes) -> exact q-adic fp64
-//      words, written transposed/padded for the GEMM (dqt.cpp:23-37).
-// K1b  Zech/discrete-log tabulated pack: reps -> float_eval(rep) through the
-//      float table staged in shared memory (gfq.cpp:194-207, 355).
-// K4   C = A*B as an exact fp64 contraction on the packed words
-//      (gfq.cpp:389-404 -> fgdp_dot, gfq.cpp:335-387):
-//        * 128x128 CTA tile, 8 consumer warps each 64x32, fp64 tensor-core
-//          MMA (mma.sync m8n8k4 f64 -> DMMA on sm_100a; tcgen05 has no f64
-//          kind), accumulators in registers;
-//        * a producer warp streams 16-deep K slices of A^T and B with TMA
-//          bulk copies (one 1 KB row per lane) into padded shared rows
-//          (conflict-free fragment loads), 4-stage mbarrier pipeline;
-//        * delayed REDQ: every `chunk` K-steps a warp re-packs each
-//          accumulator to sum(mu_i q^i) so digit sums stay below q and the
-//          word below 2^53; warps are staggered so re-packs overlap the
-//          other warps' MMAs;
-//        * epilogue: final REDQ digits -> low/high half tables (Theorem 3,
-//          gfq.cpp:218-248) in coefficient form -> bytes, or -> rep.
+//  * 128x128 CTA tile, 8 consumer warps each 64x32, fp64 tensor-core MMA
+//    (mma.sync m8n8k4 f64 -> DMMA on sm_100a; tcgen05 has no f64 kind),
+//    accumulators in registers;
+//  * a producer warp streams 16-deep K slices of A^T and B with TMA bulk
+//    copies (one 1 KB row per lane) into padded shared rows (conflict-free
+//    fragment loads), 4-stage full/empty mbarrier pipeline.  (Measured on
+//    B200, scripts/mm_variants.cu: the dedicated producer sustains 35.6
+//    TFLOP/s = 96% of the DMMA probe; letting the last consumer warp refill
+//    a stage instead reaches only 26.8 -- that warp becomes a straggler.);
+//  * delayed REDQ: every `chunk` K-steps a warp re-packs each accumulator to
+//    sum(mu_i q^i) (redq + assemble, redq.cpp:178-182) so digit sums stay
+//    below q and the word below 2^53.  Re-packs run at stage granularity,
+//    outside the stage loop (so they are never predicated into every stage)
+//    and staggered so the two consumer warps of an SM sub-partition never
+//    re-pack in the same stage: one warp's integer work overlaps the other
+//    warp's MMAs;
+//  * epilogue: final REDQ digits -> low/high half tables in coefficient form
+//    (gfq.cpp:218-248) -> bytes, or -> rep through the log table.
 //
-// Templates only; instantiated per k in gfq_matmul_inst.cu (-DQPK_INST=k).
+// Templates only; instantiated per (k, policy) in gfq_matmul_inst.cu.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -29,6 +31,7 @@
 
 #include "device_common.cuh"
 #include "kernels.hpp"
+#include "redq_core.cuh"
 
 namespace qpk {
 
@@ -53,65 +56,28 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
 }
 
-constexpr uint64_t kMask52 = (uint64_t(1) << 52) - 1;
-
-// raw REDQ digits of an accumulated word (always < 2^53 and, for every
-// supported field, <= r_max once the per-chunk bound holds)
-template <int ND, bool POW2>
-__device__ __forceinline__ void acc_digits(const RedqParams& P, double r, uint32_t (&u)[ND]) {
-    const uint64_t rb = r < kTwo52 ? (dbits(r + kTwo52) & kMask52) : __double2ull_rz(r);
-    const bool premul = r <= P.r_max;
-    const uint64_t rop = premul ? floor_div_premul(r, P.inv_p) : rb / P.p;
-    if constexpr (POW2) {
-#pragma unroll
-        for (int i = 0; i < ND; ++i) {
-            const uint32_t sh = P.qbits * i;
-            u[i] = static_cast<uint32_t>(rb >> sh) - P.p * static_cast<uint32_t>(rop >> sh);
-        }
-    } else {
-        const double ropd = static_cast<double>(rop);
-#pragma unroll
-        for (int i = 0; i < ND; ++i) {
-            uint64_t x, y;
-            if (premul) {
-                x = floor_div_premul(r, P.inv_q[i]);
-                y = floor_div_premul(ropd, P.inv_q[i]);
-            } else {
-                x = rb / P.qpow[i];
-                y = rop / P.qpow[i];
-            }
-            u[i] = static_cast<uint32_t>(x) - P.p * static_cast<uint32_t>(y);
-        }
-    }
-}
-
-// REDQ + re-pack (redq.cpp:178-182 `redq` + `assemble`): the word whose
-// digit i is (digit i of r) mod p, returned as an exact double.
-template <int ND, bool POW2>
-__device__ __forceinline__ double redq_repack(const RedqParams& P, double r) {
-    uint32_t u[ND];
-    acc_digits<ND, POW2>(P, r, u);
-    uint32_t mu[ND];
-#pragma unroll
-    for (int i = 0; i + 1 < ND; ++i) {
-        const uint32_t t = u[i] + P.neg_q * u[i + 1];
-        mu[i] = t - P.p * __umulhi(t, P.mod_magic);
-    }
-    mu[ND - 1] = u[ND - 1];
-    if constexpr (POW2) {
+// REDQ + re-pack: the word whose digit i is (digit i of r) mod p, as an
+// exact double (digits mu_i via the direct correction, then assembled)
+template <int ND, class K>
+__device__ __forceinline__ double redq_repack(const K& c, double r) {
+    uint32_t u[ND], mu[ND];
+    redq_raw_digits<ND>(c, r, u);
+    redq_correct<ND, 0>(c, u, mu, [](uint32_t) { return 0u; });
+    if constexpr (K::kPow2) {
         uint64_t v = 0;
 #pragma unroll
-        for (int i = ND - 1; i >= 0; --i) v = (v << P.qbits) | mu[i];
+        for (int i = ND - 1; i >= 0; --i) v = (v << c.qbits()) | mu[i];
         return __longlong_as_double(static_cast<long long>(v | 0x4330000000000000ull)) - kTwo52;
     } else {
         double v = 0.0;
+        const double qd = static_cast<double>(c.P.q);
 #pragma unroll
-        for (int i = ND - 1; i >= 0; --i) v = fma(v, static_cast<double>(P.q), static_cast<double>(mu[i]));
+        for (int i = ND - 1; i >= 0; --i) v = fma(v, qd, static_cast<double>(mu[i]));
         return v;
     }
 }
 
-__device__ __forceinline__ uint32_t add_mod_bytes(uint32_t x, uint32_t y, uint32_t p) {
+__device__ __forceinline__ uint32_t add_mod_bytes_mm(uint32_t x, uint32_t y, uint32_t p) {
     if (p < 128) {
         const uint32_t pp = p * 0x01010101u;
         const uint32_t s = __vadd4(x, y);
@@ -128,27 +94,29 @@ __device__ __forceinline__ uint32_t add_mod_bytes(uint32_t x, uint32_t y, uint32
 }
 
 // final conversion of one accumulated word to packed coefficient bytes
-template <int K, bool POW2>
-__device__ __forceinline__ uint32_t acc_to_coeffs(const GfqMatmulParams& P, double r, const uint32_t* lc,
-                                                  const uint32_t* hc) {
-    constexpr int ND = 2 * K - 1;
+template <int KR, class K>
+__device__ __forceinline__ uint32_t acc_to_coeffs(const K& c, uint32_t lh_radix, double r, uint32_t lc_s,
+                                                  uint32_t hc_s) {
+    constexpr int ND = 2 * KR - 1;
     uint32_t u[ND];
-    acc_digits<ND, POW2>(P.rq, r, u);
+    redq_raw_digits<ND>(c, r, u);
     uint32_t il = 0, ih = 0;
 #pragma unroll
-    for (int i = K - 1; i >= 0; --i) {
-        il = il * P.lh_radix + u[i];
-        ih = ih * P.lh_radix + u[K - 1 + i];
+    for (int i = KR - 1; i >= 0; --i) {
+        il = il * lh_radix + u[i];
+        ih = ih * lh_radix + u[KR - 1 + i];
     }
-    return add_mod_bytes(lc[il], hc[ih], P.p);
+    return add_mod_bytes_mm(lds_u32(lc_s + 4 * il), lds_u32(hc_s + 4 * ih), c.p());
 }
 
-template <int K, bool POW2>
+// REDQ_STAGE: re-pack at stage granularity (chunk a multiple of BK) rather
+// than per 4-step MMA (fields whose safe chunk is below BK)
+template <int KR, class K, bool REDQ_STAGE>
 __global__ void __launch_bounds__(THREADS, 1)
     gfq_matmul_kernel(const GfqMatmulParams P, const double* __restrict__ at, const double* __restrict__ bm,
                       uint64_t m, uint64_t n, uint64_t K_pad, uint64_t m_pad, uint64_t n_pad,
                       uint8_t* __restrict__ out_c, uint32_t* __restrict__ out_r) {
-    constexpr int ND = 2 * K - 1;
+    constexpr int ND = 2 * KR - 1;
     extern __shared__ __align__(128) uint8_t smem[];
     double* stages = reinterpret_cast<double*>(smem);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_DOUBLES * 8);
@@ -161,12 +129,10 @@ __global__ void __launch_bounds__(THREADS, 1)
 
     // epilogue tables (lc | hc | log) staged once per CTA
     uint32_t nlh = 1;
-    for (int i = 0; i < K; ++i) nlh *= P.lh_radix;
-    const uint32_t ntab = 2 * nlh + (out_r ? P.order : 0);
+    for (int i = 0; i < KR; ++i) nlh *= P.lh_radix;
     for (uint32_t i = tid; i < 2 * nlh; i += blockDim.x) tabs[i] = i < nlh ? P.lc[i] : P.hc[i - nlh];
     if (out_r)
         for (uint32_t i = tid; i < P.order; i += blockDim.x) tabs[2 * nlh + i] = P.log[i];
-    (void)ntab;
     if (tid == 0) {
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
@@ -195,7 +161,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
 
     // -------------------- consumers ---------------------------------------
-    const int wm = (warp >> 2) * WM;  // 2 x 4 warp grid
+    const K c{P.rq};
+    const int wm = (warp >> 2) * WM;  // 2 x 4 warp grid; warps w, w+4 share SMSP w%4
     const int wn = (warp & 3) * WN;
     const int lr = lane >> 2, lc4 = lane & 3;
     double acc[MT][NT][2];
@@ -204,47 +171,77 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
         for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-    // delayed REDQ schedule at 4-step granularity, staggered across warps
-    const int chunk4 = static_cast<int>(P.chunk / 4);
-    int countdown = chunk4 > 0 ? chunk4 - (warp * chunk4) / NCW : 0x7fffffff;
+    auto repack_all = [&]() {
+#pragma unroll
+        for (int i = 0; i < MT; ++i)
+#pragma unroll
+            for (int j = 0; j < NT; ++j) {
+                acc[i][j][0] = redq_repack<ND>(c, acc[i][j][0]);
+                acc[i][j][1] = redq_repack<ND>(c, acc[i][j][1]);
+            }
+    };
+    // 4 MMA k-steps of one stage; per step 8 A and 4 B fragments -> 32 DMMA
+    auto mma_kstep = [&](const double* sa, const double* sb, int kk) {
+        const double* pa = sa + (kk * 4 + lc4) * LDS_ + wm + lr;
+        const double* pb = sb + (kk * 4 + lc4) * LDS_ + wn + lr;
+        double af[MT], bf[NT];
+#pragma unroll
+        for (int i = 0; i < MT; ++i) af[i] = pa[i * 8];
+#pragma unroll
+        for (int j = 0; j < NT; ++j) bf[j] = pb[j * 8];
+#pragma unroll
+        for (int i = 0; i < MT; ++i)
+#pragma unroll
+            for (int j = 0; j < NT; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    };
 
-    for (int kt = 0; kt < KT; ++kt) {
-        const int s = kt % STAGES;
-        mbar_wait(&full[s], (kt / STAGES) & 1);
-        const double* sa = stages + s * STAGE_DOUBLES;
-        const double* sb = sa + BK * LDS_;
+    if constexpr (REDQ_STAGE) {
+        auto stage = [&](int kt) {
+            const int s = kt % STAGES;
+            mbar_wait(&full[s], (kt / STAGES) & 1);
+            const double* sa = stages + s * STAGE_DOUBLES;
 #pragma unroll 1
-        for (int kk = 0; kk < BK / 4; ++kk) {
-            const double* pa = sa + (kk * 4 + lc4) * LDS_ + wm + lr;
-            const double* pb = sb + (kk * 4 + lc4) * LDS_ + wn + lr;
-            double af[MT], bf[NT];
-#pragma unroll
-            for (int i = 0; i < MT; ++i) af[i] = pa[i * 8];
-#pragma unroll
-            for (int j = 0; j < NT; ++j) bf[j] = pb[j * 8];
-#pragma unroll
-            for (int i = 0; i < MT; ++i)
-#pragma unroll
-                for (int j = 0; j < NT; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
-            if (--countdown == 0) {
-                countdown = chunk4;
-#pragma unroll
-                for (int i = 0; i < MT; ++i)
-#pragma unroll
-                    for (int j = 0; j < NT; ++j) {
-                        acc[i][j][0] = redq_repack<ND, POW2>(P.rq, acc[i][j][0]);
-                        acc[i][j][1] = redq_repack<ND, POW2>(P.rq, acc[i][j][1]);
-                    }
+            for (int kk = 0; kk < BK / 4; ++kk) mma_kstep(sa, sa + BK * LDS_, kk);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+        };
+        // re-pack after stage `next`, every cs stages; the phase offset keeps
+        // warps w and w+4 (same sub-partition) cs/2 stages apart
+        const int cs = static_cast<int>(P.chunk / BK);
+        int next = KT;
+        if (cs > 0) next = cs - 1 - ((warp & 3) + (warp >> 2) * (cs / 2)) % cs;
+        int kt = 0;
+        while (kt < KT) {
+            const int end = next + 1 < KT ? next + 1 : KT;
+            for (; kt < end; ++kt) stage(kt);
+            if (kt == next + 1 && kt < KT) {
+                repack_all();
+                next += cs;
             }
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[s]);
+    } else {
+        // generic small-chunk fields: re-pack every `chunk` MMA k-steps
+        const int chunk4 = static_cast<int>(P.chunk / 4);
+        int countdown = chunk4 > 0 ? chunk4 - (warp * chunk4) / NCW : 0x7fffffff;
+        for (int kt = 0; kt < KT; ++kt) {
+            const int s = kt % STAGES;
+            mbar_wait(&full[s], (kt / STAGES) & 1);
+            const double* sa = stages + s * STAGE_DOUBLES;
+#pragma unroll 1
+            for (int kk = 0; kk < BK / 4; ++kk) {
+                mma_kstep(sa, sa + BK * LDS_, kk);
+                if (--countdown == 0) {
+                    countdown = chunk4;
+                    repack_all();
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+        }
     }
 
     // ------------------------- epilogue ------------------------------------
-    const uint32_t* lc = tabs;
-    const uint32_t* hc = tabs + nlh;
-    const uint32_t* lg = tabs + 2 * nlh;
+    const uint32_t lc_s = smem_addr(tabs), hc_s = lc_s + 4 * nlh, lg_s = lc_s + 8 * nlh;
 #pragma unroll
     for (int i = 0; i < MT; ++i) {
         const uint64_t row = m0 + wm + i * 8 + lr;
@@ -254,16 +251,16 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 if (row < m && col + h < n) {
-                    const uint32_t c = acc_to_coeffs<K, POW2>(P, acc[i][j][h], lc, hc);
+                    const uint32_t cf = acc_to_coeffs<KR>(c, P.lh_radix, acc[i][j][h], lc_s, hc_s);
                     if (out_c) {
-                        uint8_t* dst = out_c + (row * n + col + h) * K;
+                        uint8_t* dst = out_c + (row * n + col + h) * KR;
 #pragma unroll
-                        for (int t = 0; t < K; ++t) dst[t] = static_cast<uint8_t>(c >> (8 * t));
+                        for (int t = 0; t < KR; ++t) dst[t] = static_cast<uint8_t>(cf >> (8 * t));
                     } else {
                         uint32_t idx = 0;
 #pragma unroll
-                        for (int t = K - 1; t >= 0; --t) idx = idx * P.p + ((c >> (8 * t)) & 0xff);
-                        out_r[row * n + col + h] = lg[idx];
+                        for (int t = KR - 1; t >= 0; --t) idx = idx * c.p() + ((cf >> (8 * t)) & 0xff);
+                        out_r[row * n + col + h] = lds_u32(lg_s + 4 * idx);
                     }
                 }
             }
@@ -271,23 +268,54 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
 }
 
-template <int K, bool POW2>
-cudaError_t run_matmul(const GfqMatmulParams& P, const double* at, const double* b, uint64_t m, uint64_t n,
-                       uint64_t K_pad, uint64_t m_pad, uint64_t n_pad, uint8_t* oc, uint32_t* orp, cudaStream_t s) {
+template <int KR, class K, bool REDQ_STAGE>
+cudaError_t run_matmul_t(const GfqMatmulParams& P, const double* at, const double* b, uint64_t m, uint64_t n,
+                         uint64_t K_pad, uint64_t m_pad, uint64_t n_pad, uint8_t* oc, uint32_t* orp, cudaStream_t s) {
     uint32_t nlh = 1;
-    for (int i = 0; i < K; ++i) nlh *= P.lh_radix;
+    for (int i = 0; i < KR; ++i) nlh *= P.lh_radix;
     const size_t smem = SMEM_BYTES + size_t(2 * nlh + P.order) * 4;
     if (smem > 227 * 1024) return cudaErrorInvalidValue;
     static bool attr = false;
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(gfq_matmul_kernel<K, POW2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             227 * 1024);
+        cudaError_t e = cudaFuncSetAttribute(gfq_matmul_kernel<KR, K, REDQ_STAGE>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         if (e != cudaSuccess) return e;
         attr = true;
     }
     dim3 grid(static_cast<unsigned>(n_pad / BN), static_cast<unsigned>(m_pad / BM));
-    gfq_matmul_kernel<K, POW2><<<grid, THREADS, smem, s>>>(P, at, b, m, n, K_pad, m_pad, n_pad, oc, orp);
+    gfq_matmul_kernel<KR, K, REDQ_STAGE><<<grid, THREADS, smem, s>>>(P, at, b, m, n, K_pad, m_pad, n_pad, oc, orp);
     return cudaGetLastError();
+}
+
+// a plan is "safe" when every accumulated word stays <= min(r_max, 2^52)
+inline bool mm_plan_safe(const RedqParams& R) {
+    return R.qbits && R.limit <= R.r_max + 1.0 && R.limit <= kTwo52;
+}
+
+// VARIANT 1: compile-time fast paths for the benchmark fields (C4 GF(3^2)
+// at q = 2^16, C5 GF(3^3) at q = 2^10); returns cudaErrorNotSupported when
+// the field is not one of them.  VARIANT 0: runtime-parameter kernels.
+template <int KR, int VARIANT>
+cudaError_t run_matmul(const GfqMatmulParams& P, const double* at, const double* b, uint64_t m, uint64_t n,
+                       uint64_t K_pad, uint64_t m_pad, uint64_t n_pad, uint8_t* oc, uint32_t* orp, cudaStream_t s) {
+    const bool stage_ok = P.chunk == 0 || P.chunk % BK == 0;
+    if constexpr (VARIANT == 1) {
+        if constexpr (KR == 2) {
+            if (P.p == 3 && P.rq.qbits == 16 && mm_plan_safe(P.rq) && stage_ok)
+                return run_matmul_t<2, CtConst<3, 16>, true>(P, at, b, m, n, K_pad, m_pad, n_pad, oc, orp, s);
+        }
+        if constexpr (KR == 3) {
+            if (P.p == 3 && P.rq.qbits == 10 && mm_plan_safe(P.rq) && stage_ok)
+                return run_matmul_t<3, CtConst<3, 10>, true>(P, at, b, m, n, K_pad, m_pad, n_pad, oc, orp, s);
+        }
+        return cudaErrorNotSupported;
+    } else {
+        if (P.rq.qbits)
+            return stage_ok ? run_matmul_t<KR, RtConst<true>, true>(P, at, b, m, n, K_pad, m_pad, n_pad, oc, orp, s)
+                            : run_matmul_t<KR, RtConst<true>, false>(P, at, b, m, n, K_pad, m_pad, n_pad, oc, orp, s);
+        return stage_ok ? run_matmul_t<KR, RtConst<false>, true>(P, at, b, m, n, K_pad, m_pad, n_pad, oc, orp, s)
+                        : run_matmul_t<KR, RtConst<false>, false>(P, at, b, m, n, K_pad, m_pad, n_pad, oc, orp, s);
+    }
 }
 
 }  // namespace

@@ -9,14 +9,19 @@
 
 namespace qpk {
 
-cudaError_t matmul_launch_k1(const GfqMatmulParams&, const double*, const double*, uint64_t, uint64_t, uint64_t,
-                             uint64_t, uint64_t, uint8_t*, uint32_t*, cudaStream_t);
-cudaError_t matmul_launch_k2(const GfqMatmulParams&, const double*, const double*, uint64_t, uint64_t, uint64_t,
-                             uint64_t, uint64_t, uint8_t*, uint32_t*, cudaStream_t);
-cudaError_t matmul_launch_k3(const GfqMatmulParams&, const double*, const double*, uint64_t, uint64_t, uint64_t,
-                             uint64_t, uint64_t, uint8_t*, uint32_t*, cudaStream_t);
-cudaError_t matmul_launch_k4(const GfqMatmulParams&, const double*, const double*, uint64_t, uint64_t, uint64_t,
-                             uint64_t, uint64_t, uint8_t*, uint32_t*, cudaStream_t);
+// gfq_matmul_inst.cu, one per (k, variant): variant 1 = compile-time fast
+// path (cudaErrorNotSupported when the field is not one it covers)
+#define QPK_DECL_MM(K, V)                                                                                     \
+    cudaError_t matmul_launch_k##K##_v##V(const GfqMatmulParams&, const double*, const double*, uint64_t,     \
+                                          uint64_t, uint64_t, uint64_t, uint64_t, uint8_t*, uint32_t*,         \
+                                          cudaStream_t);
+QPK_DECL_MM(1, 0)
+QPK_DECL_MM(2, 0)
+QPK_DECL_MM(3, 0)
+QPK_DECL_MM(4, 0)
+QPK_DECL_MM(2, 1)
+QPK_DECL_MM(3, 1)
+#undef QPK_DECL_MM
 
 namespace {
 
@@ -85,11 +90,15 @@ cudaError_t launch_gfq_matmul(const GfqMatmulParams& P, const double* at, const 
                               uint32_t* out_reps, cudaStream_t s) {
     if (m == 0 || n == 0) return cudaSuccess;
     if (m_pad % 128 || n_pad % 128 || K_pad % 16) return cudaErrorInvalidValue;
+    cudaError_t e = cudaErrorNotSupported;
+    if (P.k == 2) e = matmul_launch_k2_v1(P, at, b, m, n, K_pad, m_pad, n_pad, out_coeffs, out_reps, s);
+    if (P.k == 3) e = matmul_launch_k3_v1(P, at, b, m, n, K_pad, m_pad, n_pad, out_coeffs, out_reps, s);
+    if (e != cudaErrorNotSupported) return e;
     switch (P.k) {
-        case 1: return matmul_launch_k1(P, at, b, m, n, K_pad, m_pad, n_pad, out_coeffs, out_reps, s);
-        case 2: return matmul_launch_k2(P, at, b, m, n, K_pad, m_pad, n_pad, out_coeffs, out_reps, s);
-        case 3: return matmul_launch_k3(P, at, b, m, n, K_pad, m_pad, n_pad, out_coeffs, out_reps, s);
-        case 4: return matmul_launch_k4(P, at, b, m, n, K_pad, m_pad, n_pad, out_coeffs, out_reps, s);
+        case 1: return matmul_launch_k1_v0(P, at, b, m, n, K_pad, m_pad, n_pad, out_coeffs, out_reps, s);
+        case 2: return matmul_launch_k2_v0(P, at, b, m, n, K_pad, m_pad, n_pad, out_coeffs, out_reps, s);
+        case 3: return matmul_launch_k3_v0(P, at, b, m, n, K_pad, m_pad, n_pad, out_coeffs, out_reps, s);
+        case 4: return matmul_launch_k4_v0(P, at, b, m, n, K_pad, m_pad, n_pad, out_coeffs, out_reps, s);
         default: return cudaErrorInvalidValue;
     }
 }

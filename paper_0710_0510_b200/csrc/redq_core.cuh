@@ -1,0 +1,158 @@
+// REDQ on one exact-integer fp64 word (paper Alg. 2, Theorem 2;
+// reference redq.cpp:31-100), parameterised by a constants policy:
+//
+//   RtConst<POW2>        p, q, neg_q read from the RedqParams block at run
+//                        time; any word below 2^53 (premultiplied floor when
+//                        r <= r_max, exact integer division otherwise).
+//   CtConst<P, QBITS>    p and q = 2^QBITS fixed at compile time and the
+//                        plan known to keep every word <= min(r_max, 2^52):
+//                        no range branches, shifts and the mod-p correction
+//                        fold into immediates.  Dispatched for the benchmark
+//                        fields (C1-C5); everything else uses RtConst.
+//
+// Both produce identical digits: u_i = floor(r/q^i) - p*floor(rop/q^i) in
+// [0, p-1], formed in wrapping 32-bit arithmetic.
+#pragma once
+
+#include <cstdint>
+
+#include "device_common.cuh"
+#include "kernels.hpp"
+
+namespace qpk {
+
+constexpr uint64_t kMask52 = (uint64_t(1) << 52) - 1;
+
+// t mod p for 0 <= t < 2^16 and p <= 256 (floor(t/p) from a 32-bit
+// multiply-high by ceil(2^32/p) is exact in that range)
+__device__ __forceinline__ uint32_t mod_by_magic(uint32_t t, uint32_t p, uint32_t magic) {
+    return t - p * __umulhi(t, magic);
+}
+
+template <bool POW2>
+struct RtConst {
+    static constexpr bool kSafe = false;
+    static constexpr bool kPow2 = POW2;
+    const RedqParams& P;
+    __device__ __forceinline__ uint32_t p() const { return P.p; }
+    __device__ __forceinline__ uint32_t qbits() const { return P.qbits; }
+    __device__ __forceinline__ uint32_t neg_q() const { return P.neg_q; }
+    __device__ __forceinline__ uint32_t radix() const { return P.radix; }
+    __device__ __forceinline__ uint32_t modp(uint32_t t) const { return mod_by_magic(t, P.p, P.mod_magic); }
+};
+
+template <uint32_t P_, uint32_t QBITS_>
+struct CtConst {
+    static constexpr bool kSafe = true;
+    static constexpr bool kPow2 = true;
+    static constexpr uint32_t kP = P_, kQbits = QBITS_;
+    static constexpr uint32_t kNegQ = (P_ - (uint32_t(1) << QBITS_) % P_) % P_;
+    const RedqParams& P;
+    __device__ __forceinline__ static constexpr uint32_t p() { return P_; }
+    __device__ __forceinline__ static constexpr uint32_t qbits() { return QBITS_; }
+    __device__ __forceinline__ static constexpr uint32_t neg_q() { return kNegQ; }
+    __device__ __forceinline__ static constexpr uint32_t radix() { return P_; }
+    // t <= (p-1)(1+neg_q): a packed lookup constant when it fits 32 bits
+    __device__ __forceinline__ static uint32_t modp(uint32_t t) {
+        constexpr uint32_t tmax = (P_ - 1) * (1 + kNegQ);
+        if constexpr (P_ <= 4 && tmax < 16) {
+            constexpr uint32_t lut = [] {
+                uint32_t v = 0;
+                for (uint32_t i = 0; i <= tmax; ++i) v |= (i % P_) << (2 * i);
+                return v;
+            }();
+            return (lut >> (2 * t)) & 3u;
+        } else {
+            return t % P_;
+        }
+    }
+};
+
+// Exact integer of a non-negative double below 2^52 in (lo, hi) halves.
+__device__ __forceinline__ uint64_t int_bits52(double r) { return dbits(r + kTwo52) & kMask52; }
+
+// Raw digits of r (an exact integer < 2^53; <= r_max and < 2^52 for CtConst).
+template <int ND, class K>
+__device__ __forceinline__ void redq_raw_digits(const K& c, double r, uint32_t (&u)[ND]) {
+    const RedqParams& P = c.P;
+    uint64_t rb, rop;
+    bool premul = true;
+    if constexpr (K::kSafe) {
+        rb = int_bits52(r);
+        rop = floor_div_premul(r, P.inv_p);
+    } else {
+        premul = r <= P.r_max;
+        rb = r < kTwo52 ? int_bits52(r) : __double2ull_rz(r);
+        rop = premul ? floor_div_premul(r, P.inv_p) : rb / P.p;
+    }
+    if constexpr (K::kPow2) {
+#pragma unroll
+        for (int i = 0; i < ND; ++i) {
+            const uint32_t sh = c.qbits() * i;
+            u[i] = static_cast<uint32_t>(rb >> sh) - c.p() * static_cast<uint32_t>(rop >> sh);
+        }
+    } else {
+        const double ropd = static_cast<double>(rop);
+#pragma unroll
+        for (int i = 0; i < ND; ++i) {
+            uint64_t x, y;
+            if (premul) {
+                x = floor_div_premul(r, P.inv_q[i]);
+                y = floor_div_premul(ropd, P.inv_q[i]);
+            } else {
+                x = rb / P.qpow[i];
+                y = rop / P.qpow[i];
+            }
+            u[i] = static_cast<uint32_t>(x) - c.p() * static_cast<uint32_t>(y);
+        }
+    }
+}
+
+// Word validation with packed_from_double semantics (dqt.cpp:96-100) plus
+// check_input (redq.cpp:22-29): returns trunc(w); sets kErrDomain when w is
+// negative, NaN or not below min(q^(d+1), 2^53).  Invalid words still flow
+// through the arithmetic (their residues are unspecified; the batch fails).
+__device__ __forceinline__ double checked_word(const RedqParams& P, double w, uint32_t& err) {
+    const double r = trunc(w);
+    if (!(w >= 0.0 && r < P.limit)) err |= kErrDomain;
+    return r;
+}
+
+// Correction mu from u (redq.cpp:61-100): W = 0 direct (identity when
+// p | q), W = 2..4 windowed table of Alg. 3 with one byte per residue.
+template <int ND, int W, class K, class TabLoad>
+__device__ __forceinline__ void redq_correct(const K& c, const uint32_t (&u)[ND], uint32_t (&mu)[ND], TabLoad tab) {
+    constexpr int D = ND - 1;
+    if constexpr (W == 0 || D == 0) {
+        if (D > 0 && c.neg_q() != 0) {
+#pragma unroll
+            for (int i = 0; i < D; ++i) mu[i] = c.modp(u[i] + c.neg_q() * u[i + 1]);
+            mu[D] = u[D];
+        } else {
+#pragma unroll
+            for (int i = 0; i < ND; ++i) mu[i] = u[i];
+        }
+    } else {
+        constexpr int A = (D + W - 2) / (W - 1);
+#pragma unroll
+        for (int a = 0; a < A; ++a) {
+            const int s = a * (W - 1);
+            uint32_t idx = 0;
+#pragma unroll
+            for (int j = W - 1; j >= 0; --j) idx = idx * c.radix() + (s + j <= D ? u[s + j] : 0u);
+            const uint32_t e = tab(idx);
+#pragma unroll
+            for (int j = 0; j < W; ++j)
+                if (s + j <= D && (j + 1 < W || s + j == D)) mu[s + j] = byte_of(e, j);
+        }
+    }
+}
+
+// shared-memory u32 load at a 32-bit shared address
+__device__ __forceinline__ uint32_t lds_u32(uint32_t saddr) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(saddr));
+    return v;
+}
+
+}  // namespace qpk

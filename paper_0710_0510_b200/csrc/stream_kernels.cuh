@@ -18,7 +18,6 @@
 //
 // Records that do not fill a whole tile, or buffers that are not 16-byte
 // aligned, go through stream_tail_kernel (plain byte loads, same op).
-
 #pragma once
 
 #include <cuda_runtime.h>
@@ -28,162 +27,147 @@
 
 #include "device_common.cuh"
 #include "kernels.hpp"
+#include "redq_core.cuh"
 
 namespace qpk {
 
 namespace {
 
-constexpr uint64_t kMask52 = (uint64_t(1) << 52) - 1;
-
-// ------------------------------------------------------------------ REDQ core
-// Raw REDQ digits of one word (redq.cpp:31-59): rop = floor(r/p) with one
-// premultiplied fp64 floor, u_i = floor(r/q^i) - p*floor(rop/q^i).  Every
-// u_i is in [0, p-1] (paper Theorem 2), so it is formed in wrapping 32-bit
-// arithmetic from the low 32 bits of the two shifted quotients.
-//
-// `w` follows packed_from_double (dqt.cpp:96-100): truncated toward zero,
-// rejected when negative, NaN or not below min(q^(d+1), 2^53) (the latter is
-// check_input, redq.cpp:22-29).
-template <int ND, bool POW2>
-__device__ __forceinline__ void redq_digits(const RedqParams& P, double w, uint32_t (&u)[ND], uint32_t& err) {
-    double r = trunc(w);
-    if (!(w >= 0.0 && r < P.limit)) {
-        err |= kErrDomain;
-        r = 0.0;
-    }
-    const bool premul = r <= P.r_max;
-    const uint64_t rb = r < kTwo52 ? (dbits(r + kTwo52) & kMask52) : __double2ull_rz(r);
-    const uint64_t rop = premul ? floor_div_premul(r, P.inv_p) : rb / P.p;
-    if constexpr (POW2) {
+// records -> contiguous byte stream -> u32 words (all indices constexpr)
+template <int R, int OUT>
+__device__ __forceinline__ void pack_records(const uint64_t (&rec)[R], uint32_t (&ow)[R * OUT / 4]) {
 #pragma unroll
-        for (int i = 0; i < ND; ++i) {
-            const uint32_t sh = P.qbits * i;
-            u[i] = static_cast<uint32_t>(rb >> sh) - P.p * static_cast<uint32_t>(rop >> sh);
-        }
-    } else {
-        const double ropd = static_cast<double>(rop);
+    for (int i = 0; i < R * OUT / 4; ++i) {
+        uint32_t w = 0;
 #pragma unroll
-        for (int i = 0; i < ND; ++i) {
-            uint64_t x, y;
-            if (premul) {
-                x = floor_div_premul(r, P.inv_q[i]);
-                y = floor_div_premul(ropd, P.inv_q[i]);
-            } else {
-                x = rb / P.qpow[i];
-                y = rop / P.qpow[i];
-            }
-            u[i] = static_cast<uint32_t>(x) - P.p * static_cast<uint32_t>(y);
+        for (int b = 0; b < 4; ++b) {
+            const int g = 4 * i + b;
+            w |= static_cast<uint32_t>((rec[g / OUT] >> (8 * (g % OUT))) & 0xffu) << (8 * b);
         }
+        ow[i] = w;
     }
 }
 
-// (u_i + neg_q * u_{i+1}) mod p for t < 2^16, p <= 256: floor(t/p) from a
-// 32-bit multiply-high by ceil(2^32/p) is exact in that range.
-__device__ __forceinline__ uint32_t mod_small(uint32_t t, uint32_t p, uint32_t magic) {
-    return t - p * __umulhi(t, magic);
-}
+// byte `i` of a run of packed u32 words
+__device__ __forceinline__ uint32_t run_byte(const uint32_t* w, int i) { return byte_of(w[i >> 2], i & 3); }
 
-// Correction mu from u (redq.cpp:61-100).  W = 0: direct formula (or the
-// identity when p | q); W = 2..4: the windowed table of Alg. 3, windows of
-// W digits starting at a*(W-1), zero padded past the top digit, a window's
-// last slot kept only at the top digit.  The device table stores each
-// window's residues one per byte so decoding is a byte extract.
-template <int ND, int W>
-__device__ __forceinline__ void redq_correct(const RedqParams& P, const uint32_t (&u)[ND], uint32_t (&mu)[ND],
-                                             const uint32_t* tab) {
+// residues mu_0..mu_{ND-1} of one word, packed one per byte
+template <int ND, int W, class K>
+__device__ __forceinline__ uint64_t redq_record(const K& c, double r, uint32_t tab_saddr) {
+    uint32_t u[ND];
+    redq_raw_digits<ND>(c, r, u);
     constexpr int D = ND - 1;
-    if constexpr (W == 0 || D == 0) {
-        if (W == 0 && D > 0 && P.neg_q != 0) {
+    if constexpr (W > 0 && D > 0) {
+        if (c.neg_q() != 0) {
+            // windowed table (Alg. 3): window a covers digits s..s+W-1,
+            // s = a(W-1); its first W-1 residues are final, the last one only
+            // at the top digit
+            constexpr int A = (D + W - 2) / (W - 1);
+            uint64_t rec = 0;
 #pragma unroll
-            for (int i = 0; i < D; ++i) mu[i] = mod_small(u[i] + P.neg_q * u[i + 1], P.p, P.mod_magic);
-            mu[D] = u[D];
-        } else {
+            for (int a = 0; a < A; ++a) {
+                const int s = a * (W - 1);
+                uint32_t idx = 0;
 #pragma unroll
-            for (int i = 0; i < ND; ++i) mu[i] = u[i];
-        }
-    } else {
-        constexpr int A = (D + W - 2) / (W - 1);
-#pragma unroll
-        for (int a = 0; a < A; ++a) {
-            const int s = a * (W - 1);
-            uint32_t idx = 0;
-#pragma unroll
-            for (int j = W - 1; j >= 0; --j) idx = idx * P.radix + (s + j <= D ? u[s + j] : 0u);
-            const uint32_t e = tab[idx];
-#pragma unroll
-            for (int j = 0; j < W; ++j)
-                if (s + j <= D && (j + 1 < W || s + j == D)) mu[s + j] = byte_of(e, j);
+                for (int j = W - 1; j >= 0; --j) idx = idx * c.radix() + (s + j <= D ? u[s + j] : 0u);
+                const uint32_t e = lds_u32(tab_saddr + 4 * idx);
+                const int keep = (a == A - 1) ? (D - s + 1) : (W - 1);  // bytes of this window kept
+                const uint32_t mask = keep >= 4 ? 0xffffffffu : ((1u << (8 * keep)) - 1);
+                rec |= static_cast<uint64_t>(e & mask) << (8 * s);
+            }
+            return rec;
         }
     }
+    uint32_t mu[ND];
+    redq_correct<ND, 0>(c, u, mu, [](uint32_t) { return 0u; });
+    uint64_t rec = 0;
+#pragma unroll
+    for (int j = 0; j < ND; ++j) rec |= static_cast<uint64_t>(mu[j]) << (8 * j);
+    return rec;
 }
 
-// --------------------------------------------------------------------- ops
-// An op maps R consecutive records (IN0 + IN1 bytes each, given as packed
-// little-endian u32 words) to R output records of OUT bytes.
+// ----------------------------------------------------------------- ops
+// An op maps R consecutive records (IN0 + IN1 bytes each, as packed
+// little-endian u32 words) to R output records of OUT bytes (packed u32).
 
-template <int ND, bool POW2, int W>
+template <int ND, int W, class K>
 struct RedqOp {
     static constexpr int IN0 = 8, IN1 = 0, OUT = ND, R = 4;
     RedqParams P;
     __host__ __device__ uint32_t tables_words() const { return W ? P.n_entries : 0u; }
     __host__ __device__ const uint32_t* tables_src() const { return P.table; }
-    __device__ __forceinline__ void apply(const uint32_t* a, const uint32_t*, uint8_t (&o)[R * OUT],
-                                          const uint32_t* tab, uint32_t& err) const {
+    __device__ __forceinline__ void apply(const uint32_t* a, const uint32_t*, uint32_t (&ow)[R * OUT / 4],
+                                          uint32_t tab, uint32_t& err) const {
+        const K c{P};
+        uint64_t rec[R];
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             const double w = __hiloint2double(static_cast<int>(a[2 * r + 1]), static_cast<int>(a[2 * r]));
-            uint32_t u[ND], mu[ND];
-            redq_digits<ND, POW2>(P, w, u, err);
-            redq_correct<ND, W>(P, u, mu, tab);
-#pragma unroll
-            for (int j = 0; j < ND; ++j) o[r * OUT + j] = static_cast<uint8_t>(mu[j]);
+            double x = checked_word(P, w, err);
+            if constexpr (K::kSafe) x = (err & kErrDomain) ? 0.0 : x;  // keep table indices in range
+            rec[r] = redq_record<ND, W>(c, x, tab);
         }
+        pack_records<R, OUT>(rec, ow);
     }
 };
 
-// byte `i` of a run of packed u32 words
-__device__ __forceinline__ uint32_t run_byte(const uint32_t* w, int i) { return byte_of(w[i >> 2], i & 3); }
+// coefficient records: reduce mod p (DensePoly, poly.hpp:19-21) unless every
+// byte is already below p
+template <int K_, class C>
+__device__ __forceinline__ void record_coeffs(const C& c, uint32_t magic, const uint32_t* w, int rec,
+                                              uint32_t (&cf)[K_]) {
+#pragma unroll
+    for (int i = 0; i < K_; ++i) cf[i] = run_byte(w, rec * K_ + i);
+    bool clean = true;
+#pragma unroll
+    for (int i = 0; i < K_; ++i) clean &= cf[i] < c.p();
+    if (!clean) {
+#pragma unroll
+        for (int i = 0; i < K_; ++i) cf[i] = mod_by_magic(cf[i], c.p(), magic);
+    }
+}
 
-template <int K, bool POW2, int W>
+// DQT pack at q (dqt.cpp:23-37): exact integer as a double
+template <int K_, class C>
+__device__ __forceinline__ double pack_word(const C& c, double qd, const uint32_t (&cf)[K_]) {
+    if constexpr (C::kPow2) {
+        uint64_t v = 0;
+#pragma unroll
+        for (int i = K_ - 1; i >= 0; --i) v = (v << c.qbits()) | cf[i];
+        return static_cast<double>(v);
+    } else {
+        double v = 0.0;
+#pragma unroll
+        for (int i = K_ - 1; i >= 0; --i) v = fma(v, qd, static_cast<double>(cf[i]));
+        return v;
+    }
+}
+
+template <int K_, int W, class K>
 struct PolymulOp {
-    static constexpr int ND = 2 * K - 1;
-    static constexpr int IN0 = K, IN1 = K, OUT = ND, R = 4;
+    static constexpr int ND = 2 * K_ - 1;
+    static constexpr int IN0 = K_, IN1 = K_, OUT = ND, R = 4;
     PolymulParams P;
     __host__ __device__ uint32_t tables_words() const { return W ? P.rq.n_entries : 0u; }
     __host__ __device__ const uint32_t* tables_src() const { return P.rq.table; }
-
-    // DQT pack (dqt.cpp:23-37) of one record, coefficients reduced mod p first
-    // as DensePoly's constructor does (poly.hpp:19-21)
-    __device__ __forceinline__ double pack(const uint32_t* w, int rec) const {
-        const RedqParams& Q = P.rq;
-        uint64_t v = 0;
-        double vd = 0.0;
-#pragma unroll
-        for (int i = K - 1; i >= 0; --i) {
-            const uint32_t c = mod_small(run_byte(w, rec * K + i), Q.p, Q.mod_magic);
-            if constexpr (POW2)
-                v = (v << Q.qbits) | c;
-            else
-                vd = fma(vd, static_cast<double>(Q.q), static_cast<double>(c));
-        }
-        return POW2 ? static_cast<double>(v) : vd;
-    }
-
-    __device__ __forceinline__ void apply(const uint32_t* a, const uint32_t* b, uint8_t (&o)[R * OUT],
-                                          const uint32_t* tab, uint32_t& err) const {
+    __device__ __forceinline__ void apply(const uint32_t* a, const uint32_t* b, uint32_t (&ow)[R * OUT / 4],
+                                          uint32_t tab, uint32_t&) const {
+        const K c{P.rq};
+        const double qd = static_cast<double>(P.rq.q);
+        uint64_t rec[R];
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-            const double prod = pack(a, r) * pack(b, r);  // exact: q^(2k-1) < 2^53
-            uint32_t u[ND], mu[ND];
-            redq_digits<ND, POW2>(P.rq, prod, u, err);
-            redq_correct<ND, W>(P.rq, u, mu, tab);
-#pragma unroll
-            for (int j = 0; j < ND; ++j) o[r * OUT + j] = static_cast<uint8_t>(mu[j]);
+            uint32_t ca[K_], cb[K_];
+            record_coeffs<K_>(c, P.rq.mod_magic, a, r, ca);
+            record_coeffs<K_>(c, P.rq.mod_magic, b, r, cb);
+            // exact: q^(2k-1) < 2^53 (validated)
+            rec[r] = redq_record<ND, W>(c, pack_word<K_>(c, qd, ca) * pack_word<K_>(c, qd, cb), tab);
         }
+        pack_records<R, OUT>(rec, ow);
     }
 };
 
-// bytewise (x + y) mod p for packed coefficient bytes, each < p
+// bytewise (x + y) mod p of packed coefficient bytes, each < p
 __device__ __forceinline__ uint32_t add_mod_bytes(uint32_t x, uint32_t y, uint32_t p, uint32_t k) {
     if (p < 128) {
         const uint32_t pp = p * 0x01010101u;
@@ -199,81 +183,59 @@ __device__ __forceinline__ uint32_t add_mod_bytes(uint32_t x, uint32_t y, uint32
     return r;
 }
 
-template <int K, bool POW2>
+template <int K_, class K>
 struct GfqElemOp {
-    static constexpr int ND = 2 * K - 1;
-    static constexpr int IN0 = K, IN1 = K, OUT = K, R = 4;
+    static constexpr int ND = 2 * K_ - 1;
+    static constexpr int IN0 = K_, IN1 = K_, OUT = K_, R = 4;
     GfqElemParams P;
     __host__ __device__ uint32_t tables_words() const { return P.tables_words; }
     __host__ __device__ const uint32_t* tables_src() const { return P.lc; }  // lc|hc|log|alog contiguous
 
-    __device__ __forceinline__ void apply(const uint32_t* a, const uint32_t* b, uint8_t (&o)[R * OUT],
-                                          const uint32_t* tab, uint32_t& err) const {
-        const uint32_t p = P.p, magic = P.rq.mod_magic;
+    __device__ __forceinline__ void apply(const uint32_t* a, const uint32_t* b, uint32_t (&ow)[R * OUT / 4],
+                                          uint32_t tab, uint32_t&) const {
+        const K c{P.rq};
         uint32_t nlh = 1;
 #pragma unroll
-        for (int i = 0; i < K; ++i) nlh *= P.lh_radix;
-        const uint32_t* lc = tab;
-        const uint32_t* hc = tab + nlh;
-        const uint32_t* lg = tab + 2 * nlh;
-        const uint32_t* al = tab + 2 * nlh + P.order;
+        for (int i = 0; i < K_; ++i) nlh *= P.lh_radix;
+        const uint32_t lc = tab, hc = tab + 4 * nlh, lg = tab + 8 * nlh, al = tab + 8 * nlh + 4 * P.order;
+        uint64_t rec[R];
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-            uint32_t ca[K], cb[K];
-#pragma unroll
-            for (int i = 0; i < K; ++i) {
-                ca[i] = mod_small(run_byte(a, r * K + i), p, magic);
-                cb[i] = mod_small(run_byte(b, r * K + i), p, magic);
-            }
+            uint32_t ca[K_], cb[K_];
+            record_coeffs<K_>(c, P.rq.mod_magic, a, r, ca);
+            record_coeffs<K_>(c, P.rq.mod_magic, b, r, cb);
             uint32_t res;
             if (P.mode == 0) {
                 // paper Alg. 4 with one term: pack, fp64 product, REDQ digits,
-                // low/high half tables (gfq.cpp:353-381) -- here the tables give
-                // coefficient vectors and the two halves add coefficient-wise
-                double va = 0.0, vb = 0.0;
-                if constexpr (POW2) {
-                    uint64_t ia = 0, ib = 0;
-#pragma unroll
-                    for (int i = K - 1; i >= 0; --i) {
-                        ia = (ia << P.rq.qbits) | ca[i];
-                        ib = (ib << P.rq.qbits) | cb[i];
-                    }
-                    va = static_cast<double>(ia);
-                    vb = static_cast<double>(ib);
-                } else {
-#pragma unroll
-                    for (int i = K - 1; i >= 0; --i) {
-                        va = fma(va, P.qd, static_cast<double>(ca[i]));
-                        vb = fma(vb, P.qd, static_cast<double>(cb[i]));
-                    }
-                }
+                // low/high half tables (gfq.cpp:353-381); the tables give
+                // coefficient vectors, so the halves add coefficient-wise
                 uint32_t u[ND];
-                redq_digits<ND, POW2>(P.rq, va * vb, u, err);
+                redq_raw_digits<ND>(c, pack_word<K_>(c, P.qd, ca) * pack_word<K_>(c, P.qd, cb), u);
                 uint32_t il = 0, ih = 0;
 #pragma unroll
-                for (int i = K - 1; i >= 0; --i) {
+                for (int i = K_ - 1; i >= 0; --i) {
                     il = il * P.lh_radix + u[i];
-                    ih = ih * P.lh_radix + u[K - 1 + i];
+                    ih = ih * P.lh_radix + u[K_ - 1 + i];
                 }
-                res = add_mod_bytes(lc[il], hc[ih], p, K);
+                res = add_mod_bytes(lds_u32(lc + 4 * il), lds_u32(hc + 4 * ih), c.p(), K_);
             } else {
-                // dlog representation: rep(a*b) = rep(a) + rep(b) mod p^k-1 with
-                // the zero sentinel (gfq.cpp:260-264), then back to coefficients
+                // dlog representation: rep(a*b) = rep(a) + rep(b) mod p^k-1,
+                // zero sentinel (gfq.cpp:260-264), then back to coefficients
                 uint32_t ia = 0, ib = 0;
 #pragma unroll
-                for (int i = K - 1; i >= 0; --i) {
-                    ia = ia * p + ca[i];
-                    ib = ib * p + cb[i];
+                for (int i = K_ - 1; i >= 0; --i) {
+                    ia = ia * c.p() + ca[i];
+                    ib = ib * c.p() + cb[i];
                 }
-                const uint32_t ra = lg[ia], rb = lg[ib];
+                const uint32_t ra = lds_u32(lg + 4 * ia), rb = lds_u32(lg + 4 * ib);
                 uint32_t rc = ra + rb;
                 if (rc >= P.group) rc -= P.group;
                 if (ra == P.group || rb == P.group) rc = P.group;
-                res = al[rc];
+                res = lds_u32(al + 4 * rc);
             }
-#pragma unroll
-            for (int j = 0; j < K; ++j) o[r * OUT + j] = static_cast<uint8_t>(byte_of(res, j));
+            rec[r] = res;
         }
+        pack_records<R, OUT>(rec, ow);
     }
 };
 
@@ -293,7 +255,7 @@ struct Geometry {
     static constexpr size_t smem_fixed = size_t(kStages) * (B0 + B1) + size_t(kOutStages) * BO + kStages * 8;
 };
 
-// load `N` u32 words at smem+off with the widest conflict-light vector
+// `N` u32 words from shared memory with the widest vector that divides N
 template <int N>
 __device__ __forceinline__ void lds_run(const uint8_t* base, uint32_t (&w)[N > 0 ? N : 1]) {
     if constexpr (N == 0) {
@@ -308,14 +270,6 @@ __device__ __forceinline__ void lds_run(const uint8_t* base, uint32_t (&w)[N > 0
 #pragma unroll
         for (int i = 0; i < N; ++i) w[i] = reinterpret_cast<const uint32_t*>(base)[i];
     }
-}
-
-template <int N>
-__device__ __forceinline__ void pack_out(const uint8_t (&o)[4 * N], uint32_t (&w)[N]) {
-#pragma unroll
-    for (int i = 0; i < N; ++i)
-        w[i] = uint32_t(o[4 * i]) | (uint32_t(o[4 * i + 1]) << 8) | (uint32_t(o[4 * i + 2]) << 16) |
-               (uint32_t(o[4 * i + 3]) << 24);
 }
 
 __device__ __forceinline__ void report(uint32_t err, uint32_t* status) {
@@ -341,6 +295,7 @@ __global__ void __launch_bounds__(kThreads) stream_tma_kernel(const Op op, const
     uint8_t* s_out = smem + size_t(kStages) * (G::B0 + G::B1);
     uint64_t* bars = reinterpret_cast<uint64_t*>(s_out + size_t(kOutStages) * G::BO);
     uint32_t* s_tab = reinterpret_cast<uint32_t*>(bars + kStages);
+    const uint32_t tab = smem_addr(s_tab);
     const int tid = threadIdx.x;
 
     stage_tables(op, s_tab);
@@ -378,10 +333,8 @@ __global__ void __launch_bounds__(kThreads) stream_tma_kernel(const Op op, const
         uint32_t a[G::W0 > 0 ? G::W0 : 1], b[G::W1 > 0 ? G::W1 : 1];
         lds_run<G::W0>(src + tid * (G::R * Op::IN0), a);
         lds_run<G::W1>(src + G::B0 + tid * (G::R * Op::IN1), b);
-        uint8_t o[G::R * Op::OUT];
-        op.apply(a, b, o, s_tab, err);
         uint32_t ow[G::WO];
-        pack_out<G::WO>(o, ow);
+        op.apply(a, b, ow, tab, err);
         uint32_t* dst = reinterpret_cast<uint32_t*>(s_out + size_t(os) * G::BO) + tid * G::WO;
 #pragma unroll
         for (int i = 0; i < G::WO; ++i) dst[i] = ow[i];
@@ -410,6 +363,7 @@ __global__ void __launch_bounds__(kThreads) stream_tail_kernel(const Op op, cons
     uint32_t* s_tab = reinterpret_cast<uint32_t*>(smem);
     stage_tables(op, s_tab);
     __syncthreads();
+    const uint32_t tab = smem_addr(s_tab);
     uint32_t err = 0;
     const uint64_t stride = uint64_t(gridDim.x) * blockDim.x * G::R;
     for (uint64_t base = first + (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) * G::R; base < n;
@@ -418,10 +372,10 @@ __global__ void __launch_bounds__(kThreads) stream_tail_kernel(const Op op, cons
         uint32_t a[G::W0 > 0 ? G::W0 : 1] = {}, b[G::W1 > 0 ? G::W1 : 1] = {};
         for (int i = 0; i < cnt * Op::IN0; ++i) a[i >> 2] |= uint32_t(in0[base * Op::IN0 + i]) << (8 * (i & 3));
         for (int i = 0; i < cnt * Op::IN1; ++i) b[i >> 2] |= uint32_t(in1[base * Op::IN1 + i]) << (8 * (i & 3));
-        uint8_t o[G::R * Op::OUT];
+        uint32_t ow[G::WO];
         // zero padding is a valid input for every op, so it never raises
-        op.apply(a, b, o, s_tab, err);
-        for (int i = 0; i < cnt * Op::OUT; ++i) out[base * Op::OUT + i] = o[i];
+        op.apply(a, b, ow, tab, err);
+        for (int i = 0; i < cnt * Op::OUT; ++i) out[base * Op::OUT + i] = static_cast<uint8_t>(ow[i >> 2] >> (8 * (i & 3)));
     }
     report(err, status);
 }
@@ -473,47 +427,69 @@ cudaError_t run_stream(const Op& op, const uint8_t* in0, const uint8_t* in1, uin
     return cudaSuccess;
 }
 
+// compile-time fast paths for the benchmark fields (BASELINE configs):
+//   C2  REDQ   p=5, q=2^7,  7 digits, window 4
+//   C1  polymul p=3, q=2^5,  k=4, window 4
+//   C3  GF(7^3) p=7, q=2^8,  k=3
+// safe = every word of the plan stays <= min(r_max, 2^52)
+inline bool plan_is_safe(const RedqParams& P) {
+    return P.qbits && P.limit <= P.r_max + 1.0 && P.limit <= kTwo52;
+}
+
 template <int ND, bool POW2>
-cudaError_t redq_dispatch_w(const RedqParams& P, const double* w, uint64_t n, uint8_t* out, uint32_t* st,
+cudaError_t redq_dispatch_pow2(const RedqParams& P, const double* w, uint64_t n, uint8_t* out, uint32_t* st,
                             cudaStream_t s) {
     const auto* in = reinterpret_cast<const uint8_t*>(w);
+    if constexpr (ND == 7 && POW2) {
+        if (P.p == 5 && P.qbits == 7 && P.window == 4 && P.radix == 5 && plan_is_safe(P))
+            return run_stream(RedqOp<7, 4, CtConst<5, 7>>{P}, in, nullptr, out, n, st, s);
+    }
     switch (P.window) {
-        case 2: return run_stream(RedqOp<ND, POW2, 2>{P}, in, nullptr, out, n, st, s);
-        case 3: return run_stream(RedqOp<ND, POW2, 3>{P}, in, nullptr, out, n, st, s);
-        case 4: return run_stream(RedqOp<ND, POW2, 4>{P}, in, nullptr, out, n, st, s);
-        default: return run_stream(RedqOp<ND, POW2, 0>{P}, in, nullptr, out, n, st, s);
+        case 2: return run_stream(RedqOp<ND, 2, RtConst<POW2>>{P}, in, nullptr, out, n, st, s);
+        case 3: return run_stream(RedqOp<ND, 3, RtConst<POW2>>{P}, in, nullptr, out, n, st, s);
+        case 4: return run_stream(RedqOp<ND, 4, RtConst<POW2>>{P}, in, nullptr, out, n, st, s);
+        default: return run_stream(RedqOp<ND, 0, RtConst<POW2>>{P}, in, nullptr, out, n, st, s);
     }
 }
 
 template <int ND>
 cudaError_t redq_dispatch_q(const RedqParams& P, const double* w, uint64_t n, uint8_t* out, uint32_t* st,
                             cudaStream_t s) {
-    return P.qbits ? redq_dispatch_w<ND, true>(P, w, n, out, st, s) : redq_dispatch_w<ND, false>(P, w, n, out, st, s);
+    return P.qbits ? redq_dispatch_pow2<ND, true>(P, w, n, out, st, s)
+                   : redq_dispatch_pow2<ND, false>(P, w, n, out, st, s);
 }
 
-template <int K, bool POW2>
+template <int K_, bool POW2>
 cudaError_t polymul_dispatch_w(const PolymulParams& P, const uint8_t* a, const uint8_t* b, uint64_t n, uint8_t* out,
                                uint32_t* st, cudaStream_t s) {
+    if constexpr (K_ == 4 && POW2) {
+        if (P.rq.p == 3 && P.rq.qbits == 5 && P.rq.window == 4 && P.rq.radix == 3 && plan_is_safe(P.rq))
+            return run_stream(PolymulOp<4, 4, CtConst<3, 5>>{P}, a, b, out, n, st, s);
+    }
     switch (P.rq.window) {
-        case 2: return run_stream(PolymulOp<K, POW2, 2>{P}, a, b, out, n, st, s);
-        case 3: return run_stream(PolymulOp<K, POW2, 3>{P}, a, b, out, n, st, s);
-        case 4: return run_stream(PolymulOp<K, POW2, 4>{P}, a, b, out, n, st, s);
-        default: return run_stream(PolymulOp<K, POW2, 0>{P}, a, b, out, n, st, s);
+        case 2: return run_stream(PolymulOp<K_, 2, RtConst<POW2>>{P}, a, b, out, n, st, s);
+        case 3: return run_stream(PolymulOp<K_, 3, RtConst<POW2>>{P}, a, b, out, n, st, s);
+        case 4: return run_stream(PolymulOp<K_, 4, RtConst<POW2>>{P}, a, b, out, n, st, s);
+        default: return run_stream(PolymulOp<K_, 0, RtConst<POW2>>{P}, a, b, out, n, st, s);
     }
 }
 
-template <int K>
+template <int K_>
 cudaError_t polymul_dispatch_q(const PolymulParams& P, const uint8_t* a, const uint8_t* b, uint64_t n,
                                uint8_t* out, uint32_t* st, cudaStream_t s) {
-    return P.rq.qbits ? polymul_dispatch_w<K, true>(P, a, b, n, out, st, s)
-                      : polymul_dispatch_w<K, false>(P, a, b, n, out, st, s);
+    return P.rq.qbits ? polymul_dispatch_w<K_, true>(P, a, b, n, out, st, s)
+                      : polymul_dispatch_w<K_, false>(P, a, b, n, out, st, s);
 }
 
-template <int K>
+template <int K_>
 cudaError_t gfq_elem_dispatch(const GfqElemParams& P, const uint8_t* a, const uint8_t* b, uint64_t n,
                               uint8_t* out, cudaStream_t s) {
-    return P.rq.qbits ? run_stream(GfqElemOp<K, true>{P}, a, b, out, n, nullptr, s)
-                      : run_stream(GfqElemOp<K, false>{P}, a, b, out, n, nullptr, s);
+    if constexpr (K_ == 3) {
+        if (P.p == 7 && P.rq.qbits == 8 && plan_is_safe(P.rq))
+            return run_stream(GfqElemOp<3, CtConst<7, 8>>{P}, a, b, out, n, nullptr, s);
+    }
+    return P.rq.qbits ? run_stream(GfqElemOp<K_, RtConst<true>>{P}, a, b, out, n, nullptr, s)
+                      : run_stream(GfqElemOp<K_, RtConst<false>>{P}, a, b, out, n, nullptr, s);
 }
 
 }  // namespace
