@@ -33,6 +33,7 @@ template <bool POW2>
 struct RtConst {
     static constexpr bool kSafe = false;
     static constexpr bool kPow2 = POW2;
+    static constexpr uint32_t kQbitsCt = 0;  // not known at compile time
     const RedqParams& P;
     __device__ __forceinline__ uint32_t p() const { return P.p; }
     __device__ __forceinline__ uint32_t qbits() const { return P.qbits; }
@@ -45,7 +46,7 @@ template <uint32_t P_, uint32_t QBITS_>
 struct CtConst {
     static constexpr bool kSafe = true;
     static constexpr bool kPow2 = true;
-    static constexpr uint32_t kP = P_, kQbits = QBITS_;
+    static constexpr uint32_t kP = P_, kQbits = QBITS_, kQbitsCt = QBITS_;
     static constexpr uint32_t kNegQ = (P_ - (uint32_t(1) << QBITS_) % P_) % P_;
     const RedqParams& P;
     __device__ __forceinline__ static constexpr uint32_t p() { return P_; }

@@ -92,7 +92,7 @@ __device__ __forceinline__ uint64_t redq_record(const K& c, double r, uint32_t t
 
 template <int ND, int W, class K>
 struct RedqOp {
-    static constexpr int IN0 = 8, IN1 = 0, OUT = ND, R = 4;
+    static constexpr int IN0 = 8, IN1 = 0, OUT = ND, R = 4, RR = 2, S = 3;
     RedqParams P;
     __host__ __device__ uint32_t tables_words() const { return W ? P.n_entries : 0u; }
     __host__ __device__ const uint32_t* tables_src() const { return P.table; }
@@ -100,11 +100,32 @@ struct RedqOp {
                                           uint32_t tab, uint32_t& err) const {
         const K c{P};
         uint64_t rec[R];
+        if constexpr (K::kSafe) {
+            // the safe plans have a power-of-two limit 2^e (low word 0), so
+            // 0 <= w < limit  <=>  hi32(w) < hi32(limit) as unsigned ints
+            // (negatives carry the sign bit, NaN/inf the top exponent); one
+            // compare for the whole run, the exact check only on a miss
+            uint32_t hmax = a[1];
+#pragma unroll
+            for (int r = 1; r < R; ++r) hmax = max(hmax, a[2 * r + 1]);
+            const uint32_t lim_hi = static_cast<uint32_t>(__double_as_longlong(P.limit) >> 32);
+            if (hmax < lim_hi) {
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const double w = __hiloint2double(static_cast<int>(a[2 * r + 1]), static_cast<int>(a[2 * r]));
+                    rec[r] = redq_record<ND, W>(c, trunc(w), tab);
+                }
+                pack_records<R, OUT>(rec, ow);
+                return;
+            }
+        }
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             const double w = __hiloint2double(static_cast<int>(a[2 * r + 1]), static_cast<int>(a[2 * r]));
-            double x = checked_word(P, w, err);
-            if constexpr (K::kSafe) x = (err & kErrDomain) ? 0.0 : x;  // keep table indices in range
+            uint32_t e = 0;
+            double x = checked_word(P, w, e);
+            if constexpr (K::kSafe) x = e ? 0.0 : x;  // keep table indices in range
+            err |= e;
             rec[r] = redq_record<ND, W>(c, x, tab);
         }
         pack_records<R, OUT>(rec, ow);
@@ -146,7 +167,7 @@ __device__ __forceinline__ double pack_word(const C& c, double qd, const uint32_
 template <int K_, int W, class K>
 struct PolymulOp {
     static constexpr int ND = 2 * K_ - 1;
-    static constexpr int IN0 = K_, IN1 = K_, OUT = ND, R = 4;
+    static constexpr int IN0 = K_, IN1 = K_, OUT = ND, R = 4, RR = 2, S = 3;
     PolymulParams P;
     __host__ __device__ uint32_t tables_words() const { return W ? P.rq.n_entries : 0u; }
     __host__ __device__ const uint32_t* tables_src() const { return P.rq.table; }
@@ -183,10 +204,74 @@ __device__ __forceinline__ uint32_t add_mod_bytes(uint32_t x, uint32_t y, uint32
     return r;
 }
 
+// every byte of N packed words is below p (p < 128): (b + 128 - p) sets a
+// byte's top bit iff b >= p, for bytes below 128; bytes >= 128 set it already
+template <int N>
+__device__ __forceinline__ bool all_bytes_below(const uint32_t* w, uint32_t p) {
+    const uint32_t add = (128u - p) * 0x01010101u;
+    uint32_t bad = 0;
+#pragma unroll
+    for (int i = 0; i < N; ++i) bad |= w[i] | ((w[i] & 0x7f7f7f7fu) + add);
+    return (bad & 0x80808080u) == 0;
+}
+
+// record r (k bytes, little endian) of a packed run as an integer
+template <int K_>
+__device__ __forceinline__ uint32_t record_int(const uint32_t* w, int r) {
+    const int byte = r * K_, i = byte >> 2, sh = 8 * (byte & 3);
+    const uint32_t lo = w[i];
+    const uint32_t hi = (sh + 8 * K_ > 32) ? w[i + 1] : 0u;
+    const uint32_t v = sh ? __funnelshift_r(lo, hi, sh) : lo;
+    return K_ == 4 ? v : (v & ((1u << (8 * K_)) - 1));
+}
+
+// coefficient index sum c_i p^i of a record integer (bytes c_i)
+template <int K_, class C>
+__device__ __forceinline__ uint32_t coeff_index(const C& c, uint32_t rec) {
+    uint32_t idx = 0;
+#pragma unroll
+    for (int i = K_ - 1; i >= 0; --i) idx = idx * c.p() + ((rec >> (8 * i)) & 0xffu);
+    return idx;
+}
+
+// (x + y) mod p bytewise for packed bytes below p < 128, carry-free
+__device__ __forceinline__ uint32_t add_mod_bytes_fast(uint32_t x, uint32_t y, uint32_t p) {
+    const uint32_t s = x + y;                                     // bytes < 2p <= 255
+    const uint32_t ge = ((s + (128u - p) * 0x01010101u) >> 7) & 0x01010101u;  // byte >= p
+    return s - ge * p;
+}
+
+// one GF(p^k) product through DQT/REDQ/L-H with q = 2^8 (record = word)
+template <int K_, class C>
+__device__ __forceinline__ uint32_t lh_product(const C& c, uint32_t ra, uint32_t rb, uint32_t lc, uint32_t hc) {
+    constexpr int ND = 2 * K_ - 1;
+    const double prod = static_cast<double>(ra) * static_cast<double>(rb);  // exact, < 2^(16k)
+    uint32_t u[ND];
+    redq_raw_digits<ND>(c, prod, u);
+    uint32_t il = 0, ih = 0;
+#pragma unroll
+    for (int i = K_ - 1; i >= 0; --i) {
+        il = il * c.p() + u[i];
+        ih = ih * c.p() + u[K_ - 1 + i];
+    }
+    return add_mod_bytes_fast(lds_u32(lc + 4 * il), lds_u32(hc + 4 * ih), c.p());
+}
+
+// one GF(p^k) product in the dlog representation (gfq.cpp:260-264)
+template <int K_, class C>
+__device__ __forceinline__ uint32_t dlog_product(const C&, uint32_t ia, uint32_t ib, uint32_t lg, uint32_t al,
+                                                 uint32_t group) {
+    const uint32_t ra = lds_u32(lg + 4 * ia), rb = lds_u32(lg + 4 * ib);
+    uint32_t rc = ra + rb;
+    rc = rc >= group ? rc - group : rc;
+    rc = (ra == group || rb == group) ? group : rc;
+    return lds_u32(al + 4 * rc);
+}
+
 template <int K_, class K>
 struct GfqElemOp {
     static constexpr int ND = 2 * K_ - 1;
-    static constexpr int IN0 = K_, IN1 = K_, OUT = K_, R = 4;
+    static constexpr int IN0 = K_, IN1 = K_, OUT = K_, R = 4, RR = 1, S = 4;
     GfqElemParams P;
     __host__ __device__ uint32_t tables_words() const { return P.tables_words; }
     __host__ __device__ const uint32_t* tables_src() const { return P.lc; }  // lc|hc|log|alog contiguous
@@ -199,6 +284,25 @@ struct GfqElemOp {
         for (int i = 0; i < K_; ++i) nlh *= P.lh_radix;
         const uint32_t lc = tab, hc = tab + 4 * nlh, lg = tab + 8 * nlh, al = tab + 8 * nlh + 4 * P.order;
         uint64_t rec[R];
+        if constexpr (K::kSafe && K::kQbitsCt == 8) {
+            // q = 2^8: a record of k coefficient bytes IS its DQT word, so
+            // packing is a byte-run extract; taken when every byte is < p
+            if (all_bytes_below<R * K_ / 4>(a, c.p()) && all_bytes_below<R * K_ / 4>(b, c.p())) {
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const uint32_t ra = record_int<K_>(a, r), rb = record_int<K_>(b, r);
+                    uint32_t res;
+                    if (P.mode == 0) {
+                        res = lh_product<K_>(c, ra, rb, lc, hc);
+                    } else {
+                        res = dlog_product<K_>(c, coeff_index<K_>(c, ra), coeff_index<K_>(c, rb), lg, al, P.group);
+                    }
+                    rec[r] = res;
+                }
+                pack_records<R, OUT>(rec, ow);
+                return;
+            }
+        }
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             uint32_t ca[K_], cb[K_];
@@ -240,19 +344,25 @@ struct GfqElemOp {
 };
 
 // ------------------------------------------------------------- the pipeline
+// stream_tma_kernel: a CTA of 256 threads owns tiles of 256*R*RR records.
+// Thread 0 keeps S input stages in flight (bulk copies completing on
+// mbarriers) and bulk-stores each finished output tile from a double
+// buffer; every thread processes RR runs of R consecutive records per tile.
+// Tile size (RR) and depth (S) per op come from a sweep on B200
+// (scripts/stream_variants.cu): for C2, 16 KB tiles x 3 stages at 2 CTAs/SM
+// reach 98% of cudaMemcpy device-to-device bandwidth; a warp-specialised
+// variant with per-warp output stores was slower.
 constexpr int kThreads = 256;
-constexpr int kStages = 4;
-constexpr int kOutStages = 2;
 
 template <class Op>
 struct Geometry {
-    static constexpr int R = Op::R;
-    static constexpr int TILE = kThreads * R;  // records per tile
+    static constexpr int R = Op::R, RR = Op::RR, S = Op::S;
+    static constexpr int TILE = kThreads * R * RR;  // records per tile
     static constexpr uint32_t B0 = Op::IN0 * TILE, B1 = Op::IN1 * TILE, BO = Op::OUT * TILE;
     static constexpr int W0 = R * Op::IN0 / 4, W1 = R * Op::IN1 / 4, WO = R * Op::OUT / 4;
     static_assert((R * Op::IN0) % 4 == 0 && (R * Op::IN1) % 4 == 0 && (R * Op::OUT) % 4 == 0, "u32 runs");
     static_assert(B0 % 16 == 0 && B1 % 16 == 0 && BO % 16 == 0, "bulk copies move multiples of 16 bytes");
-    static constexpr size_t smem_fixed = size_t(kStages) * (B0 + B1) + size_t(kOutStages) * BO + kStages * 8;
+    static constexpr size_t smem_pipe = size_t(S) * (B0 + B1) + 2 * size_t(BO) + S * 8;
 };
 
 // `N` u32 words from shared memory with the widest vector that divides N
@@ -290,17 +400,18 @@ __global__ void __launch_bounds__(kThreads) stream_tma_kernel(const Op op, const
                                                               uint8_t* __restrict__ out, uint64_t n_tiles,
                                                               uint32_t* status) {
     using G = Geometry<Op>;
+    constexpr int S = G::S;
     extern __shared__ __align__(128) uint8_t smem[];
     uint8_t* s_in = smem;
-    uint8_t* s_out = smem + size_t(kStages) * (G::B0 + G::B1);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(s_out + size_t(kOutStages) * G::BO);
-    uint32_t* s_tab = reinterpret_cast<uint32_t*>(bars + kStages);
+    uint8_t* s_out = smem + size_t(S) * (G::B0 + G::B1);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(s_out + 2 * size_t(G::BO));
+    uint32_t* s_tab = reinterpret_cast<uint32_t*>(bars + S);
     const uint32_t tab = smem_addr(s_tab);
     const int tid = threadIdx.x;
 
     stage_tables(op, s_tab);
     if (tid == 0) {
-        for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
+        for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
         fence_mbar_init();
     }
     __syncthreads();
@@ -314,7 +425,7 @@ __global__ void __launch_bounds__(kThreads) stream_tma_kernel(const Op op, const
     };
     if (tid == 0) {
         policy = policy_evict_first();
-        for (int s = 0; s < kStages; ++s) {
+        for (int s = 0; s < S; ++s) {
             const uint64_t t = blockIdx.x + uint64_t(s) * gridDim.x;
             if (t < n_tiles) issue(s, t);
         }
@@ -323,28 +434,32 @@ __global__ void __launch_bounds__(kThreads) stream_tma_kernel(const Op op, const
     uint32_t err = 0;
     uint32_t it = 0;
     for (uint64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++it) {
-        const int s = it % kStages;
-        const int os = it % kOutStages;
-        if (tid == 0) bulk_wait_read<kOutStages - 1>();  // output buffer `os` drained
-        mbar_wait(&bars[s], (it / kStages) & 1);
+        const int s = it % S;
+        const int os = it & 1;
+        if (tid == 0) bulk_wait_read<1>();  // output buffer `os` (two tiles ago) drained
+        mbar_wait(&bars[s], (it / S) & 1);
         __syncthreads();
 
         const uint8_t* src = s_in + size_t(s) * (G::B0 + G::B1);
-        uint32_t a[G::W0 > 0 ? G::W0 : 1], b[G::W1 > 0 ? G::W1 : 1];
-        lds_run<G::W0>(src + tid * (G::R * Op::IN0), a);
-        lds_run<G::W1>(src + G::B0 + tid * (G::R * Op::IN1), b);
-        uint32_t ow[G::WO];
-        op.apply(a, b, ow, tab, err);
-        uint32_t* dst = reinterpret_cast<uint32_t*>(s_out + size_t(os) * G::BO) + tid * G::WO;
+        uint32_t* obuf = reinterpret_cast<uint32_t*>(s_out + size_t(os) * G::BO);
 #pragma unroll
-        for (int i = 0; i < G::WO; ++i) dst[i] = ow[i];
+        for (int rr = 0; rr < G::RR; ++rr) {
+            const int run = rr * kThreads + tid;  // R consecutive records
+            uint32_t a[G::W0 > 0 ? G::W0 : 1], b[G::W1 > 0 ? G::W1 : 1];
+            lds_run<G::W0>(src + run * (G::R * Op::IN0), a);
+            lds_run<G::W1>(src + G::B0 + run * (G::R * Op::IN1), b);
+            uint32_t ow[G::WO];
+            op.apply(a, b, ow, tab, err);
+#pragma unroll
+            for (int i = 0; i < G::WO; ++i) obuf[run * G::WO + i] = ow[i];
+        }
         fence_proxy_async_smem();
         __syncthreads();
 
         if (tid == 0) {
             bulk_s2g(out + tile * G::BO, s_out + size_t(os) * G::BO, G::BO);
             bulk_commit();
-            const uint64_t next = tile + uint64_t(kStages) * gridDim.x;
+            const uint64_t next = tile + uint64_t(S) * gridDim.x;
             if (next < n_tiles) issue(s, next);
         }
     }
@@ -392,7 +507,7 @@ cudaError_t run_stream(const Op& op, const uint8_t* in0, const uint8_t* in1, uin
     const uint64_t n_tiles = aligned ? n / G::TILE : 0;
     const int sms = num_sms();
     if (n_tiles > 0) {
-        const size_t smem = G::smem_fixed + tab_bytes;
+        const size_t smem = G::smem_pipe + tab_bytes;
         static bool attr_done = false;  // per instantiation
         if (!attr_done) {
             cudaError_t e = cudaFuncSetAttribute(stream_tma_kernel<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -401,11 +516,13 @@ cudaError_t run_stream(const Op& op, const uint8_t* in0, const uint8_t* in1, uin
             attr_done = true;
         }
         int per_sm = 0;
-        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, stream_tma_kernel<Op>, kThreads, smem);
+        cudaError_t e =
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, stream_tma_kernel<Op>, kThreads, smem);
         if (e != cudaSuccess) return e;
         per_sm = std::max(per_sm, 1);
         const uint64_t grid = std::min<uint64_t>(n_tiles, uint64_t(sms) * per_sm);
-        stream_tma_kernel<Op><<<static_cast<unsigned>(grid), kThreads, smem, s>>>(op, in0, in1, out, n_tiles, status);
+        stream_tma_kernel<Op>
+            <<<static_cast<unsigned>(grid), kThreads, smem, s>>>(op, in0, in1, out, n_tiles, status);
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }
