@@ -37,15 +37,14 @@ CXX_UNITS = ["capi.cpp"] + [f"host/{f}" for f in
 
 
 def _ninja_text() -> str:
-    hdrs_cu = " ".join(os.path.join(CSRC, h) for h in
-                       ("device_common.cuh", "kernels.hpp", "stream_kernels.cuh", "stream_inst.hpp", "gfq_matmul.cuh",
-                        "redq_core.cuh"))
     lines = [
         f"nvcc = {NVCC}",
         f"nvflags = {NVCC_FLAGS}",
         f"cxxflags = {CXX_FLAGS}",
         "rule nvcc",
-        "  command = $nvcc $nvflags $defs -c $in -o $out",
+        "  command = $nvcc $nvflags $defs -MD -MF $out.d -c $in -o $out",
+        "  depfile = $out.d",
+        "  deps = gcc",
         "  description = NVCC $out",
         "rule cxx",
         "  command = g++ $cxxflags -MMD -MF $out.d -c $in -o $out",
@@ -63,7 +62,7 @@ def _ninja_text() -> str:
         else:
             tag, defs = (f"_{inst}", f"-DQPK_INST={inst}") if inst else ("", "")
         obj = os.path.join(BUILD, os.path.splitext(src)[0] + tag + ".o")
-        lines.append(f"build {obj}: nvcc {os.path.join(CSRC, src)} | {hdrs_cu}")
+        lines.append(f"build {obj}: nvcc {os.path.join(CSRC, src)}")
         if defs:
             lines.append(f"  defs = {defs}")
         objs.append(obj)

@@ -37,14 +37,17 @@ namespace qpk {
 
 namespace {
 
-constexpr int BM = 128, BN = 128, BK = 16, STAGES = 4, PAD = 4;
+constexpr int BM = 128, BN = 128, BK = 16, PAD = 4;
 constexpr int LDS_ = BM + PAD;            // shared row stride in doubles (== BN + PAD)
 constexpr int NCW = 8;                    // consumer warps
 constexpr int THREADS = (NCW + 1) * 32;   // + producer warp
 constexpr int WM = 64, WN = 32;           // warp tile
 constexpr int MT = WM / 8, NT = WN / 8;   // 8 x 4 DMMA tiles per warp
 constexpr size_t STAGE_DOUBLES = size_t(2) * BK * LDS_;
-constexpr size_t SMEM_BYTES = STAGES * STAGE_DOUBLES * 8 + 2 * STAGES * 8;
+// NST pipeline stages: 6 for the compile-time fast paths (deeper buffering
+// lets one warp of a sub-partition run ahead while the other re-packs), 4
+// for the generic kernels (leaves shared memory for large field tables)
+constexpr size_t smem_bytes(int nst) { return nst * STAGE_DOUBLES * 8 + 2 * nst * 8; }
 
 __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -75,6 +78,52 @@ __device__ __forceinline__ double redq_repack(const K& c, double r) {
         for (int i = ND - 1; i >= 0; --i) v = fma(v, qd, static_cast<double>(mu[i]));
         return v;
     }
+}
+
+// The same REDQ + re-pack for p = 3 and q = 2^B with B even (q == 1 mod 3),
+// computed lane-wise inside one 64-bit integer (lane i = bits [Bi, Bi+B)):
+//  * u_i in [0, 2] is fixed by its value mod 4, and
+//    u_i = (r >> Bi) - 3 (rop >> Bi) == a_i + b_i (mod 4) with a_i, b_i the
+//    two low bits of lane i of r and rop (-3 == 1 mod 4): one masked add
+//    produces every lane's u_i (lane sums <= 6 never reach the next lane);
+//  * mu_i = u_i + neg_q u_{i+1} = u_i - u_{i+1} (mod 3): with
+//    V = u_i + 8 - u_{i+1} in [6, 10] and g = [V >= 8], mu_i = V - 5 - 3g
+//    (every lane stays non-negative, so no borrow crosses lanes);
+//  * the mu lanes already sit at q^i: the re-packed word, no assembly.
+// rop = floor(r/3) is still the one premultiplied fp64 floor of Lemma 1.
+template <int ND, uint32_t B>
+__device__ __forceinline__ double redq_repack_swar3(const RedqParams& P, double r) {
+    static_assert(B % 2 == 0 && B >= 4 && B * (ND - 1) + 3 <= 52, "lanes of >= 4 bits below 2^52");
+    constexpr uint64_t M1 = [] {
+        uint64_t m = 0;
+        for (int i = 0; i < ND; ++i) m |= uint64_t(1) << (B * i);
+        return m;
+    }();
+    constexpr uint64_t M3 = 3 * M1;
+    const uint64_t rb = dbits(r + kTwo52);                          // low 52 bits = r
+    const uint64_t ob = dbits(__dadd_rz(__dmul_ru(r, P.inv_p), kTwo52));  // low 52 bits = floor(r/3)
+    const uint64_t u = ((rb & M3) + (ob & M3)) & M3;                // lane i = u_i
+    const uint64_t v = u + 8 * M1 - (u >> B);                       // u_i + 8 - u_{i+1}
+    const uint64_t g = (v >> 3) & M1;                               // [u_i >= u_{i+1}]
+    const uint64_t mu = v - 5 * M1 - 3 * g;                         // (u_i - u_{i+1}) mod 3
+    return __longlong_as_double(static_cast<long long>(mu | 0x4330000000000000ull)) - kTwo52;
+}
+
+template <class K>
+struct is_swar3 {
+    static constexpr bool value = false;
+};
+template <uint32_t QB>
+struct is_swar3<CtConst<3, QB>> {
+    static constexpr bool value = (QB % 2 == 0) && QB >= 4;
+};
+
+template <int ND, class K>
+__device__ __forceinline__ double repack_one(const K& c, double r) {
+    if constexpr (is_swar3<K>::value)
+        return redq_repack_swar3<ND, K::kQbits>(c.P, r);
+    else
+        return redq_repack<ND>(c, r);
 }
 
 __device__ __forceinline__ uint32_t add_mod_bytes_mm(uint32_t x, uint32_t y, uint32_t p) {
@@ -111,7 +160,7 @@ __device__ __forceinline__ uint32_t acc_to_coeffs(const K& c, uint32_t lh_radix,
 
 // REDQ_STAGE: re-pack at stage granularity (chunk a multiple of BK) rather
 // than per 4-step MMA (fields whose safe chunk is below BK)
-template <int KR, class K, bool REDQ_STAGE>
+template <int KR, class K, bool REDQ_STAGE, int NST>
 __global__ void __launch_bounds__(THREADS, 1)
     gfq_matmul_kernel(const GfqMatmulParams P, const double* __restrict__ at, const double* __restrict__ bm,
                       uint64_t m, uint64_t n, uint64_t K_pad, uint64_t m_pad, uint64_t n_pad,
@@ -119,9 +168,9 @@ __global__ void __launch_bounds__(THREADS, 1)
     constexpr int ND = 2 * KR - 1;
     extern __shared__ __align__(128) uint8_t smem[];
     double* stages = reinterpret_cast<double*>(smem);
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_DOUBLES * 8);
-    uint64_t* empty = full + STAGES;
-    uint32_t* tabs = reinterpret_cast<uint32_t*>(empty + STAGES);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + NST * STAGE_DOUBLES * 8);
+    uint64_t* empty = full + NST;
+    uint32_t* tabs = reinterpret_cast<uint32_t*>(empty + NST);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint64_t m0 = uint64_t(blockIdx.y) * BM, n0 = uint64_t(blockIdx.x) * BN;
@@ -134,7 +183,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (out_r)
         for (uint32_t i = tid; i < P.order; i += blockDim.x) tabs[2 * nlh + i] = P.log[i];
     if (tid == 0) {
-        for (int s = 0; s < STAGES; ++s) {
+        for (int s = 0; s < NST; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], NCW);
         }
@@ -145,8 +194,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (warp == NCW) {
         // ---------------- producer: one TMA bulk row copy per lane ----------
         for (int kt = 0; kt < KT; ++kt) {
-            const int s = kt % STAGES;
-            if (kt >= STAGES) mbar_wait(&empty[s], ((kt / STAGES) - 1) & 1);
+            const int s = kt % NST;
+            if (kt >= NST) mbar_wait(&empty[s], ((kt / NST) - 1) & 1);
             if (lane == 0) mbar_expect_tx(&full[s], 2 * BK * BM * 8);
             __syncwarp();
             double* sa = stages + s * STAGE_DOUBLES;
@@ -176,8 +225,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int i = 0; i < MT; ++i)
 #pragma unroll
             for (int j = 0; j < NT; ++j) {
-                acc[i][j][0] = redq_repack<ND>(c, acc[i][j][0]);
-                acc[i][j][1] = redq_repack<ND>(c, acc[i][j][1]);
+                acc[i][j][0] = repack_one<ND>(c, acc[i][j][0]);
+                acc[i][j][1] = repack_one<ND>(c, acc[i][j][1]);
             }
     };
     // 4 MMA k-steps of one stage; per step 8 A and 4 B fragments -> 32 DMMA
@@ -196,9 +245,11 @@ __global__ void __launch_bounds__(THREADS, 1)
     };
 
     if constexpr (REDQ_STAGE) {
+        // (a register-lean fragment prefetch was measured here and gained
+        // nothing while adding spills under the 168-register cap)
         auto stage = [&](int kt) {
-            const int s = kt % STAGES;
-            mbar_wait(&full[s], (kt / STAGES) & 1);
+            const int s = kt % NST;
+            mbar_wait(&full[s], (kt / NST) & 1);
             const double* sa = stages + s * STAGE_DOUBLES;
 #pragma unroll 1
             for (int kk = 0; kk < BK / 4; ++kk) mma_kstep(sa, sa + BK * LDS_, kk);
@@ -224,8 +275,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         const int chunk4 = static_cast<int>(P.chunk / 4);
         int countdown = chunk4 > 0 ? chunk4 - (warp * chunk4) / NCW : 0x7fffffff;
         for (int kt = 0; kt < KT; ++kt) {
-            const int s = kt % STAGES;
-            mbar_wait(&full[s], (kt / STAGES) & 1);
+            const int s = kt % NST;
+            mbar_wait(&full[s], (kt / NST) & 1);
             const double* sa = stages + s * STAGE_DOUBLES;
 #pragma unroll 1
             for (int kk = 0; kk < BK / 4; ++kk) {
@@ -268,22 +319,23 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
 }
 
-template <int KR, class K, bool REDQ_STAGE>
+template <int KR, class K, bool REDQ_STAGE, int NST = 4>
 cudaError_t run_matmul_t(const GfqMatmulParams& P, const double* at, const double* b, uint64_t m, uint64_t n,
                          uint64_t K_pad, uint64_t m_pad, uint64_t n_pad, uint8_t* oc, uint32_t* orp, cudaStream_t s) {
     uint32_t nlh = 1;
     for (int i = 0; i < KR; ++i) nlh *= P.lh_radix;
-    const size_t smem = SMEM_BYTES + size_t(2 * nlh + P.order) * 4;
+    const size_t smem = smem_bytes(NST) + size_t(2 * nlh + P.order) * 4;
     if (smem > 227 * 1024) return cudaErrorInvalidValue;
     static bool attr = false;
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(gfq_matmul_kernel<KR, K, REDQ_STAGE>,
+        cudaError_t e = cudaFuncSetAttribute(gfq_matmul_kernel<KR, K, REDQ_STAGE, NST>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         if (e != cudaSuccess) return e;
         attr = true;
     }
     dim3 grid(static_cast<unsigned>(n_pad / BN), static_cast<unsigned>(m_pad / BM));
-    gfq_matmul_kernel<KR, K, REDQ_STAGE><<<grid, THREADS, smem, s>>>(P, at, b, m, n, K_pad, m_pad, n_pad, oc, orp);
+    gfq_matmul_kernel<KR, K, REDQ_STAGE, NST><<<grid, THREADS, smem, s>>>(P, at, b, m, n, K_pad, m_pad, n_pad, oc,
+                                                                          orp);
     return cudaGetLastError();
 }
 
@@ -302,11 +354,11 @@ cudaError_t run_matmul(const GfqMatmulParams& P, const double* at, const double*
     if constexpr (VARIANT == 1) {
         if constexpr (KR == 2) {
             if (P.p == 3 && P.rq.qbits == 16 && mm_plan_safe(P.rq) && stage_ok)
-                return run_matmul_t<2, CtConst<3, 16>, true>(P, at, b, m, n, K_pad, m_pad, n_pad, oc, orp, s);
+                return run_matmul_t<2, CtConst<3, 16>, true, 6>(P, at, b, m, n, K_pad, m_pad, n_pad, oc, orp, s);
         }
         if constexpr (KR == 3) {
             if (P.p == 3 && P.rq.qbits == 10 && mm_plan_safe(P.rq) && stage_ok)
-                return run_matmul_t<3, CtConst<3, 10>, true>(P, at, b, m, n, K_pad, m_pad, n_pad, oc, orp, s);
+                return run_matmul_t<3, CtConst<3, 10>, true, 6>(P, at, b, m, n, K_pad, m_pad, n_pad, oc, orp, s);
         }
         return cudaErrorNotSupported;
     } else {

@@ -42,7 +42,7 @@ struct DevBuf {
 
 // pinned-free chunked host<->device pipeline resources
 struct Staging {
-    static constexpr int kStreams = 3;
+    static constexpr int kStreams = 4;
     cudaStream_t streams[kStreams] = {};
     DevBuf in0[kStreams], in1[kStreams], out[kStreams];
     Staging();

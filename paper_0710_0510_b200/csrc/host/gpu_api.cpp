@@ -231,7 +231,9 @@ void redq_host(DevicePlanCache& dp, const double* h_words, u64 n, uint8_t* h_out
     if (!dp.staging) dp.staging = std::make_unique<Staging>();
     Staging& S = *dp.staging;
     const u64 nd = dp.prm.d + 1;
-    const u64 chunk = u64(1) << 22;
+    // 16 MB of words per chunk: short pipeline fill/drain against PCIe
+    // (measured Gen5 x16: 55.6 GB/s H2D, 57.2 D2H, 100 GB/s both ways)
+    const u64 chunk = u64(1) << 21;
     for (u64 off = 0, c = 0; off < n; off += chunk, ++c) {
         const int si = static_cast<int>(c % Staging::kStreams);
         cudaStream_t s = S.streams[si];
