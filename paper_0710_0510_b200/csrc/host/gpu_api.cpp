@@ -143,7 +143,11 @@ DeviceFieldCache& device_field(const GfqField& f) {
     u64 nlh = 1;
     for (u32 i = 0; i < k; ++i) nlh *= lh;
     const u64 order = f.order();
-    const u64 words = 2 * nlh + 2 * order;
+    // small fields (p <= 8, k = 3) also get the L, H and log tables re-indexed
+    // with 3 bits per digit, so the device forms indices by bit gathers
+    const bool bin = p <= 8 && k == 3;
+    const u64 base_words = 2 * nlh + 2 * order;
+    const u64 words = base_words + (bin ? 3 * 512 : 0);
     if (words * 4 > 96 * 1024)
         throw std::invalid_argument("qpack-b200 GF(p^k): field tables exceed the shared-memory budget");
     // coefficient-form tables: rep -> packed coefficient bytes
@@ -161,6 +165,18 @@ DeviceFieldCache& device_field(const GfqField& f) {
     for (u64 i = 0; i < order; ++i) {
         host[2 * nlh + i] = FieldAccess::log(f)[i];
         host[2 * nlh + order + i] = bytes_of(static_cast<u32>(i));
+    }
+    if (bin) {
+        // index d0 | d1 << 3 | d2 << 6 for digits d_j < p; other slots unused
+        for (u64 d2 = 0; d2 < p; ++d2)
+            for (u64 d1 = 0; d1 < p; ++d1)
+                for (u64 d0 = 0; d0 < p; ++d0) {
+                    const u64 b8 = d0 | (d1 << 3) | (d2 << 6);
+                    const u64 lh_idx = d0 + lh * (d1 + lh * d2);
+                    host[base_words + b8] = host[lh_idx];
+                    host[base_words + 512 + b8] = host[nlh + lh_idx];
+                    host[base_words + 1024 + b8] = FieldAccess::log(f)[d0 + p * (d1 + p * d2)];
+                }
     }
     c->tables.ensure(words * 4);
     check(cudaMemcpy(c->tables.ptr, host.data(), words * 4, cudaMemcpyHostToDevice), "field tables upload");
@@ -184,6 +200,7 @@ DeviceFieldCache& device_field(const GfqField& f) {
     E.log = tb + 2 * nlh;
     E.alog = tb + 2 * nlh + order;
     E.tables_words = static_cast<uint32_t>(words);
+    E.bin_off = bin ? static_cast<uint32_t>(base_words) : 0u;
     qpk::GfqMatmulParams& M = c->mm;
     M.rq = rq;
     M.k = k;

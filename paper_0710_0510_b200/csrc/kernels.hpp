@@ -54,7 +54,8 @@ struct GfqElemParams {
     const uint32_t* hc;     // lh^k: corrected high half -> coefficient bytes (reduced by the modulus)
     const uint32_t* log;    // p^k: coefficient index -> rep
     const uint32_t* alog;   // p^k: rep -> coefficient bytes (sentinel -> 0)
-    uint32_t tables_words;  // lc+hc+log+alog total (for smem staging)
+    uint32_t tables_words;  // all tables, contiguous from lc (for smem staging)
+    uint32_t bin_off;       // word offset of the 3-bit-indexed lc8|hc8|log8 tables (p <= 8, k = 3), else 0
     int mode;               // 0 packed (DQT/REDQ/L-H), 1 dlog/Zech
 };
 

@@ -204,15 +204,44 @@ __device__ __forceinline__ uint32_t add_mod_bytes(uint32_t x, uint32_t y, uint32
     return r;
 }
 
-// every byte of N packed words is below p (p < 128): (b + 128 - p) sets a
-// byte's top bit iff b >= p, for bytes below 128; bytes >= 128 set it already
+// every byte of N packed words is below p (p < 128): b + 128 - p sets a
+// byte's top bit iff p <= b < 128; bytes >= 128 carry it already.  Only
+// such bytes can carry into a neighbour, so carries never hide a bad byte
+// (at worst they flag a good one and the exact path runs).
 template <int N>
 __device__ __forceinline__ bool all_bytes_below(const uint32_t* w, uint32_t p) {
     const uint32_t add = (128u - p) * 0x01010101u;
     uint32_t bad = 0;
 #pragma unroll
-    for (int i = 0; i < N; ++i) bad |= w[i] | ((w[i] & 0x7f7f7f7fu) + add);
+    for (int i = 0; i < N; ++i) bad |= w[i] | (w[i] + add);
     return (bad & 0x80808080u) == 0;
+}
+
+__device__ __forceinline__ uint32_t add_mod_bytes_fast(uint32_t x, uint32_t y, uint32_t p);
+
+// 3-bit gather of byte lanes 0..2: b0 | b1 << 3 | b2 << 6 (each lane < 8)
+__device__ __forceinline__ uint32_t gather3(uint32_t x) {
+    return (x & 7u) | ((x >> 5) & 0x38u) | ((x >> 10) & 0x1c0u);
+}
+
+// GF(p^k) product for q = 2^8, k = 3, p < 8, all REDQ digits in one
+// register: u_i in [0, p-1] is fixed by its value mod 8 and
+// u_i = (w >> 8i) - p (rop >> 8i) == a_i + (-p mod 8) b_i (mod 8) with a_i, b_i
+// the low 3 bits of byte i of w and rop -- one masked multiply-add gives all
+// five digits as byte lanes; the L/H tables are indexed 3 bits per digit.
+template <class C>
+__device__ __forceinline__ uint32_t lh_product_swar(const C& c, double inv_p, uint32_t ra, uint32_t rb,
+                                                    uint32_t lc8, uint32_t hc8) {
+    constexpr uint32_t F = (8u - C::kP % 8u) % 8u;
+    const uint64_t w = static_cast<uint64_t>(ra) * rb;  // the DQT word product, exact
+    const double wd = static_cast<double>(ra) * static_cast<double>(rb);
+    const uint64_t ob = dbits(__dadd_rz(__dmul_ru(wd, inv_p), kTwo52));  // low 52 bits: floor(w/p)
+    const uint32_t ulo = ((static_cast<uint32_t>(w) & 0x07070707u) + (static_cast<uint32_t>(ob) & 0x07070707u) * F) &
+                         0x07070707u;
+    const uint32_t uhi = (static_cast<uint32_t>(w >> 32) + static_cast<uint32_t>(ob >> 32) * F) & 7u;
+    const uint32_t il = gather3(ulo);
+    const uint32_t ih = gather3(ulo >> 16) | (uhi << 6);
+    return add_mod_bytes_fast(lds_u32(lc8 + 4 * il), lds_u32(hc8 + 4 * ih), C::kP);
 }
 
 // record r (k bytes, little endian) of a packed run as an integer
@@ -288,6 +317,23 @@ struct GfqElemOp {
             // q = 2^8: a record of k coefficient bytes IS its DQT word, so
             // packing is a byte-run extract; taken when every byte is < p
             if (all_bytes_below<R * K_ / 4>(a, c.p()) && all_bytes_below<R * K_ / 4>(b, c.p())) {
+                if constexpr (K_ == 3 && K::kP < 8) {
+                    if (P.bin_off) {
+                        // register-SIMD digits + 3-bit-indexed tables
+                        const uint32_t b8 = tab + 4 * P.bin_off;
+#pragma unroll
+                        for (int r = 0; r < R; ++r) {
+                            const uint32_t ra = record_int<K_>(a, r), rb = record_int<K_>(b, r);
+                            if (P.mode == 0) {
+                                rec[r] = lh_product_swar(c, P.rq.inv_p, ra, rb, b8, b8 + 2048);
+                            } else {
+                                rec[r] = dlog_product<K_>(c, gather3(ra), gather3(rb), b8 + 4096, al, P.group);
+                            }
+                        }
+                        pack_records<R, OUT>(rec, ow);
+                        return;
+                    }
+                }
 #pragma unroll
                 for (int r = 0; r < R; ++r) {
                     const uint32_t ra = record_int<K_>(a, r), rb = record_int<K_>(b, r);

@@ -12,6 +12,15 @@
 using namespace qpk;
 using Op = RedqOp<7, 4, CtConst<5, 7>>;
 
+struct XorOp {
+    static constexpr int IN0 = 3, IN1 = 3, OUT = 3, R = 4;
+    __host__ __device__ uint32_t tables_words() const { return 0; }
+    __host__ __device__ const uint32_t* tables_src() const { return nullptr; }
+    __device__ void apply(const uint32_t* a, const uint32_t* b, uint32_t (&ow)[3], uint32_t, uint32_t&) const {
+        ow[0] = a[0] ^ b[0], ow[1] = a[1] ^ b[1], ow[2] = a[2] ^ b[2];
+    }
+};
+
 // V_CTA: all threads consume; thread 0 produces after a CTA barrier; the CTA
 // stores one output tile.  NT threads, R records per thread, S stages.
 template <class OpT, int NT, int RR, int S>
@@ -223,6 +232,23 @@ int main() {
     }
             RUN3(256, 1, 4) RUN3(256, 2, 4) RUN3(256, 4, 3) RUN3(256, 4, 4) RUN3(256, 8, 3) RUN3(512, 4, 3)
         }
+        // pipeline ceiling for 3+3 -> 3 byte records: out = a ^ b
+        XorOp xop;
+#define RUNX(NT, RR, S)                                                                                          \
+    {                                                                                                            \
+        auto k = v_cta<XorOp, NT, RR, S>;                                                                        \
+        const size_t sm = S * 6 * NT * 4 * RR + 2 * 3 * NT * 4 * RR + 64;                                        \
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);                        \
+        int per = 0;                                                                                             \
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, NT, sm);                                          \
+        const uint64_t tiles = n3 / (NT * 4 * RR);                                                               \
+        const unsigned grid = unsigned(148 * per < tiles ? 148 * per : tiles);                                   \
+        float ms = timeit([&] { k<<<grid, NT, sm>>>(xop, a3, b3, o3, tiles); });                                 \
+        printf("C3 xor-copy cta NT=%d RR=%d S=%d cps=%d  %.4f ms  %.1f GB/s %s\n", NT, RR, S, per, ms,            \
+               b3y / (ms * 1e-3) / 1e9, cudaGetErrorString(cudaGetLastError()));                                 \
+    }
+        RUNX(256, 1, 4) RUNX(256, 2, 4) RUNX(256, 4, 3) RUNX(256, 4, 4) RUNX(256, 8, 2) RUNX(128, 4, 4)
+        RUNX(256, 2, 8) RUNX(512, 2, 4)
     }
     double* w2;
     cudaMalloc(&w2, n * 8);
