@@ -21,6 +21,8 @@ from .configs import CONFIGS, C1, C2, C3, C4, C5, Config, scaled  # noqa: F401
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "lib", "libqpack_b200.so")
+if os.environ.get("QPK_DEV_LIB"):  # development: load a variant build (scripts/)
+    LIB_PATH = os.path.abspath(os.environ["QPK_DEV_LIB"])
 
 # ---------------------------------------------------------------- errors
 QPK_OK, QPK_ERR_INVALID_ARGUMENT, QPK_ERR_DOMAIN, QPK_ERR_LENGTH = 0, 1, 2, 3

@@ -143,11 +143,12 @@ DeviceFieldCache& device_field(const GfqField& f) {
     u64 nlh = 1;
     for (u32 i = 0; i < k; ++i) nlh *= lh;
     const u64 order = f.order();
-    // small fields (p <= 8, k = 3) also get the L, H and log tables re-indexed
-    // with 3 bits per digit, so the device forms indices by bit gathers
+    // small fields (p <= 8, k = 3) also get the L, H, log and antilog tables
+    // re-indexed by the 9-bit hash of the digit bytes (kernels.hpp kHash9)
     const bool bin = p <= 8 && k == 3;
     const u64 base_words = 2 * nlh + 2 * order;
-    const u64 words = base_words + (bin ? 3 * 512 : 0);
+    const u64 group = order - 1;
+    const u64 words = base_words + (bin ? 3 * 512 + 2 * group : 0);
     if (words * 4 > 96 * 1024)
         throw std::invalid_argument("qpack-b200 GF(p^k): field tables exceed the shared-memory budget");
     // coefficient-form tables: rep -> packed coefficient bytes
@@ -167,16 +168,25 @@ DeviceFieldCache& device_field(const GfqField& f) {
         host[2 * nlh + order + i] = bytes_of(static_cast<u32>(i));
     }
     if (bin) {
-        // index d0 | d1 << 3 | d2 << 6 for digits d_j < p; other slots unused
-        for (u64 d2 = 0; d2 < p; ++d2)
-            for (u64 d1 = 0; d1 < p; ++d1)
-                for (u64 d0 = 0; d0 < p; ++d0) {
-                    const u64 b8 = d0 | (d1 << 3) | (d2 << 6);
+        uint32_t* hl = host.data() + base_words;
+        uint32_t* hh = hl + 512;
+        uint32_t* hg = hl + 1024;
+        uint32_t* al2 = hl + 1536;
+        std::vector<uint8_t> seen(512, 0);
+        for (u64 d2 = 0; d2 < 8; ++d2)
+            for (u64 d1 = 0; d1 < 8; ++d1)
+                for (u64 d0 = 0; d0 < 8; ++d0) {
+                    const uint32_t h = qpk::hash9_host(static_cast<uint32_t>(d0 | (d1 << 8) | (d2 << 16)));
+                    if (seen[h]++) throw std::logic_error("qpack-b200: kHash9 is not injective");
+                    if (d0 >= p || d1 >= p || d2 >= p) continue;
                     const u64 lh_idx = d0 + lh * (d1 + lh * d2);
-                    host[base_words + b8] = host[lh_idx];
-                    host[base_words + 512 + b8] = host[nlh + lh_idx];
-                    host[base_words + 1024 + b8] = FieldAccess::log(f)[d0 + p * (d1 + p * d2)];
+                    hl[h] = host[lh_idx];
+                    hh[h] = host[nlh + lh_idx];
+                    const u64 lg = FieldAccess::log(f)[d0 + p * (d1 + p * d2)];
+                    hg[h] = static_cast<uint32_t>(4 * (lg == group ? 2 * group - 1 : lg));
                 }
+        for (u64 i = 0; i + 1 < 2 * group; ++i) al2[i] = bytes_of(static_cast<u32>(i % group));
+        al2[2 * group - 1] = 0;
     }
     c->tables.ensure(words * 4);
     check(cudaMemcpy(c->tables.ptr, host.data(), words * 4, cudaMemcpyHostToDevice), "field tables upload");
@@ -201,6 +211,12 @@ DeviceFieldCache& device_field(const GfqField& f) {
     E.alog = tb + 2 * nlh + order;
     E.tables_words = static_cast<uint32_t>(words);
     E.bin_off = bin ? static_cast<uint32_t>(base_words) : 0u;
+    if (k == 3) {
+        const std::vector<u64> xv = {0, 1, 0};
+        const GfqElt x = f.from_coeffs(xv);
+        E.col3 = bytes_of(f.pow(x, 3).rep);
+        E.col4 = bytes_of(f.pow(x, 4).rep);
+    }
     qpk::GfqMatmulParams& M = c->mm;
     M.rq = rq;
     M.k = k;

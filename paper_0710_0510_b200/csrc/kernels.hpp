@@ -45,6 +45,15 @@ struct PolymulParams {
     uint32_t k;
 };
 
+// Small fields (p <= 8, k = 3) index their tables by a 9-bit multiplicative
+// hash of the three coefficient (or digit) bytes y = c0 | c1 << 8 | c2 << 16,
+// c_j < 8: h(y) = ((y * kHash9) mod 2^24) >> 15 is injective on all 512 such
+// keys (found by search; the host re-checks it when it builds the tables).
+// Bits 24..31 of y do not enter h, so a record can be hashed straight out of a
+// packed run without masking.
+constexpr uint32_t kHash9 = 13115393u;
+constexpr uint32_t hash9_host(uint32_t y) { return ((y * kHash9) & 0xffffffu) >> 15; }
+
 // GF(p^k) elementwise product (config 3).
 struct GfqElemParams {
     RedqParams rq;          // d = 2k-2, mode float
@@ -55,7 +64,10 @@ struct GfqElemParams {
     const uint32_t* log;    // p^k: coefficient index -> rep
     const uint32_t* alog;   // p^k: rep -> coefficient bytes (sentinel -> 0)
     uint32_t tables_words;  // all tables, contiguous from lc (for smem staging)
-    uint32_t bin_off;       // word offset of the 3-bit-indexed lc8|hc8|log8 tables (p <= 8, k = 3), else 0
+    uint32_t bin_off;       // word offset of the hash-indexed tables (p <= 8, k = 3), else 0:
+                            //   lcH[512] | hcH[512] | logH[512] (4*log, zero -> 4*(2g-1)) | alog2[2g]
+                            //   alog2[i] = coefficients of rep i mod g (i < 2g-1), alog2[2g-1] = 0
+    uint32_t col3, col4;    // k = 3: coefficient bytes of x^3 and x^4 mod the field polynomial
     int mode;               // 0 packed (DQT/REDQ/L-H), 1 dlog/Zech
 };
 

@@ -164,10 +164,19 @@ __device__ __forceinline__ double pack_word(const C& c, double qd, const uint32_
     }
 }
 
+#ifndef QPK_PM_R  // tile geometry of the batched polynomial product
+#define QPK_PM_R 4
+#endif
+#ifndef QPK_PM_RR
+#define QPK_PM_RR 1
+#endif
+#ifndef QPK_PM_S
+#define QPK_PM_S 2
+#endif
 template <int K_, int W, class K>
 struct PolymulOp {
     static constexpr int ND = 2 * K_ - 1;
-    static constexpr int IN0 = K_, IN1 = K_, OUT = ND, R = 4, RR = 2, S = 3;
+    static constexpr int IN0 = K_, IN1 = K_, OUT = ND, R = QPK_PM_R, RR = QPK_PM_RR, S = QPK_PM_S;
     PolymulParams P;
     __host__ __device__ uint32_t tables_words() const { return W ? P.rq.n_entries : 0u; }
     __host__ __device__ const uint32_t* tables_src() const { return P.rq.table; }
@@ -219,29 +228,84 @@ __device__ __forceinline__ bool all_bytes_below(const uint32_t* w, uint32_t p) {
 
 __device__ __forceinline__ uint32_t add_mod_bytes_fast(uint32_t x, uint32_t y, uint32_t p);
 
-// 3-bit gather of byte lanes 0..2: b0 | b1 << 3 | b2 << 6 (each lane < 8)
-__device__ __forceinline__ uint32_t gather3(uint32_t x) {
-    return (x & 7u) | ((x >> 5) & 0x38u) | ((x >> 10) & 0x1c0u);
+// 9-bit table index of three byte lanes below 8 (kernels.hpp kHash9); byte
+// lane 3 of y is ignored: (y * (kHash9 << 8)) keeps only y mod 2^24
+__device__ __forceinline__ uint32_t hash9(uint32_t y) { return (y * (kHash9 << 8)) >> 23; }
+
+// bytewise t mod p of a packed word (bytes may be any value)
+__device__ __forceinline__ uint32_t bytes_mod_p(uint32_t w, uint32_t p, uint32_t magic) {
+    uint32_t r = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) r |= mod_by_magic((w >> (8 * j)) & 0xffu, p, magic) << (8 * j);
+    return r;
 }
 
 // GF(p^k) product for q = 2^8, k = 3, p < 8, all REDQ digits in one
 // register: u_i in [0, p-1] is fixed by its value mod 8 and
 // u_i = (w >> 8i) - p (rop >> 8i) == a_i + (-p mod 8) b_i (mod 8) with a_i, b_i
-// the low 3 bits of byte i of w and rop -- one masked multiply-add gives all
-// five digits as byte lanes; the L/H tables are indexed 3 bits per digit.
+// the low 3 bits of byte i of w and rop -- one masked multiply-add gives the
+// five digits as byte lanes (no lane carries: 7 + 7*7 < 256), and the L/H
+// tables are read at the 9-bit hash of digit lanes 0..2 and 2..4.
 template <class C>
-__device__ __forceinline__ uint32_t lh_product_swar(const C& c, double inv_p, uint32_t ra, uint32_t rb,
-                                                    uint32_t lc8, uint32_t hc8) {
+__device__ __forceinline__ uint32_t lh_product_hash(const C&, double inv_p, uint32_t ra, uint32_t rb, uint32_t lcH,
+                                                    uint32_t hcH) {
     constexpr uint32_t F = (8u - C::kP % 8u) % 8u;
-    const uint64_t w = static_cast<uint64_t>(ra) * rb;  // the DQT word product, exact
-    const double wd = static_cast<double>(ra) * static_cast<double>(rb);
+    const uint64_t w = static_cast<uint64_t>(ra) * rb;  // the DQT word product, exact (< 2^48)
+    const double wd = __hiloint2double(0x43300000 | static_cast<int>(w >> 32), static_cast<int>(w)) - kTwo52;
     const uint64_t ob = dbits(__dadd_rz(__dmul_ru(wd, inv_p), kTwo52));  // low 52 bits: floor(w/p)
-    const uint32_t ulo = ((static_cast<uint32_t>(w) & 0x07070707u) + (static_cast<uint32_t>(ob) & 0x07070707u) * F) &
-                         0x07070707u;
-    const uint32_t uhi = (static_cast<uint32_t>(w >> 32) + static_cast<uint32_t>(ob >> 32) * F) & 7u;
-    const uint32_t il = gather3(ulo);
-    const uint32_t ih = gather3(ulo >> 16) | (uhi << 6);
-    return add_mod_bytes_fast(lds_u32(lc8 + 4 * il), lds_u32(hc8 + 4 * ih), C::kP);
+    const uint32_t lo = (static_cast<uint32_t>(w) & 0x07070707u) + (static_cast<uint32_t>(ob) & 0x07070707u) * F;
+    const uint32_t hi = static_cast<uint32_t>(w >> 32) + static_cast<uint32_t>(ob >> 32) * F;  // lane 0: digit 4
+    const uint32_t il = hash9(lo & 0x07070707u);
+    const uint32_t ih = hash9(__funnelshift_r(lo, hi, 16) & 0x07070707u);
+    return add_mod_bytes_fast(lds_u32(lcH + 4 * il), lds_u32(hcH + 4 * ih), C::kP);
+}
+
+// dlog product on hash-indexed tables: logH holds 4*log (zero -> 4*(2g-1)),
+// so rep(a) + rep(b) indexes the doubled antilog table with no reduction
+// mod g, and any sum involving zero clamps to its zero entry (gfq.cpp:260-264)
+__device__ __forceinline__ uint32_t dlog_product_hash(uint32_t ya, uint32_t yb, uint32_t logH, uint32_t alog2,
+                                                      uint32_t zero4) {
+    const uint32_t s = lds_u32(logH + 4 * hash9(ya)) + lds_u32(logH + 4 * hash9(yb));
+    return lds_u32(alog2 + min(s, zero4));
+}
+
+// GF(7^3) product on the integer DQT word (q = 2^8).  With coefficients
+// below 7 the q-adic word product ra*rb has byte lanes c_0..c_4, c_j =
+// sum a_i b_(j-i) <= 108 < q, so the convolution needs no carry handling in
+// 64-bit integers (the fp64 product of the reference is the same exact
+// integer).  Digit reduction mod p and reduction by the field polynomial are
+// linear over GF(7): c_0..c_2 + (c_3 mod 7) x^3 + (c_4 mod 7) x^4 with x^3, x^4
+// as packed coefficient bytes gives lanes <= 180, reduced by lanes_mod7.
+__device__ __forceinline__ uint32_t gf73_lanes(uint32_t ra, uint32_t rb, uint32_t col3, uint32_t col4) {
+    const uint64_t w = static_cast<uint64_t>(ra) * rb;
+    const uint32_t lo = static_cast<uint32_t>(w), c4 = static_cast<uint32_t>(w >> 32);
+    const uint32_t c3 = lo >> 24;
+    constexpr uint32_t kMagic7 = 613566757u;  // ceil(2^32 / 7)
+    return (lo & 0xffffffu) + mod_by_magic(c3, 7u, kMagic7) * col3 + mod_by_magic(c4, 7u, kMagic7) * col4;
+}
+
+// bytewise x mod 7 for any byte lanes (8 == 1 mod 7: x - 7 floor(x/8) keeps
+// the residue and leaves each lane non-negative, so no borrow crosses a lane)
+__device__ __forceinline__ uint32_t lanes_mod7(uint32_t t) {
+    t -= 7u * ((t >> 3) & 0x1f1f1f1fu);  // lanes <= 7 + 31
+    t -= 7u * ((t >> 3) & 0x07070707u);  // lanes <= 7 + 4
+    const uint32_t ge = ((t + 0x79797979u) >> 7) & 0x01010101u;
+    return t - 7u * ge;
+}
+
+// word holding record r of a packed 3-byte run in its low 24 bits (upper byte
+// unspecified)
+__device__ __forceinline__ uint32_t record24(const uint32_t* w, int r) {
+    const int byte = 3 * r, i = byte >> 2, sh = 8 * (byte & 3);
+    if (sh == 0) return w[i];
+    if (sh == 8) return w[i] >> 8;
+    return __funnelshift_r(w[i], w[i + 1], sh);
+}
+
+template <class K>
+constexpr bool ct_small_p() {
+    if constexpr (K::kSafe) return K::kP < 8 && K::kQbitsCt == 8;
+    else return false;
 }
 
 // record r (k bytes, little endian) of a packed run as an integer
@@ -297,16 +361,89 @@ __device__ __forceinline__ uint32_t dlog_product(const C&, uint32_t ia, uint32_t
     return lds_u32(al + 4 * rc);
 }
 
-template <int K_, class K>
+#ifndef QPK_GFE_R  // tile geometry of the GF elementwise op (records/run, runs/tile, stages)
+#define QPK_GFE_R 8
+#endif
+#ifndef QPK_GFE_RR
+#define QPK_GFE_RR 2
+#endif
+#ifndef QPK_GFE_S
+#define QPK_GFE_S 2
+#endif
+// MODE: 0 packed, 1 dlog as a compile-time choice (fast paths), -1 = P.mode
+template <int K_, class K, int MODE = -1>
 struct GfqElemOp {
     static constexpr int ND = 2 * K_ - 1;
-    static constexpr int IN0 = K_, IN1 = K_, OUT = K_, R = 4, RR = 1, S = 4;
+    static constexpr int IN0 = K_, IN1 = K_, OUT = K_, R = QPK_GFE_R, RR = QPK_GFE_RR, S = QPK_GFE_S;
     GfqElemParams P;
-    __host__ __device__ uint32_t tables_words() const { return P.tables_words; }
-    __host__ __device__ const uint32_t* tables_src() const { return P.lc; }  // lc|hc|log|alog contiguous
+    // hash-indexed fast path (GF(p^3), p < 8, q = 2^8) when the host built its tables
+    static constexpr bool kHashable = K_ == 3 && ct_small_p<K>() && R % 4 == 0;
+    __host__ __device__ bool hashed() const { return kHashable && P.bin_off != 0; }
+    // staged tables: lc|hc|log|alog, or only the hash-indexed block
+    __host__ __device__ uint32_t tables_words() const { return P.tables_words - (hashed() ? P.bin_off : 0u); }
+    __host__ __device__ const uint32_t* tables_src() const { return P.lc + (hashed() ? P.bin_off : 0u); }
+
+    __device__ __forceinline__ bool packed() const { return MODE < 0 ? P.mode == 0 : MODE == 0; }
+
+    // groups of 4 records = 3 packed words
+    __device__ __forceinline__ void apply_hashed(const uint32_t* a, const uint32_t* b, uint32_t (&ow)[R * OUT / 4],
+                                                 uint32_t tab) const {
+        const K c{P.rq};
+        constexpr int NW = R * 3 / 4;
+        uint32_t aw[NW], bw[NW];
+#pragma unroll
+        for (int i = 0; i < NW; ++i) aw[i] = a[i], bw[i] = b[i];
+        if (!(all_bytes_below<NW>(aw, c.p()) && all_bytes_below<NW>(bw, c.p()))) {
+            // coefficient bytes >= p are reduced mod p, as record_coeffs does
+#pragma unroll
+            for (int i = 0; i < NW; ++i) {
+                aw[i] = bytes_mod_p(aw[i], c.p(), P.rq.mod_magic);
+                bw[i] = bytes_mod_p(bw[i], c.p(), P.rq.mod_magic);
+            }
+        }
+        if constexpr (K::kP == 7) {
+            if (packed()) {
+#pragma unroll
+                for (int g = 0; g < R / 4; ++g) {
+                    uint32_t t[4];
+#pragma unroll
+                    for (int r = 0; r < 4; ++r)
+                        t[r] = gf73_lanes(record24(aw + 3 * g, r) & 0xffffffu, record24(bw + 3 * g, r) & 0xffffffu,
+                                          P.col3, P.col4);
+                    ow[3 * g] = lanes_mod7(t[0] | (t[1] << 24));
+                    ow[3 * g + 1] = lanes_mod7((t[1] >> 8) | (t[2] << 16));
+                    ow[3 * g + 2] = lanes_mod7((t[2] >> 16) | (t[3] << 8));
+                }
+                return;
+            }
+        }
+        const uint32_t zero4 = 4 * (2 * P.group - 1);
+#pragma unroll
+        for (int g = 0; g < R / 4; ++g) {
+            uint32_t res[4];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const uint32_t ya = record24(aw + 3 * g, r), yb = record24(bw + 3 * g, r);
+                if (packed()) {
+                    res[r] = lh_product_hash(c, P.rq.inv_p, ya & 0xffffffu, yb & 0xffffffu, tab, tab + 2048);
+                } else {
+                    res[r] = dlog_product_hash(ya, yb, tab + 4096, tab + 6144, zero4);
+                }
+            }
+            ow[3 * g] = res[0] | (res[1] << 24);
+            ow[3 * g + 1] = (res[1] >> 8) | (res[2] << 16);
+            ow[3 * g + 2] = (res[2] >> 16) | (res[3] << 8);
+        }
+    }
 
     __device__ __forceinline__ void apply(const uint32_t* a, const uint32_t* b, uint32_t (&ow)[R * OUT / 4],
                                           uint32_t tab, uint32_t&) const {
+        if constexpr (kHashable) {
+            if (P.bin_off) {
+                apply_hashed(a, b, ow, tab);
+                return;
+            }
+        }
         const K c{P.rq};
         uint32_t nlh = 1;
 #pragma unroll
@@ -317,28 +454,11 @@ struct GfqElemOp {
             // q = 2^8: a record of k coefficient bytes IS its DQT word, so
             // packing is a byte-run extract; taken when every byte is < p
             if (all_bytes_below<R * K_ / 4>(a, c.p()) && all_bytes_below<R * K_ / 4>(b, c.p())) {
-                if constexpr (K_ == 3 && K::kP < 8) {
-                    if (P.bin_off) {
-                        // register-SIMD digits + 3-bit-indexed tables
-                        const uint32_t b8 = tab + 4 * P.bin_off;
-#pragma unroll
-                        for (int r = 0; r < R; ++r) {
-                            const uint32_t ra = record_int<K_>(a, r), rb = record_int<K_>(b, r);
-                            if (P.mode == 0) {
-                                rec[r] = lh_product_swar(c, P.rq.inv_p, ra, rb, b8, b8 + 2048);
-                            } else {
-                                rec[r] = dlog_product<K_>(c, gather3(ra), gather3(rb), b8 + 4096, al, P.group);
-                            }
-                        }
-                        pack_records<R, OUT>(rec, ow);
-                        return;
-                    }
-                }
 #pragma unroll
                 for (int r = 0; r < R; ++r) {
                     const uint32_t ra = record_int<K_>(a, r), rb = record_int<K_>(b, r);
                     uint32_t res;
-                    if (P.mode == 0) {
+                    if (packed()) {
                         res = lh_product<K_>(c, ra, rb, lc, hc);
                     } else {
                         res = dlog_product<K_>(c, coeff_index<K_>(c, ra), coeff_index<K_>(c, rb), lg, al, P.group);
@@ -355,7 +475,7 @@ struct GfqElemOp {
             record_coeffs<K_>(c, P.rq.mod_magic, a, r, ca);
             record_coeffs<K_>(c, P.rq.mod_magic, b, r, cb);
             uint32_t res;
-            if (P.mode == 0) {
+            if (packed()) {
                 // paper Alg. 4 with one term: pack, fp64 product, REDQ digits,
                 // low/high half tables (gfq.cpp:353-381); the tables give
                 // coefficient vectors, so the halves add coefficient-wise
@@ -455,13 +575,6 @@ __global__ void __launch_bounds__(kThreads) stream_tma_kernel(const Op op, const
     const uint32_t tab = smem_addr(s_tab);
     const int tid = threadIdx.x;
 
-    stage_tables(op, s_tab);
-    if (tid == 0) {
-        for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
-        fence_mbar_init();
-    }
-    __syncthreads();
-
     uint64_t policy = 0;
     auto issue = [&](int s, uint64_t tile) {
         uint8_t* dst = s_in + size_t(s) * (G::B0 + G::B1);
@@ -469,13 +582,19 @@ __global__ void __launch_bounds__(kThreads) stream_tma_kernel(const Op op, const
         bulk_g2s_stream(dst, in0 + tile * G::B0, G::B0, &bars[s], policy);
         if constexpr (G::B1 > 0) bulk_g2s_stream(dst + G::B0, in1 + tile * G::B1, G::B1, &bars[s], policy);
     };
+    // thread 0 puts the first S tiles in flight before the table staging,
+    // so the per-CTA table copy overlaps the first loads
     if (tid == 0) {
+        for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
+        fence_mbar_init();
         policy = policy_evict_first();
         for (int s = 0; s < S; ++s) {
             const uint64_t t = blockIdx.x + uint64_t(s) * gridDim.x;
             if (t < n_tiles) issue(s, t);
         }
     }
+    stage_tables(op, s_tab);
+    __syncthreads();
 
     uint32_t err = 0;
     uint32_t it = 0;
@@ -561,15 +680,21 @@ cudaError_t run_stream(const Op& op, const uint8_t* in0, const uint8_t* in1, uin
             if (e != cudaSuccess) return e;
             attr_done = true;
         }
-        int per_sm = 0;
-        cudaError_t e =
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, stream_tma_kernel<Op>, kThreads, smem);
-        if (e != cudaSuccess) return e;
-        per_sm = std::max(per_sm, 1);
-        const uint64_t grid = std::min<uint64_t>(n_tiles, uint64_t(sms) * per_sm);
+        // occupancy per instantiation and table size (a per-call query costs
+        // microseconds of host time, comparable to a small launch)
+        static thread_local size_t occ_smem = 0;
+        static thread_local int occ_per_sm = 0;
+        if (occ_smem != smem) {
+            int v = 0;
+            cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, stream_tma_kernel<Op>, kThreads, smem);
+            if (e != cudaSuccess) return e;
+            occ_smem = smem;
+            occ_per_sm = std::max(v, 1);
+        }
+        const uint64_t grid = std::min<uint64_t>(n_tiles, uint64_t(sms) * occ_per_sm);
         stream_tma_kernel<Op>
             <<<static_cast<unsigned>(grid), kThreads, smem, s>>>(op, in0, in1, out, n_tiles, status);
-        e = cudaGetLastError();
+        const cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }
     const uint64_t first = n_tiles * G::TILE;
@@ -649,7 +774,8 @@ cudaError_t gfq_elem_dispatch(const GfqElemParams& P, const uint8_t* a, const ui
                               uint8_t* out, cudaStream_t s) {
     if constexpr (K_ == 3) {
         if (P.p == 7 && P.rq.qbits == 8 && plan_is_safe(P.rq))
-            return run_stream(GfqElemOp<3, CtConst<7, 8>>{P}, a, b, out, n, nullptr, s);
+            return P.mode == 0 ? run_stream(GfqElemOp<3, CtConst<7, 8>, 0>{P}, a, b, out, n, nullptr, s)
+                               : run_stream(GfqElemOp<3, CtConst<7, 8>, 1>{P}, a, b, out, n, nullptr, s);
     }
     return P.rq.qbits ? run_stream(GfqElemOp<K_, RtConst<true>>{P}, a, b, out, n, nullptr, s)
                       : run_stream(GfqElemOp<K_, RtConst<false>>{P}, a, b, out, n, nullptr, s);
