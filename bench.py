@@ -404,6 +404,27 @@ def measure_secondary(Q, torch, dev):
         res[f"c3_gfq_mul_{name}"] = {"products_per_s": n3 / (ms * 1e-3), "ms": ms, "GBps": gbs,
                                      "frac_hbm": gbs / peak_hbm, "ms_single_launch_flushed": single}
     del sets3
+    # K5: GF(3^3) GEMV on reps, 8192 x 8192 (256 MiB of
+    # A, streamed once per launch: > L2), and one long fgdp_dot of 2^26 terms
+    f5 = Q.GfqField(3, 3, 1 << 10)
+    gen = torch.Generator(device=dev).manual_seed(5)
+    nn = 8192
+    A5 = torch.randint(0, 27, (nn, nn), dtype=torch.int32, device=dev, generator=gen)
+    x5 = torch.randint(0, 27, (nn,), dtype=torch.int32, device=dev, generator=gen)
+    y5 = torch.empty((nn,), dtype=torch.int32, device=dev)
+    ms = time_graph([lambda: f5.gemv(A5, x5, out=y5)] * 4)
+    gbs = (nn * nn * 4 + nn * 4 * 2) / (ms * 1e-3) / 1e9
+    res["k5_gfq_gemv"] = {"m": nn, "K": nn, "field": "GF(3^3) q=2^10", "ms": ms, "GBps": gbs,
+                          "frac_hbm": gbs / peak_hbm, "gf_terms_per_s": nn * nn / (ms * 1e-3)}
+    del A5
+    nd = 1 << 26
+    v1 = torch.randint(0, 27, (1, nd), dtype=torch.int32, device=dev, generator=gen)
+    v2 = torch.randint(0, 27, (nd,), dtype=torch.int32, device=dev, generator=gen)
+    y1 = torch.empty((1,), dtype=torch.int32, device=dev)
+    ms = time_graph([lambda: f5.gemv(v1, v2, out=y1)] * 2)
+    gbs = nd * 8 / (ms * 1e-3) / 1e9
+    res["k5_fgdp_dot_long"] = {"n": nd, "field": "GF(3^3) q=2^10", "ms": ms, "GBps": gbs, "frac_hbm": gbs / peak_hbm}
+    del v1, v2
     # C4, C5: GF(p^k) matrix products (pack + contraction), GF ops/s = 2 n^3 / t
     for cfg in (Q.C4, Q.C5):
         nn, k = cfg.n, cfg.k

@@ -43,4 +43,14 @@ void gfq_matmul_coeffs(std::span<const std::uint8_t> A, std::span<const std::uin
                        std::size_t K, std::size_t n, const GfqField& field, std::span<std::uint8_t> C,
                        std::uint32_t chunk = 0, CostReport* cost = nullptr);
 
+// y = A x over GF(p^k) on reps: A is m x K (row-major), x has K entries, y
+// gets m.  Each y_i is fgdp_dot(A[i,:], x) (gfq.hpp:98-99, gfq.cpp:335-387).
+void gfq_gemv(std::span<const GfqElt> A, std::span<const GfqElt> x, std::size_t m, const GfqField& field,
+              std::span<GfqElt> y, CostReport* cost = nullptr);
+
+// fgdp_dot of two long vectors on the GPU (one row of gfq_gemv, split over
+// the whole device)
+GfqElt fgdp_dot(std::span<const GfqElt> v1, std::span<const GfqElt> v2, const GfqField& field,
+                CostReport* cost = nullptr);
+
 }  // namespace qpack::gpu

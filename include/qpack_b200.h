@@ -143,6 +143,15 @@ QPK_API qpk_status qpk_gfq_matmul_rep(qpk_field f, const uint32_t* A, const uint
 QPK_API qpk_status qpk_gfq_matmul_rep_host(qpk_field f, const uint32_t* A, const uint32_t* B, uint64_t m,
                                            uint64_t K, uint64_t n, uint32_t* C, qpk_cost* cost);
 
+/* y = A x on reps: y_i = fgdp_dot(A[i,:], x)    gfq.hpp:98-99, gfq.cpp:335-387
+ * A m x K u32 reps (row-major), x K reps; outputs (either may be NULL):
+ * y_rep m reps, y_coeff m x k coefficient bytes.  m = 1 is a long fgdp_dot
+ * split over the whole device. */
+QPK_API qpk_status qpk_gfq_gemv(qpk_field f, const uint32_t* A, const uint32_t* x, uint64_t m, uint64_t K,
+                                uint32_t* y_rep, uint8_t* y_coeff, void* stream);
+QPK_API qpk_status qpk_gfq_gemv_host(qpk_field f, const uint32_t* A, const uint32_t* x, uint64_t m, uint64_t K,
+                                     uint32_t* y_rep, uint8_t* y_coeff, qpk_cost* cost);
+
 /* ------------------------------------- seeded synthetic inputs (rng.hpp) */
 /* out[i] = SplitMix64(seed): draw number start+i+1, mod bound (below()) */
 QPK_API qpk_status qpk_gen_draws(uint64_t seed, uint64_t start, uint64_t count, uint32_t bound, uint8_t* out,

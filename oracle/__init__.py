@@ -85,6 +85,7 @@ def oracle():
             _sig(lib, "qo_field_mul", U32, [VP, U32, U32])
             _sig(lib, "qo_field_add", U32, [VP, U32, U32])
             _sig(lib, "qo_fgdp_dot", U32, [VP, u32p, u32p, U64, U64, u64p])
+            _sig(lib, "qo_rep_to_bytes", None, [VP, U32, u8p])
             _sig(lib, "qo_gfq_mul_batch", I, [VP, u8p, u8p, U64, u8p, I])
             _sig(lib, "qo_gfq_matmul", I, [VP, u8p, u8p, U64, U64, U64, U64, U64, u8p, I])
             _sig(lib, "qo_gfq_freivalds", I, [VP, u8p, u8p, u8p, U64, U64, U64, U64, I])
@@ -233,6 +234,11 @@ class Field:
         cost = np.zeros(4, np.uint64)
         r = oracle().qo_fgdp_dot(self.h, v1, v2, v1.size, 1, cost)
         return int(r), cost
+
+    def rep_to_coeffs(self, rep):
+        c = np.zeros(self.k, np.uint8)
+        oracle().qo_rep_to_bytes(self.h, rep, c)
+        return c.tolist()
 
 
 class RefField:

@@ -118,6 +118,8 @@ SIGNATURES = {
     "qpk_gfq_matmul_host": (I, [VP, VP, VP, U64, U64, U64, U32, VP, PCost]),
     "qpk_gfq_matmul_rep": (I, [VP, VP, VP, U64, U64, U64, VP, VP]),
     "qpk_gfq_matmul_rep_host": (I, [VP, VP, VP, U64, U64, U64, VP, PCost]),
+    "qpk_gfq_gemv": (I, [VP, VP, VP, U64, U64, VP, VP, VP]),
+    "qpk_gfq_gemv_host": (I, [VP, VP, VP, U64, U64, VP, VP, PCost]),
     "qpk_gen_draws": (I, [U64, U64, U64, U32, VP, VP]),
     "qpk_gen_words": (I, [U64, U64, U64, U64, U32, VP, VP]),
     "qpk_gen_pairs": (I, [U64, U64, U32, U32, VP, VP, VP]),
@@ -320,6 +322,22 @@ class GfqField:
                                                                         "high"))))
         return t
 
+    @property
+    def n_q(self):
+        return self.info()["n_q"]
+
+    def to_coeffs(self, rep):
+        """to_coeffs (gfq.cpp:296-314): coefficient list of a rep, low first."""
+        if rep == self.order - 1:
+            return [0] * self.k
+        if getattr(self, "_antilog", None) is None:
+            self._antilog = self.tables()["antilog"]
+        idx, out = int(self._antilog[rep]), []
+        for _ in range(self.k):
+            out.append(idx % self.p)
+            idx //= self.p
+        return out
+
     def op(self, op, a, b=None):
         a = _host(a, np.uint32).reshape(-1)
         bb = _host(b, np.uint32).reshape(-1) if b is not None else None
@@ -383,6 +401,42 @@ class GfqField:
         _check(lib().qpk_gfq_matmul_host(self._h, _ptr(A), _ptr(B), m, K, n, chunk, _ptr(out), C.byref(cost)))
         self.last_cost = cost.as_dict()
         return out
+
+    def gemv(self, A, x, coeffs=False, out=None):
+        """y = A x on reps (A m x K, x K): each y_i = fgdp_dot(A[i,:], x) on
+        the GPU.  Returns reps (m,) or, with coeffs=True, coefficients (m, k)."""
+        if _is_torch(A):
+            import torch
+            m, K = A.shape
+            if out is None:
+                out = (torch.empty((m, self.k), dtype=torch.uint8, device=A.device) if coeffs
+                       else torch.empty((m,), dtype=torch.int32, device=A.device))
+            _check(lib().qpk_gfq_gemv(self._h, _ptr(A), _ptr(x), m, K, None if coeffs else _ptr(out),
+                                      _ptr(out) if coeffs else None, _stream()))
+            return out
+        A = _host(A, np.uint32)
+        x = _host(x, np.uint32).reshape(-1)
+        if A.ndim == 1:
+            A = A.reshape(1, -1)
+        m, K = A.shape
+        if x.size != K:
+            raise InvalidArgument("gfq_gemv: x length differs from the columns of A")
+        if out is None:
+            out = np.empty((m, self.k), np.uint8) if coeffs else np.empty((m,), np.uint32)
+        cost = Cost()
+        _check(lib().qpk_gfq_gemv_host(self._h, _ptr(A), _ptr(x), m, K, None if coeffs else _ptr(out),
+                                       _ptr(out) if coeffs else None, C.byref(cost)))
+        self.last_cost = cost.as_dict()
+        return out
+
+    def fgdp_dot_gpu(self, v1, v2):
+        """fgdp_dot of two long rep vectors on the GPU; (rep, counters)."""
+        v1 = _host(v1, np.uint32).reshape(-1)
+        v2 = _host(v2, np.uint32).reshape(-1)
+        if v1.size != v2.size:
+            raise InvalidArgument("fgdp_dot: vector length mismatch")  # gfq.cpp:337
+        y = self.gemv(v1.reshape(1, -1), v2)
+        return int(y[0]), self.last_cost
 
     def matmul_rep(self, A, B):
         """The reference gfq_matmul on GfqMatrix data (reps in, reps out)."""

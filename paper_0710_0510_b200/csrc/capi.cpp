@@ -379,6 +379,31 @@ qpk_status qpk_gfq_matmul_rep_host(qpk_field f, const uint32_t* A, const uint32_
     });
 }
 
+qpk_status qpk_gfq_gemv(qpk_field f, const uint32_t* A, const uint32_t* x, uint64_t m, uint64_t K, uint32_t* y_rep,
+                        uint8_t* y_coeff, void* stream) {
+    return guard([&] {
+        need(f != nullptr, "null field");
+        need(m == 0 || ((A || K == 0) && (x || K == 0) && (y_rep || y_coeff)), "null buffer");
+        qpack::gpu::gfq_gemv_device(qpack::detail::device_field(f->f), f->f, A, x, m, K, y_rep, y_coeff,
+                                    as_stream(stream));
+    });
+}
+
+qpk_status qpk_gfq_gemv_host(qpk_field f, const uint32_t* A, const uint32_t* x, uint64_t m, uint64_t K,
+                             uint32_t* y_rep, uint8_t* y_coeff, qpk_cost* cost) {
+    return guard([&] {
+        need(f != nullptr, "null field");
+        need(m == 0 || ((A || K == 0) && (x || K == 0) && (y_rep || y_coeff)), "null buffer");
+        const uint64_t order = f->f.order();
+        for (uint64_t i = 0; i < m * K; ++i)
+            if (A[i] >= order) throw std::out_of_range("gfq_gemv: rep outside the field");
+        for (uint64_t i = 0; i < K; ++i)
+            if (x[i] >= order) throw std::out_of_range("gfq_gemv: rep outside the field");
+        if (m) qpack::gpu::gfq_gemv_host(qpack::detail::device_field(f->f), f->f, A, x, m, K, y_rep, y_coeff);
+        put_cost(cost, qpack::gpu::gemv_cost(f->f, m, K));
+    });
+}
+
 // ---------------------------------------------------------------- inputs
 qpk_status qpk_gen_draws(uint64_t seed, uint64_t start, uint64_t count, uint32_t bound, uint8_t* out, void* stream) {
     return guard([&] {

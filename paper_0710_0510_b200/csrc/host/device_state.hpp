@@ -66,8 +66,10 @@ struct DeviceFieldCache {
     gpu::DevBuf fval;    // rep -> q-adic double
     qpk::GfqElemParams elem{};
     qpk::GfqMatmulParams mm{};
+    qpk::GfqGemvParams gemv{};
     uint32_t nlh = 0;
     gpu::DevBuf ws_a, ws_b;  // packed A^T and B
+    gpu::DevBuf ws_gemv;     // GEMV split partials
     gpu::DevBuf io_a, io_b, io_c;
     std::mutex mu;
     std::unique_ptr<gpu::Staging> staging;

@@ -229,6 +229,17 @@ DeviceFieldCache& device_field(const GfqField& f) {
     M.hc = E.hc;
     M.log = E.log;
     M.fval = c->fval.as<double>();
+    qpk::GfqGemvParams& G = c->gemv;
+    G.rq = rq;
+    G.k = k;
+    G.p = E.p;
+    G.order = E.order;
+    G.lh_radix = E.lh_radix;
+    G.lc = E.lc;
+    G.log = E.log;
+    G.fval = M.fval;
+    G.vals32 = 1;
+    for (const double v : FieldAccess::fval(f)) G.vals32 &= v < 4294967296.0 ? 1u : 0u;
     slot = std::move(c);
     return *slot;
 }
@@ -490,6 +501,66 @@ CostReport matmul_cost(const GfqField& field, u64 m, u64 K, u64 n) {
     c.divisions = c.reduction_calls = m * n * groups;
     c.table_accesses = 2 * m * n * K + 2 * m * n * groups;
     return c;
+}
+
+// ---- GEMV / long dot (K5) ----
+void gfq_gemv_device(DeviceFieldCache& F, const GfqField& field, const uint32_t* A, const uint32_t* x, u64 m, u64 K,
+                     uint32_t* y_rep, uint8_t* y_coeff, cudaStream_t s) {
+    if (m == 0) return;
+    const uint32_t splits = qpk::gemv_splits(m, K);
+    // products one lane accumulates: a split is rounded up to 128 elements,
+    // 4 per lane per 128
+    const u64 ksplit = (K + splits - 1) / splits;
+    const u64 lane_terms = (ksplit + 127) / 128 * 4;
+    // groups of at most n_q products per lane, as the reference's grouping
+    // (gfq.cpp:346-385); multiples of 4 keep the 16-byte vector path
+    const u64 n_q = field.params().n_q;
+    qpk::GfqGemvParams G = F.gemv;
+    G.chunk = lane_terms <= n_q ? 0u : static_cast<uint32_t>(n_q >= 4 ? n_q - n_q % 4 : n_q);
+    void* ws = F.ws_gemv.ensure(qpk::gemv_workspace_bytes(m, K, splits));
+    check(qpk::launch_gfq_gemv(G, A, x, m, K, splits, ws, y_rep, y_coeff, s), "gfq_gemv launch");
+}
+
+void gfq_gemv_host(DeviceFieldCache& F, const GfqField& field, const uint32_t* A, const uint32_t* x, u64 m, u64 K,
+                   uint32_t* y_rep, uint8_t* y_coeff) {
+    std::lock_guard<std::mutex> lock(F.mu);
+    auto* da = static_cast<uint32_t*>(F.io_a.ensure(std::max<u64>(m * K, 1) * 4));
+    auto* dx = static_cast<uint32_t*>(F.io_b.ensure(std::max<u64>(K, 1) * 4));
+    auto* dy = static_cast<uint8_t*>(F.io_c.ensure(m * (4 + field.k())));
+    if (m * K != 0) check(cudaMemcpy(da, A, m * K * 4, cudaMemcpyHostToDevice), "H2D");
+    if (K) check(cudaMemcpy(dx, x, K * 4, cudaMemcpyHostToDevice), "H2D");
+    uint32_t* dr = reinterpret_cast<uint32_t*>(dy);
+    uint8_t* dc = dy + m * 4;
+    gfq_gemv_device(F, field, da, dx, m, K, y_rep ? dr : nullptr, y_coeff ? dc : nullptr, 0);
+    if (y_rep) check(cudaMemcpy(y_rep, dr, m * 4, cudaMemcpyDeviceToHost), "D2H");
+    if (y_coeff) check(cudaMemcpy(y_coeff, dc, m * field.k(), cudaMemcpyDeviceToHost), "D2H");
+}
+
+CostReport gemv_cost(const GfqField& field, u64 m, u64 K) {
+    // per row the reference fgdp_dot's counters (gfq.cpp:346-385) minus the
+    // data-dependent Zech additions, as matmul_cost
+    return matmul_cost(field, m, K, 1);
+}
+
+void gfq_gemv(std::span<const GfqElt> A, std::span<const GfqElt> x, std::size_t m, const GfqField& field,
+              std::span<GfqElt> y, CostReport* cost) {
+    const u64 K = x.size();
+    if (A.size() != m * K || y.size() < m)
+        throw std::invalid_argument("gfq_gemv: span sizes do not match m x K / K / m");
+    for (const auto& v : {A, x})
+        for (const GfqElt& e : v)
+            if (e.rep >= field.order()) throw std::out_of_range("gfq_gemv: rep outside the field");
+    static_assert(sizeof(GfqElt) == 4, "GfqElt is one u32 rep");
+    gfq_gemv_host(detail::device_field(field), field, reinterpret_cast<const uint32_t*>(A.data()),
+                  reinterpret_cast<const uint32_t*>(x.data()), m, K, reinterpret_cast<uint32_t*>(y.data()), nullptr);
+    if (cost) *cost += gemv_cost(field, m, K);
+}
+
+GfqElt fgdp_dot(std::span<const GfqElt> v1, std::span<const GfqElt> v2, const GfqField& field, CostReport* cost) {
+    if (v1.size() != v2.size()) throw std::invalid_argument("fgdp_dot: vector length mismatch");
+    GfqElt r{};
+    gfq_gemv(v1, v2, 1, field, std::span<GfqElt>(&r, 1), cost);
+    return r;
 }
 
 void gfq_matmul_coeffs(std::span<const std::uint8_t> A, std::span<const std::uint8_t> B, std::size_t m, std::size_t K,

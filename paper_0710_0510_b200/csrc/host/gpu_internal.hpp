@@ -42,4 +42,10 @@ void gfq_matmul_host(detail::DeviceFieldCache& F, const GfqField& field, const v
                      u64 n, uint32_t chunk, void* C, bool reps);
 CostReport matmul_cost(const GfqField& field, u64 m, u64 K, u64 n);
 
+void gfq_gemv_device(detail::DeviceFieldCache& F, const GfqField& field, const uint32_t* A, const uint32_t* x, u64 m,
+                     u64 K, uint32_t* y_rep, uint8_t* y_coeff, cudaStream_t s);
+void gfq_gemv_host(detail::DeviceFieldCache& F, const GfqField& field, const uint32_t* A, const uint32_t* x, u64 m,
+                   u64 K, uint32_t* y_rep, uint8_t* y_coeff);
+CostReport gemv_cost(const GfqField& field, u64 m, u64 K);
+
 }  // namespace qpack::gpu

@@ -83,6 +83,17 @@ struct GfqMatmulParams {
     const double* fval;   // rep -> q-adic evaluation (float_eval, gfq.cpp:194-207)
 };
 
+// GF(p^k) matrix-vector product / long dot product on dlog reps (K5).
+struct GfqGemvParams {
+    RedqParams rq;        // d = 2k-2
+    uint32_t k, p, order, lh_radix;
+    uint32_t chunk;       // products per lane per REDQ group (<= n_q; 0 = one group)
+    uint32_t vals32;      // every packed value (fval) is below 2^32: u32 values, exact u64 MAC
+    const uint32_t* lc;   // lc | hc contiguous (lh_radix^k words each), as GfqElemParams
+    const uint32_t* log;  // p^k: coefficient index -> rep
+    const double* fval;   // rep -> q-adic evaluation (float_eval, gfq.cpp:194-207)
+};
+
 // ---- launchers (return cudaError_t of the launch) ----
 cudaError_t launch_redq_f64(const RedqParams& P, const double* words, uint64_t n, uint8_t* out,
                             uint32_t* status, cudaStream_t s);
@@ -108,6 +119,15 @@ cudaError_t launch_pack_reps(const double* fval, uint32_t order, const uint32_t*
 cudaError_t launch_gfq_matmul(const GfqMatmulParams& P, const double* at, const double* b, uint64_t m,
                               uint64_t n, uint64_t K_pad, uint64_t m_pad, uint64_t n_pad, uint8_t* out_coeffs,
                               uint32_t* out_reps, cudaStream_t s);
+
+// K5: y = A x over GF(p^k), A m x K reps (row-major), x K reps; `splits`
+// K-ranges per row (gemv_splits); ws: gemv_workspace_bytes (packed x and
+// split partials, 16-byte aligned).  Either output may be null: y_rep (m
+// reps) and/or y_coeff (m x k bytes).
+uint32_t gemv_splits(uint64_t m, uint64_t K);
+uint64_t gemv_workspace_bytes(uint64_t m, uint64_t K, uint32_t splits);
+cudaError_t launch_gfq_gemv(const GfqGemvParams& P, const uint32_t* A, const uint32_t* x, uint64_t m, uint64_t K,
+                            uint32_t splits, void* ws, uint32_t* y_rep, uint8_t* y_coeff, cudaStream_t s);
 
 // Synthetic inputs: out[i] = SplitMix64(seed) draw (start+i+1) mod bound.
 cudaError_t launch_gen_draws(uint64_t seed, uint64_t start, uint64_t count, uint32_t bound, uint8_t* out,

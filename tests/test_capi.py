@@ -156,3 +156,12 @@ def test_compute_entry_points_fail_loudly_without_a_device(qpk):
         qpk.GfqField(3, 2, 1 << 16).matmul(np.zeros((2, 2, 2), np.uint8), np.zeros((2, 2, 2), np.uint8), 2, 2, 2)
     with pytest.raises(qpk.CudaError):
         qpk.PolymulPlan(3, 32, 4, 1)
+    with pytest.raises(qpk.CudaError):
+        qpk.GfqField(3, 3, 1 << 10).gemv(np.zeros((2, 8), np.uint32), np.zeros(8, np.uint32))
+
+
+def test_to_coeffs_matches_oracle(qpk, orc):
+    f = qpk.GfqField(7, 3, 256)
+    of = orc.Field(7, 3, 256)
+    for rep in (0, 1, 5, 100, 341, 342):
+        assert f.to_coeffs(rep) == of.rep_to_coeffs(rep)
