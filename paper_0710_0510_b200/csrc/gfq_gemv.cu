@@ -102,64 +102,99 @@ __global__ void __launch_bounds__(kGemvThreads) gfq_gemv_kernel(const GfqGemvPar
     const int lane = threadIdx.x & 31;
     const V* tl = REPL ? tv + lane : tv;  // this lane's copy: entry e at tl[32 e]
     auto val = [&](uint32_t e) -> V { return REPL ? tl[e << 5] : tl[e]; };
-    const uint64_t warps = uint64_t(gridDim.x) * (kGemvThreads / 32);
+    // CTA-uniform rounds of 8 tasks; with many splits (a multiple of 8) the
+    // 8 tasks of a round are 8 consecutive splits of one row and the CTA adds
+    // them before writing one partial (slot split/8)
+    __shared__ uint32_t red[kGemvThreads / 32];
+    const bool cta_red = splits >= 64 && splits % 8 == 0;
+    const uint32_t warp = threadIdx.x >> 5;
     const uint64_t tasks = m * splits;
-    for (uint64_t t = uint64_t(blockIdx.x) * (kGemvThreads / 32) + (threadIdx.x >> 5); t < tasks; t += warps) {
+    for (uint64_t base = uint64_t(blockIdx.x) * 8; base < tasks; base += uint64_t(gridDim.x) * 8) {
+        const uint64_t t = base + warp;
         const uint64_t row = t / splits, s = t % splits;
-        const uint64_t k0 = s * ksplit, k1 = std::min<uint64_t>(Kd, k0 + ksplit);
-        const uint32_t* arow = A + row * Kd;
-        typename AC::T acc = 0;
-        uint32_t cnt = 0, csum = 0;
-        auto close_group = [&]() {
-            csum = add_mod_bytes_mm(csum, acc_to_coeffs<KR>(c, P.lh_radix, AC::word(acc), lc_s, hc_s), P.p);
-            acc = 0;
-            cnt = 0;
-        };
-        auto four = [&](const uint4& a, uint64_t j) {
-            V xs[4];
-            if constexpr (XREP) {
-                const uint4 b = ldg_stream(xr + j);  // few rows: x is streamed too
-                xs[0] = val(b.x), xs[1] = val(b.y), xs[2] = val(b.z), xs[3] = val(b.w);
-            } else if constexpr (INT) {
-                const V* xq = xv + j;
-                const uint4 b = __ldg(reinterpret_cast<const uint4*>(xq));
-                xs[0] = b.x, xs[1] = b.y, xs[2] = b.z, xs[3] = b.w;
+        uint32_t cf = 0;
+        if (t < tasks) {
+            const uint64_t k0 = s * ksplit, k1 = std::min<uint64_t>(Kd, k0 + ksplit);
+            const uint32_t* arow = A + row * Kd;
+            typename AC::T acc = 0;
+            uint32_t cnt = 0, csum = 0;
+            auto close_group = [&]() {
+                csum = add_mod_bytes_mm(csum, acc_to_coeffs<KR>(c, P.lh_radix, AC::word(acc), lc_s, hc_s), P.p);
+                acc = 0;
+                cnt = 0;
+            };
+            auto four = [&](const uint4& a, uint64_t j) {
+                V xs[4];
+                if constexpr (XREP) {
+                    const uint4 b = ldg_stream(xr + j);  // few rows: x is streamed too
+                    xs[0] = val(b.x), xs[1] = val(b.y), xs[2] = val(b.z), xs[3] = val(b.w);
+                } else if constexpr (INT) {
+                    const V* xq = xv + j;
+                    const uint4 b = __ldg(reinterpret_cast<const uint4*>(xq));
+                    xs[0] = b.x, xs[1] = b.y, xs[2] = b.z, xs[3] = b.w;
+                } else {
+                    const V* xq = xv + j;
+                    const double2 b0 = __ldg(reinterpret_cast<const double2*>(xq));
+                    const double2 b1 = __ldg(reinterpret_cast<const double2*>(xq) + 1);
+                    xs[0] = b0.x, xs[1] = b0.y, xs[2] = b1.x, xs[3] = b1.y;
+                }
+                AC::mac(acc, val(a.x), xs[0]);
+                AC::mac(acc, val(a.y), xs[1]);
+                AC::mac(acc, val(a.z), xs[2]);
+                AC::mac(acc, val(a.w), xs[3]);
+                if (P.chunk) {
+                    cnt += 4;
+                    if (cnt >= P.chunk) close_group();
+                }
+            };
+            if constexpr (VEC) {
+                // k0 and Kd are multiples of 4: every 16-byte vector is whole.
+                // Software pipelined: the next kGemvUnroll vectors of A are in
+                // flight while the current ones are multiplied.
+                constexpr uint64_t kStep = 128 * kGemvUnroll;
+                uint64_t j = k0 + 4 * lane;
+                if (j + kStep - 128 < k1) {
+                    uint4 cur[kGemvUnroll];
+#pragma unroll
+                    for (int u = 0; u < kGemvUnroll; ++u) cur[u] = ldg_stream(arow + j + 128 * u);
+                    for (; j + 2 * kStep - 128 < k1; j += kStep) {
+                        uint4 nxt[kGemvUnroll];
+#pragma unroll
+                        for (int u = 0; u < kGemvUnroll; ++u) nxt[u] = ldg_stream(arow + j + kStep + 128 * u);
+#pragma unroll
+                        for (int u = 0; u < kGemvUnroll; ++u) four(cur[u], j + 128 * u);
+#pragma unroll
+                        for (int u = 0; u < kGemvUnroll; ++u) cur[u] = nxt[u];
+                    }
+#pragma unroll
+                    for (int u = 0; u < kGemvUnroll; ++u) four(cur[u], j + 128 * u);
+                    j += kStep;
+                }
+                for (; j < k1; j += 128) four(ldg_stream(arow + j), j);
             } else {
-                const V* xq = xv + j;
-                const double2 b0 = __ldg(reinterpret_cast<const double2*>(xq));
-                const double2 b1 = __ldg(reinterpret_cast<const double2*>(xq) + 1);
-                xs[0] = b0.x, xs[1] = b0.y, xs[2] = b1.x, xs[3] = b1.y;
+                for (uint64_t j = k0 + lane; j < k1; j += 32) {
+                    AC::mac(acc, val(arow[j]), XREP ? val(xr[j]) : xv[j]);
+                    if (P.chunk && ++cnt >= P.chunk) close_group();
+                }
             }
-            AC::mac(acc, val(a.x), xs[0]);
-            AC::mac(acc, val(a.y), xs[1]);
-            AC::mac(acc, val(a.z), xs[2]);
-            AC::mac(acc, val(a.w), xs[3]);
-            if (P.chunk) {
-                cnt += 4;
-                if (cnt >= P.chunk) close_group();
-            }
-        };
-        if constexpr (VEC) {
-            // k0 and Kd are multiples of 4: every 16-byte vector is whole
-            uint64_t j = k0 + 4 * lane;
-            for (; j + 128 * (kGemvUnroll - 1) < k1; j += 128 * kGemvUnroll) {
-                uint4 a[kGemvUnroll];
+            cf = add_mod_bytes_mm(csum, acc_to_coeffs<KR>(c, P.lh_radix, AC::word(acc), lc_s, hc_s), P.p);
 #pragma unroll
-                for (int u = 0; u < kGemvUnroll; ++u) a[u] = ldg_stream(arow + j + 128 * u);
-#pragma unroll
-                for (int u = 0; u < kGemvUnroll; ++u) four(a[u], j + 128 * u);
-            }
-            for (; j < k1; j += 128) four(ldg_stream(arow + j), j);
-        } else {
-            for (uint64_t j = k0 + lane; j < k1; j += 32) {
-                AC::mac(acc, val(arow[j]), XREP ? val(xr[j]) : xv[j]);
-                if (P.chunk && ++cnt >= P.chunk) close_group();
-            }
+            for (int off = 16; off > 0; off >>= 1)
+                cf = add_mod_bytes_mm(cf, __shfl_xor_sync(0xffffffffu, cf, off), P.p);
         }
-        uint32_t cf = add_mod_bytes_mm(csum, acc_to_coeffs<KR>(c, P.lh_radix, AC::word(acc), lc_s, hc_s), P.p);
+        if (cta_red) {
+            if (lane == 0) red[warp] = cf;
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                uint32_t v = red[0];
 #pragma unroll
-        for (int off = 16; off > 0; off >>= 1) cf = add_mod_bytes_mm(cf, __shfl_xor_sync(0xffffffffu, cf, off), P.p);
-        if (lane == 0) ws[s * m + row] = cf;
+                for (int w = 1; w < kGemvThreads / 32; ++w) v = add_mod_bytes_mm(v, red[w], P.p);
+                ws[(base % splits) / 8 * m + base / splits] = v;
+            }
+            __syncthreads();
+        } else if (t < tasks && lane == 0) {
+            ws[s * m + row] = cf;
+        }
     }
 }
 
@@ -207,9 +242,13 @@ __global__ void __launch_bounds__(256) gemv_finish_cta_kernel(uint32_t p, uint32
     }
 }
 
+// raise a kernel's dynamic shared-memory limit to `bytes` (once per size)
 template <class F>
-cudaError_t allow_smem(F* fn) {
-    return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+cudaError_t allow_smem(F* fn, size_t bytes, size_t& cur) {
+    if (bytes <= cur || bytes <= 48 * 1024) return cudaSuccess;
+    const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
+    if (e == cudaSuccess) cur = bytes;
+    return e;
 }
 
 template <int KR, class K, bool INT, bool REPL, bool XREP>
@@ -220,23 +259,18 @@ cudaError_t run_gemv_v(const GfqGemvParams& P, const uint32_t* A, const void* xv
     uint32_t nlh = 1;
     for (int i = 0; i < KR; ++i) nlh *= P.lh_radix;
     const size_t smem = size_t(REPL ? P.order * 32 : P.order) * sizeof(V) + size_t(2 * nlh) * 4;
-    if (smem > 227 * 1024) return cudaErrorInvalidValue;
+    if (smem > 226 * 1024) return cudaErrorInvalidValue;  // + the static reduction slots
     const bool vec = Kd % 4 == 0 && ksplit % 128 == 0 && P.chunk % 4 == 0 && reinterpret_cast<uintptr_t>(A) % 16 == 0 &&
                      reinterpret_cast<uintptr_t>(xv) % 16 == 0;
-    static bool attr[2] = {false, false};
+    static size_t attr[2] = {0, 0};
     if (vec) {
-        if (!attr[1]) {
-            if (cudaError_t e = allow_smem(gfq_gemv_kernel<KR, K, true, INT, REPL, XREP>); e != cudaSuccess) return e;
-            attr[1] = true;
-        }
+        if (cudaError_t e = allow_smem(gfq_gemv_kernel<KR, K, true, INT, REPL, XREP>, smem, attr[1]); e != cudaSuccess)
+            return e;
         gfq_gemv_kernel<KR, K, true, INT, REPL, XREP>
             <<<grid, kGemvThreads, smem, s>>>(P, A, xv, m, Kd, splits, ksplit, ws);
     } else {
-        if (!attr[0]) {
-            if (cudaError_t e = allow_smem(gfq_gemv_kernel<KR, K, false, INT, REPL, XREP>); e != cudaSuccess)
-                return e;
-            attr[0] = true;
-        }
+        if (cudaError_t e = allow_smem(gfq_gemv_kernel<KR, K, false, INT, REPL, XREP>, smem, attr[0]); e != cudaSuccess)
+            return e;
         gfq_gemv_kernel<KR, K, false, INT, REPL, XREP>
             <<<grid, kGemvThreads, smem, s>>>(P, A, xv, m, Kd, splits, ksplit, ws);
     }
@@ -279,12 +313,16 @@ cudaError_t run_gemv(const GfqGemvParams& P, const uint32_t* A, const void* xv, 
 int num_sms();
 
 uint32_t gemv_splits(uint64_t m, uint64_t Kd) {
-    // tasks of ~1024 elements (the last-round imbalance stays small) and at
-    // least four rounds of tasks over the GPU's warps; a split is >= 128
-    const uint64_t warps = uint64_t(num_sms()) * 64;
-    uint64_t s = Kd / 1024;
-    if (m * std::max<uint64_t>(s, 1) < 4 * warps)
-        s = std::max(s, std::min<uint64_t>((4 * warps + m - 1) / m, Kd / 128));
+    // Measured on B200 (scripts/gemv_sweep*.py, 2^26-element shapes): a round
+    // of tasks just above the resident warp count W (4 CTAs x 8 warps per
+    // SM) costs a second round, so either every task fits one round (few
+    // rows: long tasks) or there are ~7 rounds (many rows: the tail is
+    // small); tasks stay >= 2048 elements.
+    const uint64_t W = uint64_t(num_sms()) * 32;
+    const uint64_t cap = std::max<uint64_t>(Kd / 2048, 1);
+    uint64_t s = m <= W / 2 ? std::max<uint64_t>(W * 9 / 10 / m, 1) : (7 * W + m - 1) / m;
+    s = std::min(s, cap);
+    if (s >= 64) s = s / 8 * 8;  // the kernel adds the 8 splits of a CTA round
     return static_cast<uint32_t>(std::clamp<uint64_t>(s, 1, 1u << 20));
 }
 
@@ -322,12 +360,13 @@ cudaError_t launch_gfq_gemv(const GfqGemvParams& P, const uint32_t* A, const uin
         default: return cudaErrorInvalidValue;
     }
     if (e != cudaSuccess) return e;
-    if (splits >= 64) {
+    const uint32_t parts = splits >= 64 && splits % 8 == 0 ? splits / 8 : splits;  // the kernel's CTA reduction
+    if (parts >= 64) {
         const int fgrid = static_cast<int>(std::min<uint64_t>(m, uint64_t(num_sms()) * 8));
-        gemv_finish_cta_kernel<<<fgrid, 256, 0, s>>>(P.p, P.k, P.log, part, m, splits, out_rep, out_coeff);
+        gemv_finish_cta_kernel<<<fgrid, 256, 0, s>>>(P.p, P.k, P.log, part, m, parts, out_rep, out_coeff);
     } else {
         const int fgrid = static_cast<int>(std::min<uint64_t>((m + 255) / 256, uint64_t(num_sms()) * 4));
-        gemv_finish_rows_kernel<<<fgrid, 256, 0, s>>>(P.p, P.k, P.log, part, m, splits, out_rep, out_coeff);
+        gemv_finish_rows_kernel<<<fgrid, 256, 0, s>>>(P.p, P.k, P.log, part, m, parts, out_rep, out_coeff);
     }
     return cudaGetLastError();
 }

@@ -507,7 +507,8 @@ CostReport matmul_cost(const GfqField& field, u64 m, u64 K, u64 n) {
 void gfq_gemv_device(DeviceFieldCache& F, const GfqField& field, const uint32_t* A, const uint32_t* x, u64 m, u64 K,
                      uint32_t* y_rep, uint8_t* y_coeff, cudaStream_t s) {
     if (m == 0) return;
-    const uint32_t splits = qpk::gemv_splits(m, K);
+    uint32_t splits = qpk::gemv_splits(m, K);
+    if (const char* e = std::getenv("QPK_GEMV_SPLITS")) splits = static_cast<uint32_t>(std::max(1, std::atoi(e)));  // dev knob
     // products one lane accumulates: a split is rounded up to 128 elements,
     // 4 per lane per 128
     const u64 ksplit = (K + splits - 1) / splits;
