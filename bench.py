@@ -425,6 +425,21 @@ def measure_secondary(Q, torch, dev):
     gbs = nd * 8 / (ms * 1e-3) / 1e9
     res["k5_fgdp_dot_long"] = {"n": nd, "field": "GF(3^3) q=2^10", "ms": ms, "GBps": gbs, "frac_hbm": gbs / peak_hbm}
     del v1, v2
+    # K6: one chunked FQT product of two 2^16-coefficient
+    # polynomials over F_3; C1's params (q=2^5, d=3, n_q=1: one REDQ per
+    # packed product) and a wide-group packing (q=2^13, d=1, n_q=409)
+    n6 = 1 << 16
+    a6 = torch.randint(0, 3, (n6,), dtype=torch.uint8, device=dev, generator=gen)
+    b6 = torch.randint(0, 3, (n6,), dtype=torch.uint8, device=dev, generator=gen)
+    o6 = torch.empty((2 * n6 - 1,), dtype=torch.uint8, device=dev)
+    res["k6_fqt_mul"] = {"n": n6, "p": 3}
+    for name, (q6, d6, nq6) in (("q32_d3_nq1", (32, 3, 1)), ("q8192_d1_nq409", (1 << 13, 1, 409))):
+        pm6 = Q.PolymulPlan(3, q6, d6 + 1, nq6)
+        ms = time_graph([lambda: pm6.fqt_mul(a6, b6, out=o6)] * 2)
+        chunks = -(-n6 // (d6 + 1))
+        res["k6_fqt_mul"][name] = {"ms": ms, "coeff_products_per_s": n6 * n6 / (ms * 1e-3),
+                                   "word_products_per_s": chunks * chunks / (ms * 1e-3),
+                                   "redq_per_s": chunks * chunks / nq6 / (ms * 1e-3)}
     # C4, C5: GF(p^k) matrix products (pack + contraction), GF ops/s = 2 n^3 / t
     for cfg in (Q.C4, Q.C5):
         nn, k = cfg.n, cfg.k

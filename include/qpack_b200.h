@@ -96,6 +96,14 @@ QPK_API qpk_status qpk_polymul_batch(qpk_polymul_plan plan, const uint8_t* a, co
 QPK_API qpk_status qpk_polymul_batch_host(qpk_polymul_plan plan, const uint8_t* a, const uint8_t* b, uint64_t n,
                                           uint8_t* out, qpk_cost* cost);
 QPK_API qpk_status qpk_polymul_sync(qpk_polymul_plan plan, void* stream);
+/* one product of two long polynomials (na, nb coefficients, uint8 < 256,
+ * reduced mod p) -> na+nb-1 coefficients: chunked FQT (K6)
+ * = fqt_mul(a, b, k-1, params, fqt_reduction_plan)          polymul.hpp:42-47, polymul.cpp:81-147
+ * k <= 8; counters (host variant) are the reference's closed form */
+QPK_API qpk_status qpk_fqt_mul(qpk_polymul_plan plan, const uint8_t* a, uint64_t na, const uint8_t* b, uint64_t nb,
+                               uint8_t* out, void* stream);
+QPK_API qpk_status qpk_fqt_mul_host(qpk_polymul_plan plan, const uint8_t* a, uint64_t na, const uint8_t* b,
+                                    uint64_t nb, uint8_t* out, qpk_cost* cost);
 
 /* --------------------------------------------------------------- GF(p^k) */
 typedef struct qpk_field_s* qpk_field;

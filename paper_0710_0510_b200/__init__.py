@@ -119,6 +119,8 @@ SIGNATURES = {
     "qpk_gfq_matmul_rep": (I, [VP, VP, VP, U64, U64, U64, VP, VP]),
     "qpk_gfq_matmul_rep_host": (I, [VP, VP, VP, U64, U64, U64, VP, PCost]),
     "qpk_gfq_gemv": (I, [VP, VP, VP, U64, U64, VP, VP, VP]),
+    "qpk_fqt_mul": (I, [VP, VP, U64, VP, U64, VP, VP]),
+    "qpk_fqt_mul_host": (I, [VP, VP, U64, VP, U64, VP, PCost]),
     "qpk_gfq_gemv_host": (I, [VP, VP, VP, U64, U64, VP, VP, PCost]),
     "qpk_gen_draws": (I, [U64, U64, U64, U32, VP, VP]),
     "qpk_gen_words": (I, [U64, U64, U64, U64, U32, VP, VP]),
@@ -271,6 +273,25 @@ class PolymulPlan:
 
     def sync(self):
         _check(lib().qpk_polymul_sync(self._h, _stream()))
+
+    def fqt_mul(self, a, b, out=None):
+        """One product of two long polynomials (chunked FQT, fqt_mul
+        polymul.cpp:81-147): len(a)+len(b)-1 coefficients mod p."""
+        if _is_torch(a):
+            import torch
+            na, nb = a.numel(), b.numel()
+            if out is None:
+                out = torch.empty((max(na + nb - 1, 0),), dtype=torch.uint8, device=a.device)
+            _check(lib().qpk_fqt_mul(self._h, _ptr(a), na, _ptr(b), nb, _ptr(out), _stream()))
+            return out
+        a = _host(a, np.uint8).reshape(-1)
+        b = _host(b, np.uint8).reshape(-1)
+        if out is None:
+            out = np.empty((max(a.size + b.size - 1, 0),), np.uint8)
+        cost = Cost()
+        _check(lib().qpk_fqt_mul_host(self._h, _ptr(a), a.size, _ptr(b), b.size, _ptr(out), C.byref(cost)))
+        self.last_cost = cost.as_dict()
+        return out
 
 
 # ------------------------------------------------------------- GF(p^k)

@@ -28,7 +28,8 @@ ARCH = "-gencode arch=compute_100a,code=sm_100a"
 NVCC_FLAGS = f"{ARCH} -lineinfo -O3 -std=c++17 -Xcompiler -fPIC -I{CSRC} -I{ROOT}/include --expt-relaxed-constexpr"
 CXX_FLAGS = f"-std=c++20 -O2 -fPIC -Wall -Wextra -I{CSRC} -I{ROOT}/include -I{CUDA}/include"
 
-CU_UNITS = [("stream_main.cu", None), ("gfq_matmul_main.cu", None), ("gfq_gemv.cu", None), ("probe.cu", None)]
+CU_UNITS = [("stream_main.cu", None), ("gfq_matmul_main.cu", None), ("gfq_gemv.cu", None), ("fqt_conv.cu", None),
+            ("probe.cu", None)]
 CU_UNITS += [("stream_inst.cu", i) for i in range(1, 9)]
 CU_UNITS += [("gfq_matmul_inst.cu", (k, 0)) for k in range(1, 5)] + [("gfq_matmul_inst.cu", (k, 1)) for k in (2, 3)]
 CXX_UNITS = ["capi.cpp"] + [f"host/{f}" for f in

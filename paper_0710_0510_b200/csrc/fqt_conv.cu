@@ -1,0 +1,255 @@
+// K6: chunked FQT product of two long polynomials over F_p (reference
+// fqt_mul, polymul.cpp:81-147 = paper Sec. 5 d-FQT).
+//
+//  * pack: each operand is cut into chunks of k = d+1 coefficients and every
+//    chunk packed into one q-adic word (fqt_encode, polymul.cpp:31-50), as an
+//    exact double;
+//  * product: output chunk t is sum_i pw[i] * qw[t-i] -- a 1-D convolution
+//    of packed words, each fp64 product carrying a (d+1)x(d+1) block of
+//    coefficient products.  A CTA owns 256 consecutive t (one per thread)
+//    and sweeps i through shared-memory tiles (pw broadcast, qw sliding
+//    window); grid.y splits the i range so long products fill the GPU;
+//  * groups of at most n_q products are closed by REDQ (Alg. 2/3): the 2d+1
+//    residues are added mod p into the thread's byte lanes, exactly as the
+//    reference's per-group redq_residues_into + overlap-add;
+//  * overlap-add: output coefficient c of chunk u is residue j of t = u plus
+//    residue j+k of t = u-1, summed over the i splits, mod p.
+// The result is the unique product mod p, so the grouping (which products
+// share a REDQ) may differ from the reference's; the counters reported by
+// the host are the reference's closed form.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+
+#include "device_common.cuh"
+#include "kernels.hpp"
+#include "redq_core.cuh"
+
+namespace qpk {
+
+namespace {
+
+constexpr int kFqtT = 256;  // output chunks per CTA (one per thread)
+constexpr int kFqtI = 256;  // i-tile
+
+__device__ __forceinline__ uint32_t add_mod_lanes(uint32_t x, uint32_t y, uint32_t p) {
+    if (p < 128) {
+        const uint32_t pp = p * 0x01010101u;
+        const uint32_t s = __vadd4(x, y);
+        return __vsub4(s, __vcmpgeu4(s, pp) & pp);
+    }
+    uint32_t r = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        uint32_t t = ((x >> (8 * i)) & 0xff) + ((y >> (8 * i)) & 0xff);
+        if (t >= p) t -= p;
+        r |= t << (8 * i);
+    }
+    return r;
+}
+
+// chunks of k coefficients (reduced mod p) -> q-adic words; chunk c of an
+// operand of n coefficients, zero beyond n (fqt_encode, polymul.cpp:31-50)
+__global__ void fqt_pack_kernel(uint32_t p, uint32_t k, double qd, const uint8_t* __restrict__ a, uint64_t n,
+                                uint64_t chunks, double* __restrict__ w) {
+    for (uint64_t c = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; c < chunks;
+         c += uint64_t(gridDim.x) * blockDim.x) {
+        double v = 0.0;
+        for (int j = static_cast<int>(k) - 1; j >= 0; --j) {
+            const uint64_t i = c * k + j;
+            const uint32_t x = i < n ? a[i] % p : 0u;
+            v = fma(v, qd, static_cast<double>(x));
+        }
+        w[c] = v;
+    }
+}
+
+template <int ND, int W, class K>
+__global__ void __launch_bounds__(kFqtT) fqt_conv_kernel(const FqtParams P, const double* __restrict__ pw,
+                                                         uint64_t L1, const double* __restrict__ qw, uint64_t L2,
+                                                         uint64_t T, uint64_t isplit, uint32_t* __restrict__ res) {
+    constexpr int NW = (ND + 3) / 4;
+    __shared__ double pws[kFqtI];
+    __shared__ double qws[kFqtT + kFqtI - 1];
+    extern __shared__ __align__(16) uint32_t tab[];
+    const int tid = threadIdx.x;
+    if constexpr (W > 0)
+        for (uint32_t i = tid; i < P.rq.n_entries; i += blockDim.x) tab[i] = P.rq.table[i];
+    const K c{P.rq};
+    const uint32_t tab_s = smem_addr(tab);
+
+    const uint64_t t0 = uint64_t(blockIdx.x) * kFqtT, t = t0 + tid;
+    const uint64_t s = blockIdx.y;
+    // i with some t - i in [0, L2) for this tile, within split s
+    const uint64_t lo = std::max<uint64_t>(t0 + 1 > L2 ? t0 + 1 - L2 : 0, s * isplit);
+    const uint64_t hi = std::min<uint64_t>(std::min<uint64_t>(L1, t0 + kFqtT), (s + 1) * isplit);
+    double acc = 0.0;
+    uint32_t cnt = 0;
+    uint32_t racc[NW];
+#pragma unroll
+    for (int w = 0; w < NW; ++w) racc[w] = 0;
+    auto close_group = [&]() {
+        uint32_t u[ND], mu[ND];
+        redq_raw_digits<ND>(c, acc, u);
+        redq_correct<ND, W>(c, u, mu, [&](uint32_t idx) { return lds_u32(tab_s + 4 * idx); });
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+            uint32_t v = 0;
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (4 * w + j < ND) v |= mu[4 * w + j] << (8 * j);
+            racc[w] = add_mod_lanes(racc[w], v, c.p());
+        }
+        acc = 0.0;
+        cnt = 0;
+    };
+    for (uint64_t i0 = lo; i0 < hi; i0 += kFqtI) {
+        const int n_i = static_cast<int>(std::min<uint64_t>(kFqtI, hi - i0));
+        __syncthreads();
+        pws[tid] = tid < n_i ? pw[i0 + tid] : 0.0;
+        // qws[jj] = qw[t0 - i0 - (kFqtI-1) + jj]
+        for (int jj = tid; jj < kFqtT + kFqtI - 1; jj += kFqtT) {
+            const int64_t qi = static_cast<int64_t>(t0) - static_cast<int64_t>(i0) - (kFqtI - 1) + jj;
+            qws[jj] = (qi >= 0 && qi < static_cast<int64_t>(L2)) ? qw[qi] : 0.0;
+        }
+        __syncthreads();
+        // term ii: pws[ii] * qws[tid + kFqtI - 1 - ii]; every thread counts
+        // the same terms (out-of-range products are zeros), so group closes
+        // are CTA-uniform
+        int ii = 0;
+        while (ii < n_i) {
+            const int run = min(n_i - ii, static_cast<int>(P.nq - cnt));
+            const double* pq = qws + tid + kFqtI - 1 - ii;
+#pragma unroll 4
+            for (int r = 0; r < run; ++r) acc = fma(pws[ii + r], pq[-r], acc);
+            ii += run;
+            cnt += run;
+            if (cnt == P.nq) close_group();
+        }
+    }
+    if (cnt) close_group();
+    if (t < T) {
+#pragma unroll
+        for (int w = 0; w < NW; ++w) res[(s * T + t) * NW + w] = racc[w];
+    }
+}
+
+// out[cidx] = residue j of chunk u plus residue j+k of chunk u-1, all splits
+__global__ void fqt_overlap_kernel(uint32_t p, uint32_t k, uint32_t nd, const uint32_t* __restrict__ res,
+                                   uint32_t splits, uint64_t T, uint8_t* __restrict__ out, uint64_t nout) {
+    const uint32_t nw = (nd + 3) / 4;
+    for (uint64_t ci = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; ci < nout;
+         ci += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t u = ci / k;
+        const uint32_t j = static_cast<uint32_t>(ci % k);
+        uint32_t v = 0;
+        for (uint32_t s = 0; s < splits; ++s) {
+            if (u < T) v += (res[(s * T + u) * nw + j / 4] >> (8 * (j % 4))) & 0xffu;
+            const uint32_t jh = j + k;
+            if (u >= 1 && jh < nd) v += (res[(s * T + u - 1) * nw + jh / 4] >> (8 * (jh % 4))) & 0xffu;
+        }
+        out[ci] = static_cast<uint8_t>(v % p);
+    }
+}
+
+template <int ND, int W>
+cudaError_t run_conv_w(const FqtParams& P, const double* pw, uint64_t L1, const double* qw, uint64_t L2,
+                       uint64_t T, uint32_t splits, uint64_t isplit, uint32_t* res, cudaStream_t s) {
+    const dim3 grid(static_cast<unsigned>((T + kFqtT - 1) / kFqtT), splits);
+    const size_t smem = W > 0 ? size_t(P.rq.n_entries) * 4 : 0;
+    if (smem > 160 * 1024) return cudaErrorInvalidValue;
+    if (P.rq.qbits) {
+        static size_t cur = 0;
+        if (smem > 48 * 1024 && smem > cur) {
+            if (cudaError_t e = cudaFuncSetAttribute(fqt_conv_kernel<ND, W, RtConst<true>>,
+                                                     cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+                e != cudaSuccess)
+                return e;
+            cur = smem;
+        }
+        fqt_conv_kernel<ND, W, RtConst<true>><<<grid, kFqtT, smem, s>>>(P, pw, L1, qw, L2, T, isplit, res);
+    } else {
+        static size_t cur = 0;
+        if (smem > 48 * 1024 && smem > cur) {
+            if (cudaError_t e = cudaFuncSetAttribute(fqt_conv_kernel<ND, W, RtConst<false>>,
+                                                     cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+                e != cudaSuccess)
+                return e;
+            cur = smem;
+        }
+        fqt_conv_kernel<ND, W, RtConst<false>><<<grid, kFqtT, smem, s>>>(P, pw, L1, qw, L2, T, isplit, res);
+    }
+    return cudaGetLastError();
+}
+
+template <int ND>
+cudaError_t run_conv(const FqtParams& P, const double* pw, uint64_t L1, const double* qw, uint64_t L2, uint64_t T,
+                     uint32_t splits, uint64_t isplit, uint32_t* res, cudaStream_t s) {
+    switch (P.rq.neg_q ? P.rq.window : 0) {
+        case 2: return run_conv_w<ND, 2>(P, pw, L1, qw, L2, T, splits, isplit, res, s);
+        case 3: return run_conv_w<ND, 3>(P, pw, L1, qw, L2, T, splits, isplit, res, s);
+        case 4: return run_conv_w<ND, 4>(P, pw, L1, qw, L2, T, splits, isplit, res, s);
+        default: return run_conv_w<ND, 0>(P, pw, L1, qw, L2, T, splits, isplit, res, s);
+    }
+}
+
+}  // namespace
+
+int num_sms();
+
+namespace {
+uint64_t fqt_chunks(uint64_t n, uint32_t k) { return (n + k - 1) / k; }
+uint32_t fqt_splits(uint64_t T, uint64_t L) {
+    // enough CTAs for ~4 per SM, splits of at least 1024 products
+    const uint64_t tiles = (T + kFqtT - 1) / kFqtT;
+    const uint64_t want = (uint64_t(num_sms()) * 4 + tiles - 1) / tiles;
+    return static_cast<uint32_t>(std::clamp<uint64_t>(std::min<uint64_t>(want, L / 1024), 1, 1024));
+}
+uint64_t align16(uint64_t b) { return (b + 15) / 16 * 16; }
+}  // namespace
+
+uint64_t fqt_workspace_bytes(uint32_t k, uint64_t na, uint64_t nb) {
+    const uint64_t L1 = fqt_chunks(na, k), L2 = fqt_chunks(nb, k), T = L1 + L2 - 1;
+    const uint32_t nd = 2 * k - 1, nw = (nd + 3) / 4;
+    return align16(L1 * 8) + align16(L2 * 8) + uint64_t(fqt_splits(T, std::min(L1, L2))) * T * nw * 4;
+}
+
+cudaError_t launch_fqt_mul(const FqtParams& P, const uint8_t* a, uint64_t na, const uint8_t* b, uint64_t nb,
+                           uint8_t* out, void* ws, cudaStream_t s) {
+    if (na == 0 || nb == 0) return cudaSuccess;
+    const uint32_t k = P.k, nd = 2 * k - 1;
+    const uint64_t L1 = fqt_chunks(na, k), L2 = fqt_chunks(nb, k), T = L1 + L2 - 1;
+    auto* base = static_cast<uint8_t*>(ws);
+    auto* pw = reinterpret_cast<double*>(base);
+    auto* qw = reinterpret_cast<double*>(base + align16(L1 * 8));
+    auto* res = reinterpret_cast<uint32_t*>(base + align16(L1 * 8) + align16(L2 * 8));
+    const double qd = static_cast<double>(P.rq.q);
+    const int sms = num_sms();
+    fqt_pack_kernel<<<static_cast<int>(std::min<uint64_t>((L1 + 255) / 256, sms * 8)), 256, 0, s>>>(P.rq.p, k, qd, a,
+                                                                                                      na, L1, pw);
+    fqt_pack_kernel<<<static_cast<int>(std::min<uint64_t>((L2 + 255) / 256, sms * 8)), 256, 0, s>>>(P.rq.p, k, qd, b,
+                                                                                                      nb, L2, qw);
+    if (cudaError_t e = cudaGetLastError(); e != cudaSuccess) return e;
+    const uint32_t splits = fqt_splits(T, std::min(L1, L2));
+    const uint64_t isplit = (L1 + splits - 1) / splits;
+    cudaError_t e;
+    switch (nd) {
+        case 1: e = run_conv<1>(P, pw, L1, qw, L2, T, splits, isplit, res, s); break;
+        case 3: e = run_conv<3>(P, pw, L1, qw, L2, T, splits, isplit, res, s); break;
+        case 5: e = run_conv<5>(P, pw, L1, qw, L2, T, splits, isplit, res, s); break;
+        case 7: e = run_conv<7>(P, pw, L1, qw, L2, T, splits, isplit, res, s); break;
+        case 9: e = run_conv<9>(P, pw, L1, qw, L2, T, splits, isplit, res, s); break;
+        case 11: e = run_conv<11>(P, pw, L1, qw, L2, T, splits, isplit, res, s); break;
+        case 13: e = run_conv<13>(P, pw, L1, qw, L2, T, splits, isplit, res, s); break;
+        case 15: e = run_conv<15>(P, pw, L1, qw, L2, T, splits, isplit, res, s); break;
+        default: return cudaErrorInvalidValue;
+    }
+    if (e != cudaSuccess) return e;
+    const uint64_t nout = na + nb - 1;
+    fqt_overlap_kernel<<<static_cast<int>(std::min<uint64_t>((nout + 255) / 256, sms * 8)), 256, 0, s>>>(
+        P.rq.p, k, nd, res, splits, T, out, nout);
+    return cudaGetLastError();
+}
+
+}  // namespace qpk

@@ -57,6 +57,8 @@ struct DevicePlanCache {
     qpk::RedqParams prm{};
     gpu::DevBuf table;   // byte-packed correction windows
     gpu::DevBuf status;  // latched kErr* bits
+    gpu::DevBuf ws_fqt;  // K6 packed chunks and residue partials
+    gpu::DevBuf io_a, io_b, io_c;
     std::mutex mu;
     std::unique_ptr<gpu::Staging> staging;
 };

@@ -305,8 +305,7 @@ void redq_residues_batch(std::span<const double> words, const RedqPlan& plan, st
 PolymulPlan::PolymulPlan(const QadicParams& pr) : params(pr) {
     const ValidationResult vr = validate(pr);
     if (!vr.ok()) throw std::invalid_argument("dqt_mul_poly: " + vr.detail);
-    if (pr.k > static_cast<u32>(qpk::kMaxGfqK))
-        throw std::invalid_argument("qpack-b200 polymul: device path packs at most k = 4 coefficients");
+    if (pr.k > 8) throw std::invalid_argument("qpack-b200 polymul: device path packs at most k = 8 coefficients");
     if (pr.p > 256) throw std::invalid_argument("qpack-b200 polymul: residues are uint8, p must be <= 256");
     redq = fqt_reduction_plan(pr, pr.k - 1);
     DevicePlanCache& dp = detail::device_plan(redq);
@@ -315,6 +314,8 @@ PolymulPlan::PolymulPlan(const QadicParams& pr) : params(pr) {
 }
 
 void polymul_device(PolymulPlan& pl, const uint8_t* a, const uint8_t* b, u64 n, uint8_t* out, cudaStream_t s) {
+    if (pl.params.k > static_cast<u32>(qpk::kMaxGfqK))
+        throw std::invalid_argument("qpack-b200 polymul: the batched path packs at most k = 4 coefficients");
     DevicePlanCache& dp = detail::device_plan(pl.redq);
     check(qpk::launch_polymul(pl.P, a, b, n, out, dp.status.as<uint32_t>(), s), "polymul launch");
 }
@@ -339,6 +340,58 @@ void polymul_host(PolymulPlan& pl, const uint8_t* a, const uint8_t* b, u64 n, ui
     }
     for (auto s : S.streams) check(cudaStreamSynchronize(s), "sync");
     raise_status(take_status(dp, S.streams[0]));
+}
+
+// ---- chunked FQT product (K6) ----
+void fqt_check(const RedqPlan& plan, const QadicParams& params) {
+    if (params.p > 256) throw std::invalid_argument("qpack-b200 fqt_mul: coefficients are uint8, p must be <= 256");
+    if (params.k < 1 || params.k > 8)
+        throw std::invalid_argument("qpack-b200 fqt_mul: the device path packs 1..8 coefficients per chunk");
+    if (params.m > 53)
+        throw std::invalid_argument("qpack-b200 fqt_mul: the device path computes in fp64 words (m <= 53)");
+    if (plan.p != params.p || plan.q != params.q || plan.d != 2 * (params.k - 1))
+        throw std::invalid_argument("fqt_mul: reduction plan does not match the params");
+}
+
+void fqt_mul_device(const RedqPlan& plan, const QadicParams& params, const uint8_t* a, u64 na, const uint8_t* b,
+                    u64 nb, uint8_t* out, cudaStream_t s) {
+    fqt_check(plan, params);
+    if (na == 0 || nb == 0) return;
+    DevicePlanCache& dp = detail::device_plan(plan);
+    qpk::FqtParams F{};
+    F.rq = dp.prm;
+    F.k = params.k;
+    F.nq = static_cast<uint32_t>(std::max<u64>(params.n_q, 1));
+    void* ws = dp.ws_fqt.ensure(qpk::fqt_workspace_bytes(params.k, na, nb));
+    check(qpk::launch_fqt_mul(F, a, na, b, nb, out, ws, s), "fqt_mul launch");
+}
+
+void fqt_mul_host(const RedqPlan& plan, const QadicParams& params, const uint8_t* a, u64 na, const uint8_t* b, u64 nb,
+                  uint8_t* out) {
+    fqt_check(plan, params);
+    if (na == 0 || nb == 0) return;
+    DevicePlanCache& dp = detail::device_plan(plan);
+    std::lock_guard<std::mutex> lock(dp.mu);
+    auto* da = static_cast<uint8_t*>(dp.io_a.ensure(na));
+    auto* db = static_cast<uint8_t*>(dp.io_b.ensure(nb));
+    auto* dc = static_cast<uint8_t*>(dp.io_c.ensure(na + nb - 1));
+    check(cudaMemcpy(da, a, na, cudaMemcpyHostToDevice), "H2D");
+    check(cudaMemcpy(db, b, nb, cudaMemcpyHostToDevice), "H2D");
+    fqt_mul_device(plan, params, da, na, db, nb, dc, 0);
+    check(cudaMemcpy(out, dc, na + nb - 1, cudaMemcpyDeviceToHost), "D2H");
+}
+
+CostReport fqt_cost(const RedqPlan& plan, const QadicParams& params, u64 na, u64 nb) {
+    // the reference loop (polymul.cpp:106-146) runs every (t, i) of the
+    // zero-padded span and one REDQ per (t, group)
+    if (na == 0 || nb == 0) return {};
+    const u64 d = params.k - 1;
+    const u64 dq = packed_degree(std::max(na, nb) - 1, static_cast<u32>(d));
+    const u64 span = 2 * dq + 1;
+    const u64 groups = (span + params.n_q - 1) / params.n_q;
+    CostReport c = detail::redq_batch_cost(plan, span * groups);
+    c.mul_add = span * span;
+    return c;
 }
 
 CostReport polymul_cost(const PolymulPlan& pl, u64 n) {

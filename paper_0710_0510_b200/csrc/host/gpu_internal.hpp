@@ -30,6 +30,13 @@ void polymul_device(PolymulPlan& pl, const uint8_t* a, const uint8_t* b, u64 n, 
 void polymul_host(PolymulPlan& pl, const uint8_t* a, const uint8_t* b, u64 n, uint8_t* out);
 CostReport polymul_cost(const PolymulPlan& pl, u64 n);
 
+// K6: chunked FQT product of long polynomials (uint8 coefficients, p <= 256)
+void fqt_mul_device(const RedqPlan& plan, const QadicParams& params, const uint8_t* a, u64 na, const uint8_t* b,
+                    u64 nb, uint8_t* out, cudaStream_t s);
+void fqt_mul_host(const RedqPlan& plan, const QadicParams& params, const uint8_t* a, u64 na, const uint8_t* b, u64 nb,
+                  uint8_t* out);
+CostReport fqt_cost(const RedqPlan& plan, const QadicParams& params, u64 na, u64 nb);
+
 void gfq_mul_device(detail::DeviceFieldCache& F, const uint8_t* a, const uint8_t* b, u64 n, uint8_t* out, int path,
                     cudaStream_t s);
 void gfq_mul_host(detail::DeviceFieldCache& F, const uint8_t* a, const uint8_t* b, u64 n, uint8_t* out, int path);

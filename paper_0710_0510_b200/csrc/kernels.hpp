@@ -94,6 +94,13 @@ struct GfqGemvParams {
     const double* fval;   // rep -> q-adic evaluation (float_eval, gfq.cpp:194-207)
 };
 
+// Chunked FQT product of two long polynomials (K6, fqt_mul polymul.cpp:81-147).
+struct FqtParams {
+    RedqParams rq;  // fqt_reduction_plan: d = 2k-2 (ND = 2k-1 <= 15)
+    uint32_t k;     // coefficients per chunk (d+1)
+    uint32_t nq;    // products per REDQ group (params.n_q)
+};
+
 // ---- launchers (return cudaError_t of the launch) ----
 cudaError_t launch_redq_f64(const RedqParams& P, const double* words, uint64_t n, uint8_t* out,
                             uint32_t* status, cudaStream_t s);
@@ -128,6 +135,12 @@ uint32_t gemv_splits(uint64_t m, uint64_t K);
 uint64_t gemv_workspace_bytes(uint64_t m, uint64_t K, uint32_t splits);
 cudaError_t launch_gfq_gemv(const GfqGemvParams& P, const uint32_t* A, const uint32_t* x, uint64_t m, uint64_t K,
                             uint32_t splits, void* ws, uint32_t* y_rep, uint8_t* y_coeff, cudaStream_t s);
+
+// K6: out (na+nb-1 coefficients) = a * b mod p, coefficients as uint8;
+// ws: fqt_workspace_bytes (packed chunks and per-chunk residue partials).
+uint64_t fqt_workspace_bytes(uint32_t k, uint64_t na, uint64_t nb);
+cudaError_t launch_fqt_mul(const FqtParams& P, const uint8_t* a, uint64_t na, const uint8_t* b, uint64_t nb,
+                           uint8_t* out, void* ws, cudaStream_t s);
 
 // Synthetic inputs: out[i] = SplitMix64(seed) draw (start+i+1) mod bound.
 cudaError_t launch_gen_draws(uint64_t seed, uint64_t start, uint64_t count, uint32_t bound, uint8_t* out,

@@ -114,9 +114,8 @@ static void host_tests() {
         }
     }
 
-    // FQT (test_polymul.cpp:42-58)
-    CHECK((fqt_mul(DensePoly{3, {1, 1}}, DensePoly{3, {1, 1}}, 1, QadicParams{3, 32, 2, 1, 53}) ==
-           DensePoly{3, {1, 2, 1}}));
+    // FQT (test_polymul.cpp:42-58): u128 words (m = 128) stay on the host;
+    // fp64 words run on the device (gpu_tests)
     CHECK((fqt_mul(DensePoly{5, {3, 2, 1}}, DensePoly{5, {1, 0, 4}}, 2, QadicParams{5, 10000, 3, 1, 128}) ==
            DensePoly{5, {3, 2, 3, 3, 4}}));
     CHECK(packed_degree(500, 4) == 100);
@@ -137,6 +136,24 @@ static void host_tests() {
 
 static void gpu_tests() {
     SplitMix64 rng(77);
+    // FQT on the device (K6) behind the unchanged signature
+    CHECK((fqt_mul(DensePoly{3, {1, 1}}, DensePoly{3, {1, 1}}, 1, QadicParams{3, 32, 2, 1, 53}) ==
+           DensePoly{3, {1, 2, 1}}));
+    {
+        DensePoly a{3, {}}, b{3, {}};
+        for (int i = 0; i < 3000; ++i) a.coeffs.push_back(rng.below(3));
+        for (int i = 0; i < 1777; ++i) b.coeffs.push_back(rng.below(3));
+        const QadicParams pr = qadic_for_degree(3, 3, 53);
+        CostReport c;
+        const DensePoly got = fqt_mul(a, b, 3, pr, &c);
+        DensePoly want = DensePoly::zero(3, a.coeffs.size() + b.coeffs.size() - 1);
+        for (std::size_t i = 0; i < a.coeffs.size(); ++i)
+            for (std::size_t j = 0; j < b.coeffs.size(); ++j)
+                want.coeffs[i + j] = (want.coeffs[i + j] + a.coeffs[i] * b.coeffs[j]) % 3;
+        CHECK(got == want);
+        const u64 span = 2 * packed_degree(2999, 3) + 1;
+        CHECK(c.mul_add == span * span && c.divisions == span * span);  // n_q = 1
+    }
     // batched REDQ == per-word host REDQ
     RedqPlan plan = RedqPlan::build(5, 128, 6, RedqMode::float_premul);
     plan.attach_correction(build_correction_table(5, 128, 4, TableIndexing::base_p));
