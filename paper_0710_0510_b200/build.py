@@ -21,6 +21,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 BUILD = os.path.join(PKG, "_build")
 LIB = os.path.join(PKG, "lib", "libqpack_b200.so")
+TOOL = os.path.join(PKG, "bin", "qpack_b200")
 CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA, "bin", "nvcc")
 ARCH = "-gencode arch=compute_100a,code=sm_100a"
@@ -72,13 +73,24 @@ def _ninja_text() -> str:
         lines.append(f"build {obj}: cxx {os.path.join(CSRC, src)}")
         objs.append(obj)
     lines.append(f"build {LIB}: link {' '.join(objs)}")
-    lines.append(f"default {LIB}")
+    # the reference CLI surface (tools/qpack_b200.cpp) over the library
+    lines += [
+        "rule tool",
+        f"  command = g++ $cxxflags -MMD -MF $out.d $in -o $out -L{os.path.dirname(LIB)} -lqpack_b200 "
+        "-Wl,-rpath,'$$ORIGIN/../lib'",
+        "  depfile = $out.d",
+        "  deps = gcc",
+        "  description = TOOL $out",
+        f"build {TOOL}: tool {os.path.join(ROOT, 'tools', 'qpack_b200.cpp')} | {LIB}",
+    ]
+    lines.append(f"default {LIB} {TOOL}")
     return "\n".join(lines) + "\n"
 
 
 def build(verbose: bool = False) -> str:
     os.makedirs(BUILD, exist_ok=True)
     os.makedirs(os.path.dirname(LIB), exist_ok=True)
+    os.makedirs(os.path.dirname(TOOL), exist_ok=True)
     nf = os.path.join(BUILD, "build.ninja")
     text = _ninja_text()
     if not os.path.exists(nf) or open(nf).read() != text:
