@@ -289,7 +289,7 @@ def run_ours(args, rank, world, local_rank):
                    "parallelism": f"dp{world} (independent word shards, no collective)"},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": world * N_WORDS * 8,
                 "d2h_bytes_per_step": world * N_WORDS * ND, "steps": e2e_steps,
-                "path": "qpk_redq_residues_f64_host (pinned host buffers, 3-stream chunked H2D/kernel/D2H)"},
+                "path": "qpk_redq_residues_f64_host (pinned host buffers; 2M-word chunks: H2D stream -> kernel stream -> D2H stream, 4 buffer slots)"},
         "gpu_launches": args.steps,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "peak_source": peak_src,

@@ -42,11 +42,17 @@ void* DevBuf::ensure(std::size_t n) {
 }
 
 Staging::Staging() {
-    for (auto& s : streams) check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "cudaStreamCreate");
+    for (cudaStream_t* s : {&sh, &sk, &sd}) check(cudaStreamCreateWithFlags(s, cudaStreamNonBlocking), "cudaStreamCreate");
+    for (int i = 0; i < kSlots; ++i)
+        for (cudaEvent_t* e : {&ev_in[i], &ev_k[i], &ev_out[i]})
+            check(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "cudaEventCreate");
 }
 
 Staging::~Staging() {
-    for (auto& s : streams)
+    for (int i = 0; i < kSlots; ++i)
+        for (cudaEvent_t e : {ev_in[i], ev_k[i], ev_out[i]})
+            if (e) cudaEventDestroy(e);
+    for (cudaStream_t s : {sh, sk, sd})
         if (s) cudaStreamDestroy(s);
 }
 
@@ -277,19 +283,26 @@ void redq_host(DevicePlanCache& dp, const double* h_words, u64 n, uint8_t* h_out
     const u64 nd = dp.prm.d + 1;
     // 16 MB of words per chunk: short pipeline fill/drain against PCIe
     // (measured Gen5 x16: 55.6 GB/s H2D, 57.2 D2H, 100 GB/s both ways)
-    const u64 chunk = u64(1) << 21;
-    for (u64 off = 0, c = 0; off < n; off += chunk, ++c) {
-        const int si = static_cast<int>(c % Staging::kStreams);
-        cudaStream_t s = S.streams[si];
-        const u64 cnt = std::min(chunk, n - off);
-        double* din = static_cast<double*>(S.in0[si].ensure(chunk * 8));
-        uint8_t* dout = static_cast<uint8_t*>(S.out[si].ensure(chunk * nd));
-        check(cudaMemcpyAsync(din, h_words + off, cnt * 8, cudaMemcpyHostToDevice, s), "H2D");
-        redq_device(dp, din, cnt, dout, s);
-        check(cudaMemcpyAsync(h_out + off * nd, dout, cnt * nd, cudaMemcpyDeviceToHost, s), "D2H");
+    static const u64 chunk = [] {
+        const char* e = std::getenv("QPK_HOST_CHUNK_LOG2");  // dev knob (scripts/pcie_probe.py)
+        return u64(1) << (e ? std::clamp(std::atoi(e), 16, 26) : 21);
+    }();
+    for (int sl = 0; sl < Staging::kSlots; ++sl) {
+        S.in0[sl].ensure(chunk * 8);
+        S.out[sl].ensure(chunk * nd);
     }
-    for (auto s : S.streams) check(cudaStreamSynchronize(s), "sync");
-    raise_status(take_status(dp, S.streams[0]));
+    S.run(
+        n, chunk,
+        [&](int sl, u64 off, u64 cnt, cudaStream_t s) {
+            check(cudaMemcpyAsync(S.in0[sl].ptr, h_words + off, cnt * 8, cudaMemcpyHostToDevice, s), "H2D");
+        },
+        [&](int sl, u64, u64 cnt, cudaStream_t s) {
+            redq_device(dp, S.in0[sl].as<double>(), cnt, S.out[sl].as<uint8_t>(), s);
+        },
+        [&](int sl, u64 off, u64 cnt, cudaStream_t s) {
+            check(cudaMemcpyAsync(h_out + off * nd, S.out[sl].ptr, cnt * nd, cudaMemcpyDeviceToHost, s), "D2H");
+        });
+    raise_status(take_status(dp, S.sk));
 }
 
 void redq_residues_batch(std::span<const double> words, const RedqPlan& plan, std::span<std::uint8_t> out,
@@ -326,20 +339,24 @@ void polymul_host(PolymulPlan& pl, const uint8_t* a, const uint8_t* b, u64 n, ui
     if (!dp.staging) dp.staging = std::make_unique<Staging>();
     Staging& S = *dp.staging;
     const u64 k = pl.params.k, ko = 2 * k - 1, chunk = u64(1) << 22;
-    for (u64 off = 0, c = 0; off < n; off += chunk, ++c) {
-        const int si = static_cast<int>(c % Staging::kStreams);
-        cudaStream_t s = S.streams[si];
-        const u64 cnt = std::min(chunk, n - off);
-        auto* da = static_cast<uint8_t*>(S.in0[si].ensure(chunk * k));
-        auto* db = static_cast<uint8_t*>(S.in1[si].ensure(chunk * k));
-        auto* dout = static_cast<uint8_t*>(S.out[si].ensure(chunk * ko));
-        check(cudaMemcpyAsync(da, a + off * k, cnt * k, cudaMemcpyHostToDevice, s), "H2D");
-        check(cudaMemcpyAsync(db, b + off * k, cnt * k, cudaMemcpyHostToDevice, s), "H2D");
-        polymul_device(pl, da, db, cnt, dout, s);
-        check(cudaMemcpyAsync(out + off * ko, dout, cnt * ko, cudaMemcpyDeviceToHost, s), "D2H");
+    for (int sl = 0; sl < Staging::kSlots; ++sl) {
+        S.in0[sl].ensure(chunk * k);
+        S.in1[sl].ensure(chunk * k);
+        S.out[sl].ensure(chunk * ko);
     }
-    for (auto s : S.streams) check(cudaStreamSynchronize(s), "sync");
-    raise_status(take_status(dp, S.streams[0]));
+    S.run(
+        n, chunk,
+        [&](int sl, u64 off, u64 cnt, cudaStream_t s) {
+            check(cudaMemcpyAsync(S.in0[sl].ptr, a + off * k, cnt * k, cudaMemcpyHostToDevice, s), "H2D");
+            check(cudaMemcpyAsync(S.in1[sl].ptr, b + off * k, cnt * k, cudaMemcpyHostToDevice, s), "H2D");
+        },
+        [&](int sl, u64, u64 cnt, cudaStream_t s) {
+            polymul_device(pl, S.in0[sl].as<uint8_t>(), S.in1[sl].as<uint8_t>(), cnt, S.out[sl].as<uint8_t>(), s);
+        },
+        [&](int sl, u64 off, u64 cnt, cudaStream_t s) {
+            check(cudaMemcpyAsync(out + off * ko, S.out[sl].ptr, cnt * ko, cudaMemcpyDeviceToHost, s), "D2H");
+        });
+    raise_status(take_status(dp, S.sk));
 }
 
 // ---- chunked FQT product (K6) ----
@@ -432,19 +449,23 @@ void gfq_mul_host(DeviceFieldCache& F, const uint8_t* a, const uint8_t* b, u64 n
     if (!F.staging) F.staging = std::make_unique<Staging>();
     Staging& S = *F.staging;
     const u64 k = F.elem.k, chunk = u64(1) << 22;
-    for (u64 off = 0, c = 0; off < n; off += chunk, ++c) {
-        const int si = static_cast<int>(c % Staging::kStreams);
-        cudaStream_t s = S.streams[si];
-        const u64 cnt = std::min(chunk, n - off);
-        auto* da = static_cast<uint8_t*>(S.in0[si].ensure(chunk * k));
-        auto* db = static_cast<uint8_t*>(S.in1[si].ensure(chunk * k));
-        auto* dout = static_cast<uint8_t*>(S.out[si].ensure(chunk * k));
-        check(cudaMemcpyAsync(da, a + off * k, cnt * k, cudaMemcpyHostToDevice, s), "H2D");
-        check(cudaMemcpyAsync(db, b + off * k, cnt * k, cudaMemcpyHostToDevice, s), "H2D");
-        gfq_mul_device(F, da, db, cnt, dout, path, s);
-        check(cudaMemcpyAsync(out + off * k, dout, cnt * k, cudaMemcpyDeviceToHost, s), "D2H");
+    for (int sl = 0; sl < Staging::kSlots; ++sl) {
+        S.in0[sl].ensure(chunk * k);
+        S.in1[sl].ensure(chunk * k);
+        S.out[sl].ensure(chunk * k);
     }
-    for (auto s : S.streams) check(cudaStreamSynchronize(s), "sync");
+    S.run(
+        n, chunk,
+        [&](int sl, u64 off, u64 cnt, cudaStream_t s) {
+            check(cudaMemcpyAsync(S.in0[sl].ptr, a + off * k, cnt * k, cudaMemcpyHostToDevice, s), "H2D");
+            check(cudaMemcpyAsync(S.in1[sl].ptr, b + off * k, cnt * k, cudaMemcpyHostToDevice, s), "H2D");
+        },
+        [&](int sl, u64, u64 cnt, cudaStream_t s) {
+            gfq_mul_device(F, S.in0[sl].as<uint8_t>(), S.in1[sl].as<uint8_t>(), cnt, S.out[sl].as<uint8_t>(), path, s);
+        },
+        [&](int sl, u64 off, u64 cnt, cudaStream_t s) {
+            check(cudaMemcpyAsync(out + off * k, S.out[sl].ptr, cnt * k, cudaMemcpyDeviceToHost, s), "D2H");
+        });
 }
 
 void gfq_mul_batch(std::span<const std::uint8_t> a, std::span<const std::uint8_t> b, const GfqField& field,
