@@ -308,7 +308,8 @@ def measure_secondary(Q, torch, dev):
     res = {}
     peak_hbm, _ = measured_peaks()
     fp64_peak = Q.probe_fp64(1, 8192)
-    res["fp64_peaks_tflops"] = {"dmma_probe": fp64_peak, "dfma_probe": Q.probe_fp64(0, 8192), "nominal": 37.0}
+    dfma_peak = Q.probe_fp64(0, 8192)
+    res["fp64_peaks_tflops"] = {"dmma_probe": fp64_peak, "dfma_probe": dfma_peak, "nominal": 37.0}
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
     def time_it(fn, reps, warm=3, cold=True):
@@ -437,9 +438,10 @@ def measure_secondary(Q, torch, dev):
         pm6 = Q.PolymulPlan(3, q6, d6 + 1, nq6)
         ms = time_graph([lambda: pm6.fqt_mul(a6, b6, out=o6)] * 2)
         chunks = -(-n6 // (d6 + 1))
+        wp = chunks * chunks / (ms * 1e-3)
         res["k6_fqt_mul"][name] = {"ms": ms, "coeff_products_per_s": n6 * n6 / (ms * 1e-3),
-                                   "word_products_per_s": chunks * chunks / (ms * 1e-3),
-                                   "redq_per_s": chunks * chunks / nq6 / (ms * 1e-3)}
+                                   "word_products_per_s": wp, "redq_per_s": wp / nq6,
+                                   "fp64_tflops": 2 * wp / 1e12, "frac_dfma_probe": 2 * wp / 1e12 / dfma_peak}
     # C4, C5: GF(p^k) matrix products (pack + contraction), GF ops/s = 2 n^3 / t
     for cfg in (Q.C4, Q.C5):
         nn, k = cfg.n, cfg.k

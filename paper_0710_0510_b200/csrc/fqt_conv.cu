@@ -6,9 +6,10 @@
 //    exact double;
 //  * product: output chunk t is sum_i pw[i] * qw[t-i] -- a 1-D convolution
 //    of packed words, each fp64 product carrying a (d+1)x(d+1) block of
-//    coefficient products.  A CTA owns 256 consecutive t (one per thread)
-//    and sweeps i through shared-memory tiles (pw broadcast, qw sliding
-//    window); grid.y splits the i range so long products fill the GPU;
+//    coefficient products.  A CTA sweeps i through shared-memory tiles (pw
+//    broadcast, qw sliding window) for 2048 consecutive t, 8 per thread in
+//    registers (n_q >= 8), or 256 t, one per thread, when a REDQ follows
+//    nearly every product (n_q < 8); grid.y splits the i range;
 //  * groups of at most n_q products are closed by REDQ (Alg. 2/3): the 2d+1
 //    residues are added mod p into the thread's byte lanes, exactly as the
 //    reference's per-group redq_residues_into + overlap-add;
@@ -65,8 +66,11 @@ __global__ void fqt_pack_kernel(uint32_t p, uint32_t k, double qd, const uint8_t
     }
 }
 
+// n_q < 8 (e.g. C1's q = 2^5, d = 3, n_q = 1): one output chunk per thread,
+// a REDQ after every group of at most n_q products; the register-blocked
+// kernel would run 8 REDQs per step at a quarter of the occupancy.
 template <int ND, int W, class K>
-__global__ void __launch_bounds__(kFqtT) fqt_conv_kernel(const FqtParams P, const double* __restrict__ pw,
+__global__ void __launch_bounds__(kFqtT) fqt_conv_step_kernel(const FqtParams P, const double* __restrict__ pw,
                                                          uint64_t L1, const double* __restrict__ qw, uint64_t L2,
                                                          uint64_t T, uint64_t isplit, uint32_t* __restrict__ res) {
     constexpr int NW = (ND + 3) / 4;
@@ -135,6 +139,126 @@ __global__ void __launch_bounds__(kFqtT) fqt_conv_kernel(const FqtParams P, cons
     }
 }
 
+// Register-blocked convolution: thread `tid` of a CTA owns the RB = 8
+// consecutive output chunks t0 + 8 tid + r.  Step i needs qw[t - i] for its
+// eight t, the step after shifts that window down by one, so eight steps
+// read 15 window values (7 carried over) and one broadcast pw each: 64 FMAs
+// per 8 + 8 shared loads.  The qw tile is stored with one pad double per 8
+// (element j at j + j/8): lanes 8 apart in j land 9 doubles apart, 16 lanes
+// per 128-byte wavefront -- conflict-free.
+// STEP: close a group after every product (n_q < 8); else every G = n_q
+// rounded down to 8 products, checked per 8-step block.
+constexpr int kRB = 8;
+constexpr int kFqtOut = kFqtT * kRB;       // output chunks per CTA
+constexpr int kQw = kFqtOut + kFqtI - 1;   // window values per i-tile
+constexpr int kQwPad = kQw + kQw / 8 + 1;  // padded smem doubles
+
+__device__ __forceinline__ int qpad(int j) { return j + (j >> 3); }
+
+template <int ND, int W, class K, bool STEP>
+__global__ void __launch_bounds__(kFqtT) fqt_conv_kernel(const FqtParams P, const double* __restrict__ pw,
+                                                         uint64_t L1, const double* __restrict__ qw, uint64_t L2,
+                                                         uint64_t T, uint64_t isplit, uint32_t* __restrict__ res) {
+    constexpr int NW = (ND + 3) / 4;
+    __shared__ double pws[kFqtI];
+    __shared__ double qws[kQwPad];
+    extern __shared__ __align__(16) uint32_t tab[];
+    const int tid = threadIdx.x;
+    if constexpr (W > 0)
+        for (uint32_t i = tid; i < P.rq.n_entries; i += blockDim.x) tab[i] = P.rq.table[i];
+    const K c{P.rq};
+    const uint32_t tab_s = smem_addr(tab);
+
+    const uint64_t t0 = uint64_t(blockIdx.x) * kFqtOut;
+    const uint64_t s = blockIdx.y;
+    // i with some t - i in [0, L2) for this tile, within split s
+    const uint64_t lo = std::max<uint64_t>(t0 + 1 > L2 ? t0 + 1 - L2 : 0, s * isplit);
+    const uint64_t hi = std::min<uint64_t>(std::min<uint64_t>(L1, t0 + kFqtOut), (s + 1) * isplit);
+    double acc[kRB];
+    uint32_t racc[kRB][NW];
+#pragma unroll
+    for (int r = 0; r < kRB; ++r) {
+        acc[r] = 0.0;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) racc[r][w] = 0;
+    }
+    uint32_t cnt = 0;
+    const uint32_t G = STEP ? 1u : P.nq - P.nq % 8;
+    auto close_groups = [&]() {
+#pragma unroll
+        for (int r = 0; r < kRB; ++r) {
+            uint32_t u[ND], mu[ND];
+            redq_raw_digits<ND>(c, acc[r], u);
+            redq_correct<ND, W>(c, u, mu, [&](uint32_t idx) { return lds_u32(tab_s + 4 * idx); });
+#pragma unroll
+            for (int w = 0; w < NW; ++w) {
+                uint32_t v = 0;
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    if (4 * w + j < ND) v |= mu[4 * w + j] << (8 * j);
+                racc[r][w] = add_mod_lanes(racc[r][w], v, c.p());
+            }
+            acc[r] = 0.0;
+        }
+        cnt = 0;
+    };
+    for (uint64_t i0 = lo; i0 < hi; i0 += kFqtI) {
+        const int n_i = static_cast<int>(std::min<uint64_t>(kFqtI, hi - i0));
+        __syncthreads();
+        // zero past n_i: the unrolled 8-step blocks may run past the tile end
+        pws[tid] = tid < n_i ? pw[i0 + tid] : 0.0;
+        // Q(j) = qw[t0 - i0 - (kFqtI-1) + j], stored at qpad(j)
+        for (int j = tid; j < kQw; j += kFqtT) {
+            const int64_t qi = static_cast<int64_t>(t0) - static_cast<int64_t>(i0) - (kFqtI - 1) + j;
+            qws[qpad(j)] = (qi >= 0 && qi < static_cast<int64_t>(L2)) ? qw[qi] : 0.0;
+        }
+        __syncthreads();
+        // step ii, output r: Q(8 tid + r + kFqtI - 1 - ii).  Block of 8 steps
+        // from ii0: X[m] = Q(8 tid + kFqtI - 8 - ii0 + m), m = 0..14, step s
+        // output r uses X[7 - s + r]
+        double X[15];
+        const int jb = kRB * tid + kFqtI - 8;
+#pragma unroll
+        for (int m = 8; m < 15; ++m) X[m] = qws[qpad(jb + m)];
+        for (int ii0 = 0; ii0 < n_i; ii0 += 8) {
+#pragma unroll
+            for (int m = 0; m < 8; ++m) X[m] = qws[qpad(jb - ii0 + m)];
+            double pv[8];
+#pragma unroll
+            for (int m = 0; m < 8; ++m) pv[m] = pws[ii0 + m];
+            if constexpr (STEP) {
+#pragma unroll
+                for (int st = 0; st < 8; ++st) {
+                    if (ii0 + st < n_i) {
+#pragma unroll
+                        for (int r = 0; r < kRB; ++r) acc[r] = fma(pv[st], X[7 - st + r], acc[r]);
+                        close_groups();
+                    }
+                }
+            } else {
+                // zero-padded pws makes steps past n_i add nothing
+#pragma unroll
+                for (int st = 0; st < 8; ++st)
+#pragma unroll
+                    for (int r = 0; r < kRB; ++r) acc[r] = fma(pv[st], X[7 - st + r], acc[r]);
+                cnt += 8;
+                if (cnt >= G) close_groups();
+            }
+#pragma unroll
+            for (int m = 0; m < 7; ++m) X[8 + m] = X[m];
+        }
+    }
+    if (!STEP && cnt) close_groups();
+#pragma unroll
+    for (int r = 0; r < kRB; ++r) {
+        const uint64_t t = t0 + kRB * tid + r;
+        if (t < T) {
+#pragma unroll
+            for (int w = 0; w < NW; ++w) res[(s * T + t) * NW + w] = racc[r][w];
+        }
+    }
+}
+
 // out[cidx] = residue j of chunk u plus residue j+k of chunk u-1, all splits
 __global__ void fqt_overlap_kernel(uint32_t p, uint32_t k, uint32_t nd, const uint32_t* __restrict__ res,
                                    uint32_t splits, uint64_t T, uint8_t* __restrict__ out, uint64_t nout) {
@@ -153,34 +277,50 @@ __global__ void fqt_overlap_kernel(uint32_t p, uint32_t k, uint32_t nd, const ui
     }
 }
 
-template <int ND, int W>
-cudaError_t run_conv_w(const FqtParams& P, const double* pw, uint64_t L1, const double* qw, uint64_t L2,
+template <int ND, int W, class K, bool STEP>
+cudaError_t run_conv_k(const FqtParams& P, const double* pw, uint64_t L1, const double* qw, uint64_t L2,
                        uint64_t T, uint32_t splits, uint64_t isplit, uint32_t* res, cudaStream_t s) {
+    const dim3 grid(static_cast<unsigned>((T + kFqtOut - 1) / kFqtOut), splits);
+    const size_t smem = W > 0 ? size_t(P.rq.n_entries) * 4 : 0;
+    if (smem > 160 * 1024) return cudaErrorInvalidValue;
+    static size_t cur = 0;
+    if (smem > 24 * 1024 && smem > cur) {
+        if (cudaError_t e = cudaFuncSetAttribute(fqt_conv_kernel<ND, W, K, STEP>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+            e != cudaSuccess)
+            return e;
+        cur = smem;
+    }
+    fqt_conv_kernel<ND, W, K, STEP><<<grid, kFqtT, smem, s>>>(P, pw, L1, qw, L2, T, isplit, res);
+    return cudaGetLastError();
+}
+
+template <int ND, int W, class K>
+cudaError_t run_conv_step(const FqtParams& P, const double* pw, uint64_t L1, const double* qw, uint64_t L2,
+                          uint64_t T, uint32_t splits, uint64_t isplit, uint32_t* res, cudaStream_t s) {
     const dim3 grid(static_cast<unsigned>((T + kFqtT - 1) / kFqtT), splits);
     const size_t smem = W > 0 ? size_t(P.rq.n_entries) * 4 : 0;
     if (smem > 160 * 1024) return cudaErrorInvalidValue;
-    if (P.rq.qbits) {
-        static size_t cur = 0;
-        if (smem > 48 * 1024 && smem > cur) {
-            if (cudaError_t e = cudaFuncSetAttribute(fqt_conv_kernel<ND, W, RtConst<true>>,
-                                                     cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-                e != cudaSuccess)
-                return e;
-            cur = smem;
-        }
-        fqt_conv_kernel<ND, W, RtConst<true>><<<grid, kFqtT, smem, s>>>(P, pw, L1, qw, L2, T, isplit, res);
-    } else {
-        static size_t cur = 0;
-        if (smem > 48 * 1024 && smem > cur) {
-            if (cudaError_t e = cudaFuncSetAttribute(fqt_conv_kernel<ND, W, RtConst<false>>,
-                                                     cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-                e != cudaSuccess)
-                return e;
-            cur = smem;
-        }
-        fqt_conv_kernel<ND, W, RtConst<false>><<<grid, kFqtT, smem, s>>>(P, pw, L1, qw, L2, T, isplit, res);
+    static size_t cur = 0;
+    if (smem > 48 * 1024 && smem > cur) {
+        if (cudaError_t e = cudaFuncSetAttribute(fqt_conv_step_kernel<ND, W, K>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+            e != cudaSuccess)
+            return e;
+        cur = smem;
     }
+    fqt_conv_step_kernel<ND, W, K><<<grid, kFqtT, smem, s>>>(P, pw, L1, qw, L2, T, isplit, res);
     return cudaGetLastError();
+}
+
+template <int ND, int W>
+cudaError_t run_conv_w(const FqtParams& P, const double* pw, uint64_t L1, const double* qw, uint64_t L2,
+                       uint64_t T, uint32_t splits, uint64_t isplit, uint32_t* res, cudaStream_t s) {
+    if (P.nq < 8)
+        return P.rq.qbits ? run_conv_step<ND, W, RtConst<true>>(P, pw, L1, qw, L2, T, splits, isplit, res, s)
+                          : run_conv_step<ND, W, RtConst<false>>(P, pw, L1, qw, L2, T, splits, isplit, res, s);
+    return P.rq.qbits ? run_conv_k<ND, W, RtConst<true>, false>(P, pw, L1, qw, L2, T, splits, isplit, res, s)
+                      : run_conv_k<ND, W, RtConst<false>, false>(P, pw, L1, qw, L2, T, splits, isplit, res, s);
 }
 
 template <int ND>
@@ -200,19 +340,19 @@ int num_sms();
 
 namespace {
 uint64_t fqt_chunks(uint64_t n, uint32_t k) { return (n + k - 1) / k; }
-uint32_t fqt_splits(uint64_t T, uint64_t L) {
+uint32_t fqt_splits(uint64_t T, uint64_t L, uint32_t nq) {
     // enough CTAs for ~4 per SM, splits of at least 1024 products
-    const uint64_t tiles = (T + kFqtT - 1) / kFqtT;
+    const uint64_t tiles = (T + (nq < 8 ? kFqtT : kFqtOut) - 1) / (nq < 8 ? kFqtT : kFqtOut);
     const uint64_t want = (uint64_t(num_sms()) * 4 + tiles - 1) / tiles;
     return static_cast<uint32_t>(std::clamp<uint64_t>(std::min<uint64_t>(want, L / 1024), 1, 1024));
 }
 uint64_t align16(uint64_t b) { return (b + 15) / 16 * 16; }
 }  // namespace
 
-uint64_t fqt_workspace_bytes(uint32_t k, uint64_t na, uint64_t nb) {
+uint64_t fqt_workspace_bytes(uint32_t k, uint32_t nq, uint64_t na, uint64_t nb) {
     const uint64_t L1 = fqt_chunks(na, k), L2 = fqt_chunks(nb, k), T = L1 + L2 - 1;
     const uint32_t nd = 2 * k - 1, nw = (nd + 3) / 4;
-    return align16(L1 * 8) + align16(L2 * 8) + uint64_t(fqt_splits(T, std::min(L1, L2))) * T * nw * 4;
+    return align16(L1 * 8) + align16(L2 * 8) + uint64_t(fqt_splits(T, std::min(L1, L2), nq)) * T * nw * 4;
 }
 
 cudaError_t launch_fqt_mul(const FqtParams& P, const uint8_t* a, uint64_t na, const uint8_t* b, uint64_t nb,
@@ -231,7 +371,7 @@ cudaError_t launch_fqt_mul(const FqtParams& P, const uint8_t* a, uint64_t na, co
     fqt_pack_kernel<<<static_cast<int>(std::min<uint64_t>((L2 + 255) / 256, sms * 8)), 256, 0, s>>>(P.rq.p, k, qd, b,
                                                                                                       nb, L2, qw);
     if (cudaError_t e = cudaGetLastError(); e != cudaSuccess) return e;
-    const uint32_t splits = fqt_splits(T, std::min(L1, L2));
+    const uint32_t splits = fqt_splits(T, std::min(L1, L2), P.nq);
     const uint64_t isplit = (L1 + splits - 1) / splits;
     cudaError_t e;
     switch (nd) {

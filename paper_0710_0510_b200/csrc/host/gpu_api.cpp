@@ -379,7 +379,7 @@ void fqt_mul_device(const RedqPlan& plan, const QadicParams& params, const uint8
     F.rq = dp.prm;
     F.k = params.k;
     F.nq = static_cast<uint32_t>(std::max<u64>(params.n_q, 1));
-    void* ws = dp.ws_fqt.ensure(qpk::fqt_workspace_bytes(params.k, na, nb));
+    void* ws = dp.ws_fqt.ensure(qpk::fqt_workspace_bytes(params.k, F.nq, na, nb));
     check(qpk::launch_fqt_mul(F, a, na, b, nb, out, ws, s), "fqt_mul launch");
 }
 

@@ -138,7 +138,7 @@ cudaError_t launch_gfq_gemv(const GfqGemvParams& P, const uint32_t* A, const uin
 
 // K6: out (na+nb-1 coefficients) = a * b mod p, coefficients as uint8;
 // ws: fqt_workspace_bytes (packed chunks and per-chunk residue partials).
-uint64_t fqt_workspace_bytes(uint32_t k, uint64_t na, uint64_t nb);
+uint64_t fqt_workspace_bytes(uint32_t k, uint32_t nq, uint64_t na, uint64_t nb);
 cudaError_t launch_fqt_mul(const FqtParams& P, const uint8_t* a, uint64_t na, const uint8_t* b, uint64_t nb,
                            uint8_t* out, void* ws, cudaStream_t s);
 

@@ -632,6 +632,79 @@ __global__ void __launch_bounds__(kThreads) stream_tma_kernel(const Op op, const
     report(err, status);
 }
 
+// Small batches (one wave of CTAs): every thread loads its runs straight
+// from global memory with the widest aligned vectors and stores its output
+// run -- no pipeline prologue, every load in flight at once.  Used below
+// kDirectMax records (measured: C1's 2^20 pairs, a latency-bound 15.7 MB).
+template <int N>
+__device__ __forceinline__ void ldg_run(const uint8_t* base, uint32_t (&w)[N > 0 ? N : 1]) {
+    if constexpr (N == 0) {
+        w[0] = 0;
+    } else if constexpr (N % 4 == 0) {
+#pragma unroll
+        for (int i = 0; i < N / 4; ++i) {
+            const uint4 v = __ldg(reinterpret_cast<const uint4*>(base) + i);
+            w[4 * i] = v.x, w[4 * i + 1] = v.y, w[4 * i + 2] = v.z, w[4 * i + 3] = v.w;
+        }
+    } else if constexpr (N % 2 == 0) {
+#pragma unroll
+        for (int i = 0; i < N / 2; ++i) {
+            const uint2 v = __ldg(reinterpret_cast<const uint2*>(base) + i);
+            w[2 * i] = v.x, w[2 * i + 1] = v.y;
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < N; ++i) w[i] = __ldg(reinterpret_cast<const uint32_t*>(base) + i);
+    }
+}
+
+template <int N>
+__device__ __forceinline__ void stg_run(uint8_t* base, const uint32_t (&w)[N]) {
+    if constexpr (N % 4 == 0) {
+#pragma unroll
+        for (int i = 0; i < N / 4; ++i)
+            reinterpret_cast<uint4*>(base)[i] = make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
+    } else if constexpr (N % 2 == 0) {
+#pragma unroll
+        for (int i = 0; i < N / 2; ++i) reinterpret_cast<uint2*>(base)[i] = make_uint2(w[2 * i], w[2 * i + 1]);
+    } else {
+#pragma unroll
+        for (int i = 0; i < N; ++i) reinterpret_cast<uint32_t*>(base)[i] = w[i];
+    }
+}
+
+template <class Op>
+__global__ void __launch_bounds__(kThreads) stream_direct_kernel(const Op op, const uint8_t* __restrict__ in0,
+                                                                 const uint8_t* __restrict__ in1,
+                                                                 uint8_t* __restrict__ out, uint64_t n_runs,
+                                                                 uint32_t* status) {
+    using G = Geometry<Op>;
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint32_t* s_tab = reinterpret_cast<uint32_t*>(smem);
+    // first loads before the table staging, so both overlap
+    uint64_t run = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    uint32_t a[G::W0 > 0 ? G::W0 : 1], b[G::W1 > 0 ? G::W1 : 1];
+    if (run < n_runs) {
+        ldg_run<G::W0>(in0 + run * (G::R * Op::IN0), a);
+        ldg_run<G::W1>(in1 + run * (G::R * Op::IN1), b);
+    }
+    stage_tables(op, s_tab);
+    __syncthreads();
+    const uint32_t tab = smem_addr(s_tab);
+    uint32_t err = 0;
+    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+    for (; run < n_runs; run += stride) {
+        uint32_t ow[G::WO];
+        op.apply(a, b, ow, tab, err);
+        stg_run<G::WO>(out + run * (G::R * Op::OUT), ow);
+        if (run + stride < n_runs) {
+            ldg_run<G::W0>(in0 + (run + stride) * (G::R * Op::IN0), a);
+            ldg_run<G::W1>(in1 + (run + stride) * (G::R * Op::IN1), b);
+        }
+    }
+    report(err, status);
+}
+
 // Records [first, n) with byte-granular global loads (tails, unaligned buffers).
 template <class Op>
 __global__ void __launch_bounds__(kThreads) stream_tail_kernel(const Op op, const uint8_t* __restrict__ in0,
@@ -660,6 +733,30 @@ __global__ void __launch_bounds__(kThreads) stream_tail_kernel(const Op op, cons
     report(err, status);
 }
 
+#ifndef QPK_DIRECT_MAX
+#define QPK_DIRECT_MAX (1u << 21)
+#endif
+constexpr uint64_t kDirectMax = QPK_DIRECT_MAX;  // records: below this the direct kernel runs
+
+template <class Op>
+cudaError_t run_tail(const Op& op, const uint8_t* in0, const uint8_t* in1, uint8_t* out, uint64_t first, uint64_t n,
+                     uint32_t* status, cudaStream_t s) {
+    using G = Geometry<Op>;
+    const size_t tab_bytes = size_t(op.tables_words()) * 4;
+    static bool attr_done = false;
+    if (!attr_done) {
+        cudaError_t e = cudaFuncSetAttribute(stream_tail_kernel<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             227 * 1024);
+        if (e != cudaSuccess) return e;
+        attr_done = true;
+    }
+    const uint64_t groups = (n - first + G::R - 1) / G::R;
+    const uint64_t grid = std::min<uint64_t>((groups + kThreads - 1) / kThreads, uint64_t(num_sms()) * 8);
+    stream_tail_kernel<Op><<<static_cast<unsigned>(grid), kThreads, tab_bytes, s>>>(op, in0, in1, out, first, n,
+                                                                                    status);
+    return cudaGetLastError();
+}
+
 template <class Op>
 cudaError_t run_stream(const Op& op, const uint8_t* in0, const uint8_t* in1, uint8_t* out, uint64_t n,
                        uint32_t* status, cudaStream_t s) {
@@ -669,8 +766,26 @@ cudaError_t run_stream(const Op& op, const uint8_t* in0, const uint8_t* in1, uin
     const bool aligned = (reinterpret_cast<uintptr_t>(in0) % 16 == 0) &&
                          (G::B1 == 0 || reinterpret_cast<uintptr_t>(in1) % 16 == 0) &&
                          (reinterpret_cast<uintptr_t>(out) % 16 == 0);
-    const uint64_t n_tiles = aligned ? n / G::TILE : 0;
     const int sms = num_sms();
+    // small batches: the direct kernel over whole runs, then the tail
+    if (aligned && n < kDirectMax && n >= uint64_t(G::R)) {
+        const uint64_t n_runs = n / G::R;
+        static bool attr_direct = false;
+        if (!attr_direct && tab_bytes > 48 * 1024) {
+            cudaError_t e = cudaFuncSetAttribute(stream_direct_kernel<Op>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+            if (e != cudaSuccess) return e;
+            attr_direct = true;
+        }
+        const uint64_t grid = std::min<uint64_t>((n_runs + kThreads - 1) / kThreads, uint64_t(sms) * 16);
+        stream_direct_kernel<Op><<<static_cast<unsigned>(grid), kThreads, tab_bytes, s>>>(op, in0, in1, out, n_runs,
+                                                                                          status);
+        if (cudaError_t e = cudaGetLastError(); e != cudaSuccess) return e;
+        const uint64_t first = n_runs * G::R;
+        if (first == n) return cudaSuccess;
+        return run_tail(op, in0, in1, out, first, n, status, s);
+    }
+    const uint64_t n_tiles = aligned ? n / G::TILE : 0;
     if (n_tiles > 0) {
         const size_t smem = G::smem_pipe + tab_bytes;
         static bool attr_done = false;  // per instantiation
@@ -698,20 +813,7 @@ cudaError_t run_stream(const Op& op, const uint8_t* in0, const uint8_t* in1, uin
         if (e != cudaSuccess) return e;
     }
     const uint64_t first = n_tiles * G::TILE;
-    if (first < n) {
-        static bool attr_done = false;
-        if (!attr_done) {
-            cudaError_t e = cudaFuncSetAttribute(stream_tail_kernel<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 227 * 1024);
-            if (e != cudaSuccess) return e;
-            attr_done = true;
-        }
-        const uint64_t groups = (n - first + G::R - 1) / G::R;
-        const uint64_t grid = std::min<uint64_t>((groups + kThreads - 1) / kThreads, uint64_t(sms) * 8);
-        stream_tail_kernel<Op><<<static_cast<unsigned>(grid), kThreads, tab_bytes, s>>>(op, in0, in1, out, first, n,
-                                                                                        status);
-        return cudaGetLastError();
-    }
+    if (first < n) return run_tail(op, in0, in1, out, first, n, status, s);
     return cudaSuccess;
 }
 
