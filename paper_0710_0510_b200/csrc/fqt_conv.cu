@@ -66,10 +66,48 @@ __global__ void fqt_pack_kernel(uint32_t p, uint32_t k, double qd, const uint8_t
     }
 }
 
+// REDQ for p = 3, q = 2^B (4 <= B <= 7) inside one 64-bit integer, lane i =
+// bits [Bi, Bi+B) (the C5 re-pack trick, gfq_matmul.cuh, generalised to both
+// signs of q mod 3):
+//  * u_i = floor(r/q^i) mod 3 is fixed by its value mod 4, and
+//    (r >> Bi) - 3 (rop >> Bi) == a_i + b_i (mod 4), a_i and b_i the two low
+//    bits of lane i of r and rop (-3 == 1 mod 4);
+//  * mu_i = (u_i + neg_q u_{i+1}) mod 3 lane-wise: neg_q = 2 (B even) as
+//    V = u_i + 8 - u_{i+1}, neg_q = 1 (B odd) as V = u_i + u_{i+1} + 5, both in
+//    [5, 10], then mu = V - 5 - 3 [V >= 8]; no lane ever borrows.
+// Residues of many groups add up in the same lanes (<= 2 each) and are folded
+// back below 3 (4 == 1 mod 3) before a lane can overflow.
+template <int B, int ND>
+struct Swar3 {
+    static constexpr uint64_t M1 = [] {
+        uint64_t m = 0;
+        for (int i = 0; i < ND && B * i < 64; ++i) m |= uint64_t(1) << (B * i);
+        return m;
+    }();
+    static constexpr uint64_t M3 = 3 * M1, Mlow = ((uint64_t(1) << (B - 2)) - 1) * M1;
+    static constexpr uint32_t adds = ((1u << B) - 3) / 2;  // lanes stay below 2^B
+    static constexpr bool negq1 = (B & 1) != 0;           // 2^B mod 3 = 2 for odd B: neg_q = 1
+    __device__ __forceinline__ static uint64_t mu(double r, double inv_p) {
+        const uint64_t rb = dbits(r + kTwo52);  // low 52 bits = r
+        const uint64_t ob = dbits(__dadd_rz(__dmul_ru(r, inv_p), kTwo52));  // low 52 bits = floor(r/3)
+        const uint64_t u = ((rb & M3) + (ob & M3)) & M3;
+        const uint64_t v = negq1 ? u + (u >> B) + 5 * M1 : u + 8 * M1 - (u >> B);
+        return v - 5 * M1 - 3 * ((v >> 3) & M1);
+    }
+    __device__ __forceinline__ static uint64_t fold(uint64_t x) {
+        x = ((x >> 2) & Mlow) + (x & M3);
+        if constexpr (B > 5) x = ((x >> 2) & Mlow) + (x & M3);
+        x = ((x >> 2) & M3) + (x & M3);  // lanes <= 5
+        return x - 3 * (((x + 5 * M1) >> 3) & M1);
+    }
+};
+
 // n_q < 8 (e.g. C1's q = 2^5, d = 3, n_q = 1): one output chunk per thread,
 // a REDQ after every group of at most n_q products; the register-blocked
-// kernel would run 8 REDQs per step at a quarter of the occupancy.
-template <int ND, int W, class K>
+// kernel would run 8 REDQs per step at a quarter of the occupancy.  SWAR3:
+// p = 3 and q = 2^4..2^7 through Swar3 (about 20 instructions per REDQ
+// instead of ~100 for the per-digit path).
+template <int ND, int W, class K, int SWAR_B>
 __global__ void __launch_bounds__(kFqtT) fqt_conv_step_kernel(const FqtParams P, const double* __restrict__ pw,
                                                          uint64_t L1, const double* __restrict__ qw, uint64_t L2,
                                                          uint64_t T, uint64_t isplit, uint32_t* __restrict__ res) {
@@ -93,7 +131,21 @@ __global__ void __launch_bounds__(kFqtT) fqt_conv_step_kernel(const FqtParams P,
     uint32_t racc[NW];
 #pragma unroll
     for (int w = 0; w < NW; ++w) racc[w] = 0;
+    constexpr bool SWAR3 = SWAR_B > 0;
+    using SW = Swar3<SWAR3 ? SWAR_B : 4, ND>;
+    uint64_t lacc = 0;
+    uint32_t ladds = 0;
     auto close_group = [&]() {
+        if constexpr (SWAR3) {
+            lacc += SW::mu(acc, P.rq.inv_p);
+            if (++ladds == SW::adds) {
+                lacc = SW::fold(lacc);
+                ladds = 0;
+            }
+            acc = 0.0;
+            cnt = 0;
+            return;
+        }
         uint32_t u[ND], mu[ND];
         redq_raw_digits<ND>(c, acc, u);
         redq_correct<ND, W>(c, u, mu, [&](uint32_t idx) { return lds_u32(tab_s + 4 * idx); });
@@ -122,6 +174,14 @@ __global__ void __launch_bounds__(kFqtT) fqt_conv_step_kernel(const FqtParams P,
         // the same terms (out-of-range products are zeros), so group closes
         // are CTA-uniform
         int ii = 0;
+        if (P.nq == 1) {
+            const double* pq = qws + tid + kFqtI - 1;
+#pragma unroll 4
+            for (; ii < n_i; ++ii) {
+                acc = pws[ii] * pq[-ii];
+                close_group();
+            }
+        }
         while (ii < n_i) {
             const int run = min(n_i - ii, static_cast<int>(P.nq - cnt));
             const double* pq = qws + tid + kFqtI - 1 - ii;
@@ -133,6 +193,12 @@ __global__ void __launch_bounds__(kFqtT) fqt_conv_step_kernel(const FqtParams P,
         }
     }
     if (cnt) close_group();
+    if constexpr (SWAR3) {
+        lacc = SW::fold(lacc);
+#pragma unroll
+        for (int j = 0; j < ND; ++j)
+            racc[j / 4] |= static_cast<uint32_t>((lacc >> (SWAR_B * j)) & 3u) << (8 * (j % 4));
+    }
     if (t < T) {
 #pragma unroll
         for (int w = 0; w < NW; ++w) res[(s * T + t) * NW + w] = racc[w];
@@ -295,7 +361,7 @@ cudaError_t run_conv_k(const FqtParams& P, const double* pw, uint64_t L1, const 
     return cudaGetLastError();
 }
 
-template <int ND, int W, class K>
+template <int ND, int W, class K, int SWAR_B = 0>
 cudaError_t run_conv_step(const FqtParams& P, const double* pw, uint64_t L1, const double* qw, uint64_t L2,
                           uint64_t T, uint32_t splits, uint64_t isplit, uint32_t* res, cudaStream_t s) {
     const dim3 grid(static_cast<unsigned>((T + kFqtT - 1) / kFqtT), splits);
@@ -303,19 +369,30 @@ cudaError_t run_conv_step(const FqtParams& P, const double* pw, uint64_t L1, con
     if (smem > 160 * 1024) return cudaErrorInvalidValue;
     static size_t cur = 0;
     if (smem > 48 * 1024 && smem > cur) {
-        if (cudaError_t e = cudaFuncSetAttribute(fqt_conv_step_kernel<ND, W, K>,
+        if (cudaError_t e = cudaFuncSetAttribute(fqt_conv_step_kernel<ND, W, K, SWAR_B>,
                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
             e != cudaSuccess)
             return e;
         cur = smem;
     }
-    fqt_conv_step_kernel<ND, W, K><<<grid, kFqtT, smem, s>>>(P, pw, L1, qw, L2, T, isplit, res);
+    fqt_conv_step_kernel<ND, W, K, SWAR_B><<<grid, kFqtT, smem, s>>>(P, pw, L1, qw, L2, T, isplit, res);
     return cudaGetLastError();
 }
 
 template <int ND, int W>
 cudaError_t run_conv_w(const FqtParams& P, const double* pw, uint64_t L1, const double* qw, uint64_t L2,
                        uint64_t T, uint32_t splits, uint64_t isplit, uint32_t* res, cudaStream_t s) {
+    // the SWAR path needs every group word below 2^52 and within r_max
+    const bool swar3 = P.rq.p == 3 && P.rq.qbits >= 4 && P.rq.qbits <= 7 && P.rq.qbits * ND <= 52 &&
+                       P.rq.limit <= P.rq.r_max + 1.0;
+    if (P.nq < 8 && swar3) {
+        switch (P.rq.qbits) {
+            case 4: return run_conv_step<ND, 0, RtConst<true>, 4>(P, pw, L1, qw, L2, T, splits, isplit, res, s);
+            case 5: return run_conv_step<ND, 0, RtConst<true>, 5>(P, pw, L1, qw, L2, T, splits, isplit, res, s);
+            case 6: return run_conv_step<ND, 0, RtConst<true>, 6>(P, pw, L1, qw, L2, T, splits, isplit, res, s);
+            default: return run_conv_step<ND, 0, RtConst<true>, 7>(P, pw, L1, qw, L2, T, splits, isplit, res, s);
+        }
+    }
     if (P.nq < 8)
         return P.rq.qbits ? run_conv_step<ND, W, RtConst<true>>(P, pw, L1, qw, L2, T, splits, isplit, res, s)
                           : run_conv_step<ND, W, RtConst<false>>(P, pw, L1, qw, L2, T, splits, isplit, res, s);
