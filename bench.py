@@ -303,6 +303,69 @@ def run_ours(args, rank, world, local_rank):
     return line
 
 
+def secondary_cpu_refs(sec):
+    """The reference's CPU path timed beside each secondary config (SURVEY
+    8(d)): oracle/_ref (the unmodified sources, -O2, asserts armed) on all host
+    threads, a bounded sample of the same seeded workload, ~1-3 s each."""
+    import numpy as np
+
+    import oracle as O
+    if O.ref() is None:
+        return
+    th = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+
+    def entry(value, unit, sample):
+        return {"value": value, "unit": unit, "cores": th, "kind": "reference", "sample": sample}
+
+    # C1: fqt_mul per pair (REDQ/FQT path), first 2^20 pairs' worth of draws
+    n = 1 << 18
+    d = O.draws(0x07100510 + 1, 8 * n, 3).reshape(n, 8)
+    _, ns, _ = O.ref_polymul_batch(3, 3, d[:, :4], d[:, 4:], algo=0, threads=th)
+    if "c1_polymul" in sec:
+        sec["c1_polymul"]["cpu_ref"] = entry(n / (ns * 1e-9), "pairs/s",
+                                             f"{n} pairs of the C1 stream, fqt_mul(a,b,3,qadic_for_degree(3,3,53))")
+    # C3: fgdp_dot on length-1 vectors (packed) and GfqField::mul (dlog)
+    n = 1 << 20
+    d = O.draws(0x07100510 + 3, 6 * n, 7).reshape(n, 6)
+    rf = O.RefField(7, 3, 256)
+    for algo, name, what in ((0, "c3_gfq_mul_packed", "fgdp_dot on length-1 vectors"),
+                             (1, "c3_gfq_mul_dlog", "GfqField::mul")):
+        _, ns, _ = rf.mul_batch(d[:, :3], d[:, 3:], algo=algo, threads=th)
+        if name in sec:
+            sec[name]["cpu_ref"] = entry(n / (ns * 1e-9), "products/s", f"{n} products of the C3 stream, {what}")
+    # C4 / C5: gfq_matmul (as shipped) on a row slab, GF ops/s = 2 terms/s
+    for cid, k, q, nn in ((4, 2, 1 << 16, 4096), (5, 3, 1 << 10, 8192)):
+        rows = max(16, th)  # one row slab per host thread at least
+        A = O.draws(0x07100510 + cid, rows * nn * k, 3).reshape(rows, nn, k)
+        B = O.draws(0x07100510 + cid, nn * nn * k, 3, start=nn * nn * k).reshape(nn, nn, k)
+        _, ns, _ = O.RefField(3, k, q).matmul(A, B, 0, rows, algo=0, threads=th)
+        name = f"c{cid}_gfq_matmul"
+        if name in sec:
+            sec[name]["cpu_ref"] = entry(2 * rows * nn * nn / (ns * 1e-9), "GF ops/s",
+                                         f"{rows} rows x {nn} x {nn} of C{cid} (gfq_matmul, as shipped), extrapolated rate")
+    # K5: fgdp_dot of two long rep vectors
+    n = 1 << 24
+    v = O.draws(0x5, 2 * n, 27).astype(np.uint32)
+    t0 = time.perf_counter()
+    O.RefField(3, 3, 1 << 10).dot(v[:n], v[n:])
+    dt = time.perf_counter() - t0
+    if "k5_fgdp_dot_long" in sec:
+        sec["k5_fgdp_dot_long"]["cpu_ref"] = {"value": n / dt, "unit": "GF terms/s", "cores": 1, "kind": "reference",
+                                              "sample": f"one fgdp_dot of {n} terms (single call, single thread)"}
+    # K6: fqt_mul of two 2^11-coefficient polynomials, C1's params
+    n = 1 << 11
+    a = O.draws(0x6, 2 * n, 3).astype(np.uint64)
+    out = np.zeros(2 * n - 1, np.uint64)
+    cost = np.zeros(4, np.uint64)
+    t0 = time.perf_counter()
+    O.ref().ref_fqt_mul(3, 3, 32, 1, a[:n], n, a[n:], n, out, cost)
+    dt = time.perf_counter() - t0
+    if "k6_fqt_mul" in sec:
+        sec["k6_fqt_mul"]["cpu_ref_q32_d3_nq1"] = {
+            "value": n * n / dt, "unit": "coefficient products/s", "cores": 1, "kind": "reference",
+            "sample": f"one fqt_mul of two {n}-coefficient polynomials over F_3 (single call, single thread)"}
+
+
 def measure_secondary(Q, torch, dev):
     """C1, C3 (both paths), C4, C5 on one GPU; CUDA-event timed."""
     res = {}
@@ -489,6 +552,8 @@ def main():
     if rank == 0:
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline_leg()
+            if "secondary" in line:
+                secondary_cpu_refs(line["secondary"])
         print(json.dumps(line))
     if world > 1:
         import torch.distributed as dist
