@@ -66,42 +66,6 @@ __global__ void fqt_pack_kernel(uint32_t p, uint32_t k, double qd, const uint8_t
     }
 }
 
-// REDQ for p = 3, q = 2^B (4 <= B <= 7) inside one 64-bit integer, lane i =
-// bits [Bi, Bi+B) (the C5 re-pack trick, gfq_matmul.cuh, generalised to both
-// signs of q mod 3):
-//  * u_i = floor(r/q^i) mod 3 is fixed by its value mod 4, and
-//    (r >> Bi) - 3 (rop >> Bi) == a_i + b_i (mod 4), a_i and b_i the two low
-//    bits of lane i of r and rop (-3 == 1 mod 4);
-//  * mu_i = (u_i + neg_q u_{i+1}) mod 3 lane-wise: neg_q = 2 (B even) as
-//    V = u_i + 8 - u_{i+1}, neg_q = 1 (B odd) as V = u_i + u_{i+1} + 5, both in
-//    [5, 10], then mu = V - 5 - 3 [V >= 8]; no lane ever borrows.
-// Residues of many groups add up in the same lanes (<= 2 each) and are folded
-// back below 3 (4 == 1 mod 3) before a lane can overflow.
-template <int B, int ND>
-struct Swar3 {
-    static constexpr uint64_t M1 = [] {
-        uint64_t m = 0;
-        for (int i = 0; i < ND && B * i < 64; ++i) m |= uint64_t(1) << (B * i);
-        return m;
-    }();
-    static constexpr uint64_t M3 = 3 * M1, Mlow = ((uint64_t(1) << (B - 2)) - 1) * M1;
-    static constexpr uint32_t adds = ((1u << B) - 3) / 2;  // lanes stay below 2^B
-    static constexpr bool negq1 = (B & 1) != 0;           // 2^B mod 3 = 2 for odd B: neg_q = 1
-    __device__ __forceinline__ static uint64_t mu(double r, double inv_p) {
-        const uint64_t rb = dbits(r + kTwo52);  // low 52 bits = r
-        const uint64_t ob = dbits(__dadd_rz(__dmul_ru(r, inv_p), kTwo52));  // low 52 bits = floor(r/3)
-        const uint64_t u = ((rb & M3) + (ob & M3)) & M3;
-        const uint64_t v = negq1 ? u + (u >> B) + 5 * M1 : u + 8 * M1 - (u >> B);
-        return v - 5 * M1 - 3 * ((v >> 3) & M1);
-    }
-    __device__ __forceinline__ static uint64_t fold(uint64_t x) {
-        x = ((x >> 2) & Mlow) + (x & M3);
-        if constexpr (B > 5) x = ((x >> 2) & Mlow) + (x & M3);
-        x = ((x >> 2) & M3) + (x & M3);  // lanes <= 5
-        return x - 3 * (((x + 5 * M1) >> 3) & M1);
-    }
-};
-
 // n_q < 8 (e.g. C1's q = 2^5, d = 3, n_q = 1): one output chunk per thread,
 // a REDQ after every group of at most n_q products; the register-blocked
 // kernel would run 8 REDQs per step at a quarter of the occupancy.  SWAR3:

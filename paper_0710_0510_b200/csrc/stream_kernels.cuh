@@ -164,6 +164,29 @@ __device__ __forceinline__ double pack_word(const C& c, double qd, const uint32_
     }
 }
 
+// every byte of N packed words is below p (p < 128): b + 128 - p sets a
+// byte's top bit iff p <= b < 128; bytes >= 128 carry it already.  Only
+// such bytes can carry into a neighbour, so carries never hide a bad byte
+// (at worst they flag a good one and the exact path runs).
+template <int N>
+__device__ __forceinline__ bool all_bytes_below(const uint32_t* w, uint32_t p) {
+    const uint32_t add = (128u - p) * 0x01010101u;
+    uint32_t bad = 0;
+#pragma unroll
+    for (int i = 0; i < N; ++i) bad |= w[i] | (w[i] + add);
+    return (bad & 0x80808080u) == 0;
+}
+
+// record r (k bytes, little endian) of a packed run as an integer
+template <int K_>
+__device__ __forceinline__ uint32_t record_int(const uint32_t* w, int r) {
+    const int byte = r * K_, i = byte >> 2, sh = 8 * (byte & 3);
+    const uint32_t lo = w[i];
+    const uint32_t hi = (sh + 8 * K_ > 32) ? w[i + 1] : 0u;
+    const uint32_t v = sh ? __funnelshift_r(lo, hi, sh) : lo;
+    return K_ == 4 ? v : (v & ((1u << (8 * K_)) - 1));
+}
+
 #ifndef QPK_PM_R  // tile geometry of the batched polynomial product
 #define QPK_PM_R 4
 #endif
@@ -180,11 +203,45 @@ struct PolymulOp {
     PolymulParams P;
     __host__ __device__ uint32_t tables_words() const { return W ? P.rq.n_entries : 0u; }
     __host__ __device__ const uint32_t* tables_src() const { return P.rq.table; }
+    // p = 3, q = 2^B (C1: B = 5, k = 4): coefficient bytes < 3 spread into
+    // B-bit lanes are the packed word; the exact integer product's lanes are
+    // the convolution digits, and Swar3 reduces all 2k-1 of them at once
+    static constexpr bool kSwar3 = [] {
+        if constexpr (K::kSafe) return K::kP == 3 && K::kQbits >= 4 && K::kQbits <= 7 &&
+                                       K::kQbits * (ND - 1) + 2 <= 32;
+        else return false;
+    }();
+
     __device__ __forceinline__ void apply(const uint32_t* a, const uint32_t* b, uint32_t (&ow)[R * OUT / 4],
                                           uint32_t tab, uint32_t&) const {
         const K c{P.rq};
         const double qd = static_cast<double>(P.rq.q);
         uint64_t rec[R];
+        if constexpr (kSwar3) {
+            constexpr int B = K::kQbits;
+            if (all_bytes_below<R * K_ / 4>(a, 3) && all_bytes_below<R * K_ / 4>(b, 3)) {
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const uint32_t xa = record_int<K_>(a, r), xb = record_int<K_>(b, r);
+                    uint32_t wa = 0, wb = 0;  // byte i (2 bits) -> bits [B i, B i + 2)
+#pragma unroll
+                    for (int i = 0; i < K_; ++i) {
+                        wa |= (xa >> (8 * i - B * i)) & (3u << (B * i));
+                        wb |= (xb >> (8 * i - B * i)) & (3u << (B * i));
+                    }
+                    const uint64_t w = static_cast<uint64_t>(wa) * wb;  // < 2^(B(2k-1)) <= 2^52
+                    const double wd =
+                        __hiloint2double(0x43300000 | static_cast<int>(w >> 32), static_cast<int>(w)) - kTwo52;
+                    const uint32_t mu = static_cast<uint32_t>(Swar3<B, ND>::mu(w, wd, P.rq.inv_p));
+                    uint64_t v = 0;  // lane j (value <= 2) -> byte j
+#pragma unroll
+                    for (int j = 0; j < ND; ++j) v |= static_cast<uint64_t>((mu >> (B * j)) & 3u) << (8 * j);
+                    rec[r] = v;
+                }
+                pack_records<R, OUT>(rec, ow);
+                return;
+            }
+        }
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             uint32_t ca[K_], cb[K_];
@@ -213,18 +270,6 @@ __device__ __forceinline__ uint32_t add_mod_bytes(uint32_t x, uint32_t y, uint32
     return r;
 }
 
-// every byte of N packed words is below p (p < 128): b + 128 - p sets a
-// byte's top bit iff p <= b < 128; bytes >= 128 carry it already.  Only
-// such bytes can carry into a neighbour, so carries never hide a bad byte
-// (at worst they flag a good one and the exact path runs).
-template <int N>
-__device__ __forceinline__ bool all_bytes_below(const uint32_t* w, uint32_t p) {
-    const uint32_t add = (128u - p) * 0x01010101u;
-    uint32_t bad = 0;
-#pragma unroll
-    for (int i = 0; i < N; ++i) bad |= w[i] | (w[i] + add);
-    return (bad & 0x80808080u) == 0;
-}
 
 __device__ __forceinline__ uint32_t add_mod_bytes_fast(uint32_t x, uint32_t y, uint32_t p);
 
@@ -308,15 +353,6 @@ constexpr bool ct_small_p() {
     else return false;
 }
 
-// record r (k bytes, little endian) of a packed run as an integer
-template <int K_>
-__device__ __forceinline__ uint32_t record_int(const uint32_t* w, int r) {
-    const int byte = r * K_, i = byte >> 2, sh = 8 * (byte & 3);
-    const uint32_t lo = w[i];
-    const uint32_t hi = (sh + 8 * K_ > 32) ? w[i + 1] : 0u;
-    const uint32_t v = sh ? __funnelshift_r(lo, hi, sh) : lo;
-    return K_ == 4 ? v : (v & ((1u << (8 * K_)) - 1));
-}
 
 // coefficient index sum c_i p^i of a record integer (bytes c_i)
 template <int K_, class C>
