@@ -88,8 +88,10 @@ __global__ void __launch_bounds__(kFqtT) fqt_conv_step_kernel(const FqtParams P,
     const uint64_t t0 = uint64_t(blockIdx.x) * kFqtT, t = t0 + tid;
     const uint64_t s = blockIdx.y;
     // i with some t - i in [0, L2) for this tile, within split s
-    const uint64_t lo = std::max<uint64_t>(t0 + 1 > L2 ? t0 + 1 - L2 : 0, s * isplit);
-    const uint64_t hi = std::min<uint64_t>(std::min<uint64_t>(L1, t0 + kFqtT), (s + 1) * isplit);
+    // chunk s (isplit products long) of this tile's own i range: every
+    // non-final chunk is the same work, empty chunks exit at once
+    const uint64_t tlo = t0 + 1 > L2 ? t0 + 1 - L2 : 0, thi = std::min<uint64_t>(L1, t0 + kFqtT);
+    const uint64_t lo = tlo + s * isplit, hi = std::min<uint64_t>(thi, lo + isplit);
     double acc = 0.0;
     uint32_t cnt = 0;
     uint32_t racc[NW];
@@ -202,8 +204,10 @@ __global__ void __launch_bounds__(kFqtT) fqt_conv_kernel(const FqtParams P, cons
     const uint64_t t0 = uint64_t(blockIdx.x) * kFqtOut;
     const uint64_t s = blockIdx.y;
     // i with some t - i in [0, L2) for this tile, within split s
-    const uint64_t lo = std::max<uint64_t>(t0 + 1 > L2 ? t0 + 1 - L2 : 0, s * isplit);
-    const uint64_t hi = std::min<uint64_t>(std::min<uint64_t>(L1, t0 + kFqtOut), (s + 1) * isplit);
+    // chunk s (isplit products long) of this tile's own i range (see the
+    // step kernel)
+    const uint64_t tlo = t0 + 1 > L2 ? t0 + 1 - L2 : 0, thi = std::min<uint64_t>(L1, t0 + kFqtOut);
+    const uint64_t lo = tlo + s * isplit, hi = std::min<uint64_t>(thi, lo + isplit);
     double acc[kRB];
     uint32_t racc[kRB][NW];
 #pragma unroll
@@ -381,11 +385,29 @@ int num_sms();
 
 namespace {
 uint64_t fqt_chunks(uint64_t n, uint32_t k) { return (n + k - 1) / k; }
-uint32_t fqt_splits(uint64_t T, uint64_t L, uint32_t nq) {
-    // enough CTAs for ~4 per SM, splits of at least 1024 products
-    const uint64_t tiles = (T + (nq < 8 ? kFqtT : kFqtOut) - 1) / (nq < 8 ? kFqtT : kFqtOut);
-    const uint64_t want = (uint64_t(num_sms()) * 4 + tiles - 1) / tiles;
-    return static_cast<uint32_t>(std::clamp<uint64_t>(std::min<uint64_t>(want, L / 1024), 1, 1024));
+// Work split: tile `x` (tw output chunks) has its own i range of len(x)
+// products; it is cut into chunks of C, so all CTAs but each tile's last
+// carry the same work (the convolution's triangle would leave fixed global
+// splits badly unbalanced).  C targets ~12 CTAs per SM; returns the chunk
+// count of the longest tile (grid.y) and C.
+struct FqtSplit {
+    uint32_t splits;
+    uint64_t chunk;
+};
+FqtSplit fqt_split(uint64_t L1, uint64_t L2, uint32_t nq) {
+    const uint64_t tw = nq < 8 ? kFqtT : kFqtOut, T = L1 + L2 - 1, tiles = (T + tw - 1) / tw;
+    uint64_t total = 0, longest = 0;
+    for (uint64_t x = 0; x < tiles; ++x) {
+        const uint64_t t0 = x * tw, lo = t0 + 1 > L2 ? t0 + 1 - L2 : 0, hi = std::min<uint64_t>(L1, t0 + tw);
+        const uint64_t len = hi > lo ? hi - lo : 0;
+        total += len;
+        longest = std::max(longest, len);
+    }
+    const uint64_t target = uint64_t(num_sms()) * 12;
+    uint64_t C = std::max<uint64_t>((total + target - 1) / target, 256);
+    C = (C + 255) / 256 * 256;
+    const uint64_t splits = std::max<uint64_t>((longest + C - 1) / C, 1);
+    return {static_cast<uint32_t>(std::min<uint64_t>(splits, 1u << 16)), std::max(C, (longest + 65535) / 65536)};
 }
 uint64_t align16(uint64_t b) { return (b + 15) / 16 * 16; }
 }  // namespace
@@ -393,7 +415,7 @@ uint64_t align16(uint64_t b) { return (b + 15) / 16 * 16; }
 uint64_t fqt_workspace_bytes(uint32_t k, uint32_t nq, uint64_t na, uint64_t nb) {
     const uint64_t L1 = fqt_chunks(na, k), L2 = fqt_chunks(nb, k), T = L1 + L2 - 1;
     const uint32_t nd = 2 * k - 1, nw = (nd + 3) / 4;
-    return align16(L1 * 8) + align16(L2 * 8) + uint64_t(fqt_splits(T, std::min(L1, L2), nq)) * T * nw * 4;
+    return align16(L1 * 8) + align16(L2 * 8) + uint64_t(fqt_split(L1, L2, nq).splits) * T * nw * 4;
 }
 
 cudaError_t launch_fqt_mul(const FqtParams& P, const uint8_t* a, uint64_t na, const uint8_t* b, uint64_t nb,
@@ -412,8 +434,9 @@ cudaError_t launch_fqt_mul(const FqtParams& P, const uint8_t* a, uint64_t na, co
     fqt_pack_kernel<<<static_cast<int>(std::min<uint64_t>((L2 + 255) / 256, sms * 8)), 256, 0, s>>>(P.rq.p, k, qd, b,
                                                                                                       nb, L2, qw);
     if (cudaError_t e = cudaGetLastError(); e != cudaSuccess) return e;
-    const uint32_t splits = fqt_splits(T, std::min(L1, L2), P.nq);
-    const uint64_t isplit = (L1 + splits - 1) / splits;
+    const FqtSplit sp = fqt_split(L1, L2, P.nq);
+    const uint32_t splits = sp.splits;
+    const uint64_t isplit = sp.chunk;
     cudaError_t e;
     switch (nd) {
         case 1: e = run_conv<1>(P, pw, L1, qw, L2, T, splits, isplit, res, s); break;
