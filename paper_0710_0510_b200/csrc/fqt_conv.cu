@@ -178,8 +178,8 @@ __global__ void __launch_bounds__(kFqtT) fqt_conv_step_kernel(const FqtParams P,
 // per 8 + 8 shared loads.  The qw tile is stored with one pad double per 8
 // (element j at j + j/8): lanes 8 apart in j land 9 doubles apart, 16 lanes
 // per 128-byte wavefront -- conflict-free.
-// STEP: close a group after every product (n_q < 8); else every G = n_q
-// rounded down to 8 products, checked per 8-step block.
+// A group closes every G = n_q rounded down to 8 products (n_q >= 8),
+// checked per 8-step block.
 constexpr int kRB = 8;
 constexpr int kFqtOut = kFqtT * kRB;       // output chunks per CTA
 constexpr int kQw = kFqtOut + kFqtI - 1;   // window values per i-tile
@@ -187,7 +187,7 @@ constexpr int kQwPad = kQw + kQw / 8 + 1;  // padded smem doubles
 
 __device__ __forceinline__ int qpad(int j) { return j + (j >> 3); }
 
-template <int ND, int W, class K, bool STEP>
+template <int ND, int W, class K>
 __global__ void __launch_bounds__(kFqtT) fqt_conv_kernel(const FqtParams P, const double* __restrict__ pw,
                                                          uint64_t L1, const double* __restrict__ qw, uint64_t L2,
                                                          uint64_t T, uint64_t isplit, uint32_t* __restrict__ res) {
@@ -217,7 +217,7 @@ __global__ void __launch_bounds__(kFqtT) fqt_conv_kernel(const FqtParams P, cons
         for (int w = 0; w < NW; ++w) racc[r][w] = 0;
     }
     uint32_t cnt = 0;
-    const uint32_t G = STEP ? 1u : P.nq - P.nq % 8;
+    const uint32_t G = P.nq - P.nq % 8;
     auto close_groups = [&]() {
 #pragma unroll
         for (int r = 0; r < kRB; ++r) {
@@ -250,39 +250,36 @@ __global__ void __launch_bounds__(kFqtT) fqt_conv_kernel(const FqtParams P, cons
         // step ii, output r: Q(8 tid + r + kFqtI - 1 - ii).  Block of 8 steps
         // from ii0: X[m] = Q(8 tid + kFqtI - 8 - ii0 + m), m = 0..14, step s
         // output r uses X[7 - s + r]
-        double X[15];
+        // two 8-value load sets alternate as the window's lower half; the
+        // other set's first 7 values are the upper half -- no register moves
+        double XA[8], XC[8];
         const int jb = kRB * tid + kFqtI - 8;
 #pragma unroll
-        for (int m = 8; m < 15; ++m) X[m] = qws[qpad(jb + m)];
-        for (int ii0 = 0; ii0 < n_i; ii0 += 8) {
+        for (int m = 0; m < 7; ++m) XC[m] = qws[qpad(jb + 8 + m)];
+        auto block = [&](int ii0, double (&lo8)[8], const double (&hi8)[8]) {
 #pragma unroll
-            for (int m = 0; m < 8; ++m) X[m] = qws[qpad(jb - ii0 + m)];
+            for (int m = 0; m < 8; ++m) lo8[m] = qws[qpad(jb - ii0 + m)];
             double pv[8];
 #pragma unroll
             for (int m = 0; m < 8; ++m) pv[m] = pws[ii0 + m];
-            if constexpr (STEP) {
+            // zero-padded pws makes steps past n_i add nothing
 #pragma unroll
-                for (int st = 0; st < 8; ++st) {
-                    if (ii0 + st < n_i) {
+            for (int st = 0; st < 8; ++st)
 #pragma unroll
-                        for (int r = 0; r < kRB; ++r) acc[r] = fma(pv[st], X[7 - st + r], acc[r]);
-                        close_groups();
-                    }
+                for (int r = 0; r < kRB; ++r) {
+                    const int m = 7 - st + r;
+                    acc[r] = fma(pv[st], m < 8 ? lo8[m] : hi8[m - 8], acc[r]);
                 }
-            } else {
-                // zero-padded pws makes steps past n_i add nothing
-#pragma unroll
-                for (int st = 0; st < 8; ++st)
-#pragma unroll
-                    for (int r = 0; r < kRB; ++r) acc[r] = fma(pv[st], X[7 - st + r], acc[r]);
-                cnt += 8;
-                if (cnt >= G) close_groups();
-            }
-#pragma unroll
-            for (int m = 0; m < 7; ++m) X[8 + m] = X[m];
+            cnt += 8;
+            if (cnt >= G) close_groups();
+        };
+        // n_i <= 256, so ii0 + 8 <= 248 keeps every window index >= 0
+        for (int ii0 = 0; ii0 < n_i; ii0 += 16) {
+            block(ii0, XA, XC);
+            block(ii0 + 8, XC, XA);
         }
     }
-    if (!STEP && cnt) close_groups();
+    if (cnt) close_groups();
 #pragma unroll
     for (int r = 0; r < kRB; ++r) {
         const uint64_t t = t0 + kRB * tid + r;
@@ -311,7 +308,7 @@ __global__ void fqt_overlap_kernel(uint32_t p, uint32_t k, uint32_t nd, const ui
     }
 }
 
-template <int ND, int W, class K, bool STEP>
+template <int ND, int W, class K>
 cudaError_t run_conv_k(const FqtParams& P, const double* pw, uint64_t L1, const double* qw, uint64_t L2,
                        uint64_t T, uint32_t splits, uint64_t isplit, uint32_t* res, cudaStream_t s) {
     const dim3 grid(static_cast<unsigned>((T + kFqtOut - 1) / kFqtOut), splits);
@@ -319,13 +316,13 @@ cudaError_t run_conv_k(const FqtParams& P, const double* pw, uint64_t L1, const 
     if (smem > 160 * 1024) return cudaErrorInvalidValue;
     static size_t cur = 0;
     if (smem > 24 * 1024 && smem > cur) {
-        if (cudaError_t e = cudaFuncSetAttribute(fqt_conv_kernel<ND, W, K, STEP>,
+        if (cudaError_t e = cudaFuncSetAttribute(fqt_conv_kernel<ND, W, K>,
                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
             e != cudaSuccess)
             return e;
         cur = smem;
     }
-    fqt_conv_kernel<ND, W, K, STEP><<<grid, kFqtT, smem, s>>>(P, pw, L1, qw, L2, T, isplit, res);
+    fqt_conv_kernel<ND, W, K><<<grid, kFqtT, smem, s>>>(P, pw, L1, qw, L2, T, isplit, res);
     return cudaGetLastError();
 }
 
@@ -364,8 +361,8 @@ cudaError_t run_conv_w(const FqtParams& P, const double* pw, uint64_t L1, const 
     if (P.nq < 8)
         return P.rq.qbits ? run_conv_step<ND, W, RtConst<true>>(P, pw, L1, qw, L2, T, splits, isplit, res, s)
                           : run_conv_step<ND, W, RtConst<false>>(P, pw, L1, qw, L2, T, splits, isplit, res, s);
-    return P.rq.qbits ? run_conv_k<ND, W, RtConst<true>, false>(P, pw, L1, qw, L2, T, splits, isplit, res, s)
-                      : run_conv_k<ND, W, RtConst<false>, false>(P, pw, L1, qw, L2, T, splits, isplit, res, s);
+    return P.rq.qbits ? run_conv_k<ND, W, RtConst<true>>(P, pw, L1, qw, L2, T, splits, isplit, res, s)
+                      : run_conv_k<ND, W, RtConst<false>>(P, pw, L1, qw, L2, T, splits, isplit, res, s);
 }
 
 template <int ND>
