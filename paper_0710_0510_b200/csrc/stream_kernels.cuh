@@ -203,45 +203,11 @@ struct PolymulOp {
     PolymulParams P;
     __host__ __device__ uint32_t tables_words() const { return W ? P.rq.n_entries : 0u; }
     __host__ __device__ const uint32_t* tables_src() const { return P.rq.table; }
-    // p = 3, q = 2^B (C1: B = 5, k = 4): coefficient bytes < 3 spread into
-    // B-bit lanes are the packed word; the exact integer product's lanes are
-    // the convolution digits, and Swar3 reduces all 2k-1 of them at once
-    static constexpr bool kSwar3 = [] {
-        if constexpr (K::kSafe) return K::kP == 3 && K::kQbits >= 4 && K::kQbits <= 7 &&
-                                       K::kQbits * (ND - 1) + 2 <= 32;
-        else return false;
-    }();
-
     __device__ __forceinline__ void apply(const uint32_t* a, const uint32_t* b, uint32_t (&ow)[R * OUT / 4],
                                           uint32_t tab, uint32_t&) const {
         const K c{P.rq};
         const double qd = static_cast<double>(P.rq.q);
         uint64_t rec[R];
-        if constexpr (kSwar3) {
-            constexpr int B = K::kQbits;
-            if (all_bytes_below<R * K_ / 4>(a, 3) && all_bytes_below<R * K_ / 4>(b, 3)) {
-#pragma unroll
-                for (int r = 0; r < R; ++r) {
-                    const uint32_t xa = record_int<K_>(a, r), xb = record_int<K_>(b, r);
-                    uint32_t wa = 0, wb = 0;  // byte i (2 bits) -> bits [B i, B i + 2)
-#pragma unroll
-                    for (int i = 0; i < K_; ++i) {
-                        wa |= (xa >> (8 * i - B * i)) & (3u << (B * i));
-                        wb |= (xb >> (8 * i - B * i)) & (3u << (B * i));
-                    }
-                    const uint64_t w = static_cast<uint64_t>(wa) * wb;  // < 2^(B(2k-1)) <= 2^52
-                    const double wd =
-                        __hiloint2double(0x43300000 | static_cast<int>(w >> 32), static_cast<int>(w)) - kTwo52;
-                    const uint32_t mu = static_cast<uint32_t>(Swar3<B, ND>::mu(w, wd, P.rq.inv_p));
-                    uint64_t v = 0;  // lane j (value <= 2) -> byte j
-#pragma unroll
-                    for (int j = 0; j < ND; ++j) v |= static_cast<uint64_t>((mu >> (B * j)) & 3u) << (8 * j);
-                    rec[r] = v;
-                }
-                pack_records<R, OUT>(rec, ow);
-                return;
-            }
-        }
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             uint32_t ca[K_], cb[K_];
