@@ -40,6 +40,23 @@ struct DevBuf {
     }
 };
 
+// Per-call device workspace in stream order (cudaMallocAsync / cudaFreeAsync
+// from the default pool): concurrent calls on different streams never share
+// scratch, like the reference's pure functions (SURVEY 8(b) "Threading"),
+// and the pool keeps repeated calls allocation-free.
+struct StreamBuf {
+    void* ptr = nullptr;
+    cudaStream_t s = nullptr;
+    StreamBuf(std::size_t bytes, cudaStream_t stream);
+    StreamBuf(const StreamBuf&) = delete;
+    StreamBuf& operator=(const StreamBuf&) = delete;
+    ~StreamBuf();
+    template <class T>
+    T* as() const {
+        return static_cast<T*>(ptr);
+    }
+};
+
 // Chunked host<->device pipeline for the `_host` entry points.  Chunk c's
 // inputs go up on the H2D stream, its kernel runs on the compute stream and
 // its outputs come back on the D2H stream; events chain the three and
@@ -85,7 +102,6 @@ struct DevicePlanCache {
     qpk::RedqParams prm{};
     gpu::DevBuf table;   // byte-packed correction windows
     gpu::DevBuf status;  // latched kErr* bits
-    gpu::DevBuf ws_fqt;  // K6 packed chunks and residue partials
     gpu::DevBuf io_a, io_b, io_c;
     std::mutex mu;
     std::unique_ptr<gpu::Staging> staging;
@@ -98,8 +114,6 @@ struct DeviceFieldCache {
     qpk::GfqMatmulParams mm{};
     qpk::GfqGemvParams gemv{};
     uint32_t nlh = 0;
-    gpu::DevBuf ws_a, ws_b;  // packed A^T and B
-    gpu::DevBuf ws_gemv;     // GEMV split partials
     gpu::DevBuf io_a, io_b, io_c;
     std::mutex mu;
     std::unique_ptr<gpu::Staging> staging;

@@ -41,6 +41,27 @@ void* DevBuf::ensure(std::size_t n) {
     return ptr;
 }
 
+StreamBuf::StreamBuf(std::size_t bytes, cudaStream_t stream) : s(stream) {
+    // keep freed workspace in the device's default pool across calls (the
+    // default release threshold of 0 would hand it back to the OS at every
+    // synchronisation, and re-mapping 1 GB costs milliseconds)
+    static const bool pool_kept = [] {
+        int dev = 0;
+        cudaMemPool_t pool = nullptr;
+        if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t keep = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+        return true;
+    }();
+    (void)pool_kept;
+    if (bytes) check(cudaMallocAsync(&ptr, bytes, s), "cudaMallocAsync");
+}
+
+StreamBuf::~StreamBuf() {
+    if (ptr) cudaFreeAsync(ptr, s);
+}
+
 Staging::Staging() {
     for (cudaStream_t* s : {&sh, &sk, &sd}) check(cudaStreamCreateWithFlags(s, cudaStreamNonBlocking), "cudaStreamCreate");
     for (int i = 0; i < kSlots; ++i)
@@ -379,8 +400,8 @@ void fqt_mul_device(const RedqPlan& plan, const QadicParams& params, const uint8
     F.rq = dp.prm;
     F.k = params.k;
     F.nq = static_cast<uint32_t>(std::max<u64>(params.n_q, 1));
-    void* ws = dp.ws_fqt.ensure(qpk::fqt_workspace_bytes(params.k, F.nq, na, nb));
-    check(qpk::launch_fqt_mul(F, a, na, b, nb, out, ws, s), "fqt_mul launch");
+    StreamBuf ws(qpk::fqt_workspace_bytes(params.k, F.nq, na, nb), s);
+    check(qpk::launch_fqt_mul(F, a, na, b, nb, out, ws.ptr, s), "fqt_mul launch");
 }
 
 void fqt_mul_host(const RedqPlan& plan, const QadicParams& params, const uint8_t* a, u64 na, const uint8_t* b, u64 nb,
@@ -530,8 +551,9 @@ void gfq_matmul_device(DeviceFieldCache& F, const GfqField& field, const void* A
                        uint32_t chunk, void* C, bool reps, cudaStream_t s) {
     if (m == 0 || n == 0) return;
     const u64 mp = round_up(m, 128), np = round_up(n, 128), kp = round_up(std::max<u64>(K, 1), 16);
-    auto* at = static_cast<double*>(F.ws_a.ensure(kp * mp * 8));
-    auto* bt = static_cast<double*>(F.ws_b.ensure(kp * np * 8));
+    StreamBuf wa(kp * mp * 8, s), wb(kp * np * 8, s);
+    auto* at = wa.as<double>();
+    auto* bt = wb.as<double>();
     if (mp != m || kp != K) check(cudaMemsetAsync(at, 0, kp * mp * 8, s), "memset");
     if (np != n || kp != K) check(cudaMemsetAsync(bt, 0, kp * np * 8, s), "memset");
     if (reps) {
@@ -592,8 +614,8 @@ void gfq_gemv_device(DeviceFieldCache& F, const GfqField& field, const uint32_t*
     const u64 n_q = field.params().n_q;
     qpk::GfqGemvParams G = F.gemv;
     G.chunk = lane_terms <= n_q ? 0u : static_cast<uint32_t>(n_q >= 4 ? n_q - n_q % 4 : n_q);
-    void* ws = F.ws_gemv.ensure(qpk::gemv_workspace_bytes(m, K, splits));
-    check(qpk::launch_gfq_gemv(G, A, x, m, K, splits, ws, y_rep, y_coeff, s), "gfq_gemv launch");
+    StreamBuf ws(qpk::gemv_workspace_bytes(m, K, splits), s);
+    check(qpk::launch_gfq_gemv(G, A, x, m, K, splits, ws.ptr, y_rep, y_coeff, s), "gfq_gemv launch");
 }
 
 void gfq_gemv_host(DeviceFieldCache& F, const GfqField& field, const uint32_t* A, const uint32_t* x, u64 m, u64 K,
