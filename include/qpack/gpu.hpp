@@ -21,6 +21,10 @@ namespace qpack::gpu {
 // residues (p <= 256).  (redq.hpp:73-74)
 void redq_residues_batch(std::span<const double> words, const RedqPlan& plan, std::span<std::uint8_t> out,
                          CostReport* cost = nullptr);
+// the same over integer words below min(q^(d+1), 2^64) (the reference's u128
+// integer mode, restricted to 64-bit words)
+void redq_residues_batch(std::span<const std::uint64_t> words, const RedqPlan& plan, std::span<std::uint8_t> out,
+                         CostReport* cost = nullptr);
 
 // n products of degree-<k polynomials (records of k coefficients) -> n*(2k-1)
 // residues, via pack -> fp64 product -> REDQ.  (dqt_mul_poly dqt.hpp:46,

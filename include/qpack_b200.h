@@ -75,6 +75,12 @@ QPK_API qpk_status qpk_redq_residues_f64(qpk_redq_plan plan, const double* words
                                          void* stream);
 QPK_API qpk_status qpk_redq_residues_f64_host(qpk_redq_plan plan, const double* words, uint64_t n,
                                               uint8_t* residues, qpk_cost* cost);
+/* the same for integer words (RedqMode::integer beyond fp64, redq.cpp:44-51):
+ * u64 words below min(q^(d+1), 2^64), any d and q                     */
+QPK_API qpk_status qpk_redq_residues_u64(qpk_redq_plan plan, const uint64_t* words, uint64_t n, uint8_t* residues,
+                                         void* stream);
+QPK_API qpk_status qpk_redq_residues_u64_host(qpk_redq_plan plan, const uint64_t* words, uint64_t n,
+                                              uint8_t* residues, qpk_cost* cost);
 /* wait for `stream`, then report (and clear) latched data errors:
  * QPK_ERR_DOMAIN = a word not below q^(d+1) / not an exact double (redq.cpp:27-28) */
 QPK_API qpk_status qpk_redq_sync(qpk_redq_plan plan, void* stream);

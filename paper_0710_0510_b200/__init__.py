@@ -97,6 +97,8 @@ SIGNATURES = {
     "qpk_redq_plan_destroy": (None, [VP]),
     "qpk_redq_residues_f64": (I, [VP, VP, U64, VP, VP]),
     "qpk_redq_residues_f64_host": (I, [VP, VP, U64, VP, PCost]),
+    "qpk_redq_residues_u64": (I, [VP, VP, U64, VP, VP]),
+    "qpk_redq_residues_u64_host": (I, [VP, VP, U64, VP, PCost]),
     "qpk_redq_sync": (I, [VP, VP]),
     "qpk_redq_cost": (I, [VP, U64, PCost]),
     "qpk_polymul_plan_create": (I, [U64, U64, U32, U32, C.POINTER(VP)]),
@@ -220,7 +222,18 @@ class RedqPlan:
             n = words.numel()
             if out is None:
                 out = torch.empty((n, nd), dtype=torch.uint8, device=words.device)
-            _check(lib().qpk_redq_residues_f64(self._h, _ptr(words), n, _ptr(out), _stream()))
+            if words.dtype in (torch.int64, torch.uint64):  # integer words (two's-complement bits as u64)
+                _check(lib().qpk_redq_residues_u64(self._h, _ptr(words), n, _ptr(out), _stream()))
+            else:
+                _check(lib().qpk_redq_residues_f64(self._h, _ptr(words), n, _ptr(out), _stream()))
+            return out
+        if isinstance(words, np.ndarray) and words.dtype == np.uint64:
+            w = np.ascontiguousarray(words).reshape(-1)
+            if out is None:
+                out = np.empty((w.size, nd), np.uint8)
+            cost = Cost()
+            _check(lib().qpk_redq_residues_u64_host(self._h, _ptr(w), w.size, _ptr(out), C.byref(cost)))
+            self.last_cost = cost.as_dict()
             return out
         w = _host(words, np.float64).reshape(-1)
         if out is None:

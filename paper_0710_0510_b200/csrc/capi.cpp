@@ -144,6 +144,26 @@ qpk_status qpk_redq_residues_f64_host(qpk_redq_plan plan, const double* words, u
     });
 }
 
+qpk_status qpk_redq_residues_u64(qpk_redq_plan plan, const uint64_t* words, uint64_t n, uint8_t* residues,
+                                 void* stream) {
+    return guard([&] {
+        need(plan != nullptr, "null plan");
+        need(n == 0 || (words && residues), "null buffer");
+        auto& dp = qpack::detail::device_plan(plan->plan);
+        qpack::gpu::redq_device_u64(dp, words, n, residues, as_stream(stream));
+    });
+}
+
+qpk_status qpk_redq_residues_u64_host(qpk_redq_plan plan, const uint64_t* words, uint64_t n, uint8_t* residues,
+                                      qpk_cost* cost) {
+    return guard([&] {
+        need(plan != nullptr, "null plan");
+        need(n == 0 || (words && residues), "null buffer");
+        qpack::gpu::redq_host_u64(qpack::detail::device_plan(plan->plan), words, n, residues);
+        put_cost(cost, qpack::detail::redq_batch_cost(plan->plan, n));
+    });
+}
+
 qpk_status qpk_redq_sync(qpk_redq_plan plan, void* stream) {
     return guard([&] {
         need(plan != nullptr, "null plan");

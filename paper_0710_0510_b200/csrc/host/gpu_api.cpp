@@ -102,6 +102,17 @@ qpk::RedqParams make_redq_params(const RedqPlan& plan, gpu::DevBuf* table) {
     P.limit = (pow_fits_u128(plan.q, plan.d + 1) && checked_pow_u128(plan.q, plan.d + 1) < two53)
                   ? static_cast<double>(static_cast<u64>(checked_pow_u128(plan.q, plan.d + 1)))
                   : 9007199254740992.0;
+    const u128 two64 = u128(1) << 64;
+    P.limit_u64 = (pow_fits_u128(plan.q, plan.d + 1) && checked_pow_u128(plan.q, plan.d + 1) < two64)
+                      ? static_cast<u64>(checked_pow_u128(plan.q, plan.d + 1))
+                      : 0;
+    {
+        u128 pw64 = 1;
+        for (unsigned i = 0; i <= plan.d; ++i) {
+            P.qpow64[i] = pw64 < two64 ? static_cast<u64>(pw64) : 0;
+            if (pw64 < two64) pw64 *= plan.q;
+        }
+    }
     u128 pw = 1;
     for (unsigned i = 0; i <= plan.d; ++i) {
         const bool small = pw < two53;
@@ -295,6 +306,33 @@ void redq_device(DevicePlanCache& dp, const double* d_words, u64 n, uint8_t* d_o
     check(qpk::launch_redq_f64(dp.prm, d_words, n, d_out, dp.status.as<uint32_t>(), s), "redq launch");
 }
 
+void redq_device_u64(DevicePlanCache& dp, const uint64_t* d_words, u64 n, uint8_t* d_out, cudaStream_t s) {
+    check(qpk::launch_redq_u64(dp.prm, d_words, n, d_out, dp.status.as<uint32_t>(), s), "redq launch");
+}
+
+void redq_host_u64(DevicePlanCache& dp, const uint64_t* h_words, u64 n, uint8_t* h_out) {
+    std::lock_guard<std::mutex> lock(dp.mu);
+    if (!dp.staging) dp.staging = std::make_unique<Staging>();
+    Staging& S = *dp.staging;
+    const u64 nd = dp.prm.d + 1, chunk = u64(1) << 21;
+    for (int sl = 0; sl < Staging::kSlots; ++sl) {
+        S.in0[sl].ensure(chunk * 8);
+        S.out[sl].ensure(chunk * nd);
+    }
+    S.run(
+        n, chunk,
+        [&](int sl, u64 off, u64 cnt, cudaStream_t s) {
+            check(cudaMemcpyAsync(S.in0[sl].ptr, h_words + off, cnt * 8, cudaMemcpyHostToDevice, s), "H2D");
+        },
+        [&](int sl, u64, u64 cnt, cudaStream_t s) {
+            redq_device_u64(dp, S.in0[sl].as<uint64_t>(), cnt, S.out[sl].as<uint8_t>(), s);
+        },
+        [&](int sl, u64 off, u64 cnt, cudaStream_t s) {
+            check(cudaMemcpyAsync(h_out + off * nd, S.out[sl].ptr, cnt * nd, cudaMemcpyDeviceToHost, s), "D2H");
+        });
+    raise_status(take_status(dp, S.sk));
+}
+
 // Host buffers in, host buffers out: H2D / kernel / D2H of consecutive
 // chunks on three streams so the copies of one chunk overlap the others.
 void redq_host(DevicePlanCache& dp, const double* h_words, u64 n, uint8_t* h_out) {
@@ -332,6 +370,15 @@ void redq_residues_batch(std::span<const double> words, const RedqPlan& plan, st
         throw std::invalid_argument("redq_residues_batch: output span holds fewer than n*(d+1) residues");
     DevicePlanCache& dp = detail::device_plan(plan);
     redq_host(dp, words.data(), words.size(), out.data());
+    if (cost) *cost += detail::redq_batch_cost(plan, words.size());
+}
+
+void redq_residues_batch(std::span<const std::uint64_t> words, const RedqPlan& plan, std::span<std::uint8_t> out,
+                         CostReport* cost) {
+    if (out.size() < words.size() * (plan.d + 1))
+        throw std::invalid_argument("redq_residues_batch: output span holds fewer than n*(d+1) residues");
+    DevicePlanCache& dp = detail::device_plan(plan);
+    redq_host_u64(dp, words.data(), words.size(), out.data());
     if (cost) *cost += detail::redq_batch_cost(plan, words.size());
 }
 

@@ -35,6 +35,8 @@ struct RedqParams {
     double limit;         // min(q^(d+1), 2^53): words must lie below
     uint64_t q;
     uint64_t qpow[kMaxDigits];
+    uint64_t qpow64[kMaxDigits];  // q^i exactly when < 2^64, else 0 (u64 words: floor(r / q^i) = 0)
+    uint64_t limit_u64;           // q^(d+1) when < 2^64, else 0 (every u64 word is in range)
     double inv_q[kMaxDigits];  // ReciprocalDivisor(q^i).inv_up, general q
     const uint32_t* table;     // device table, byte-packed windows (mu_j in byte j)
 };
@@ -103,6 +105,10 @@ struct FqtParams {
 
 // ---- launchers (return cudaError_t of the launch) ----
 cudaError_t launch_redq_f64(const RedqParams& P, const double* words, uint64_t n, uint8_t* out,
+                            uint32_t* status, cudaStream_t s);
+// REDQ of integer words (u64; the reference's integer mode beyond fp64):
+// floor(r/p) as (hi/p) 2^32 + premul floor of (hi mod p) 2^32 + lo (< 2^40 <= r_max)
+cudaError_t launch_redq_u64(const RedqParams& P, const uint64_t* words, uint64_t n, uint8_t* out,
                             uint32_t* status, cudaStream_t s);
 cudaError_t launch_polymul(const PolymulParams& P, const uint8_t* a, const uint8_t* b, uint64_t n,
                            uint8_t* out, uint32_t* status, cudaStream_t s);

@@ -61,6 +61,47 @@ __global__ void redq_generic_kernel(const RedqParams P, const double* __restrict
     report_g(err, status);
 }
 
+// REDQ of u64 integer words (any d, any q): one word per thread.  rop =
+// floor(r/p) from a 32-bit division of the high half and the premultiplied
+// fp64 floor (Lemma 1) of (hi mod p) 2^32 + lo < p 2^32 <= 2^40 <= r_max, so
+// no 64-bit division runs for p; digits by shifts (q = 2^b) or by exact u64
+// divisions by q^i.  The direct correction equals the tabulated one.
+__global__ void redq_u64_kernel(const RedqParams P, const uint64_t* __restrict__ words, uint64_t n,
+                                uint8_t* __restrict__ out, uint32_t* status) {
+    uint32_t err = 0;
+    const uint32_t nd = P.d + 1;
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
+        uint64_t r = words[i];
+        if (P.limit_u64 && r >= P.limit_u64) {
+            err |= kErrDomain;
+            r = 0;
+        }
+        const uint32_t hi = static_cast<uint32_t>(r >> 32), lo = static_cast<uint32_t>(r);
+        const uint32_t q1 = hi / P.p;
+        const uint64_t t = (static_cast<uint64_t>(hi - q1 * P.p) << 32) | lo;
+        const uint64_t rop = (static_cast<uint64_t>(q1) << 32) + floor_div_premul(static_cast<double>(t), P.inv_p);
+        uint32_t u[kMaxDigits];
+        for (uint32_t j = 0; j < nd; ++j) {
+            uint64_t x, y;
+            if (P.qbits) {
+                const uint32_t sh = P.qbits * j;
+                x = sh < 64 ? r >> sh : 0;
+                y = sh < 64 ? rop >> sh : 0;
+            } else if (P.qpow64[j]) {
+                x = r / P.qpow64[j];
+                y = rop / P.qpow64[j];
+            } else {
+                x = y = 0;
+            }
+            u[j] = static_cast<uint32_t>(x) - P.p * static_cast<uint32_t>(y);
+        }
+        if (P.neg_q)
+            for (uint32_t j = 0; j + 1 < nd; ++j) u[j] = mod_small_g(u[j] + P.neg_q * u[j + 1], P.p, P.mod_magic);
+        for (uint32_t j = 0; j < nd; ++j) out[i * nd + j] = static_cast<uint8_t>(u[j]);
+    }
+    report_g(err, status);
+}
+
 __global__ void gfq_mul_rep_kernel(uint32_t group, const uint32_t* __restrict__ a, const uint32_t* __restrict__ b,
                                    uint64_t n, uint32_t* __restrict__ out) {
     for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
@@ -127,6 +168,14 @@ cudaError_t launch_redq_f64(const RedqParams& P, const double* words, uint64_t n
             redq_generic_kernel<<<grid_for(n), 256, 0, s>>>(P, words, n, out, status);
             return cudaGetLastError();
     }
+}
+
+cudaError_t launch_redq_u64(const RedqParams& P, const uint64_t* words, uint64_t n, uint8_t* out, uint32_t* status,
+                            cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    if (P.d + 1 > uint32_t(kMaxDigits)) return cudaErrorInvalidValue;
+    redq_u64_kernel<<<grid_for(n), 256, 0, s>>>(P, words, n, out, status);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_polymul(const PolymulParams& P, const uint8_t* a, const uint8_t* b, uint64_t n, uint8_t* out,
