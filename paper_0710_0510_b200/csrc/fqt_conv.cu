@@ -290,21 +290,52 @@ __global__ void __launch_bounds__(kFqtT) fqt_conv_kernel(const FqtParams P, cons
     }
 }
 
-// out[cidx] = residue j of chunk u plus residue j+k of chunk u-1, all splits
-__global__ void fqt_overlap_kernel(uint32_t p, uint32_t k, uint32_t nd, const uint32_t* __restrict__ res,
-                                   uint32_t splits, uint64_t T, uint8_t* __restrict__ out, uint64_t nout) {
+// Overlap-add: chunk u of the output is residues 0..k-1 of product chunk u
+// plus residues k..2k-2 of chunk u-1, each summed over the splits.  A CTA
+// owns 256 chunks: every thread sums its chunk's split partials lane-wise
+// mod p (one coalesced word per split and lane word), the sums meet in
+// shared memory, and each thread writes its k coefficients.
+__global__ void __launch_bounds__(256) fqt_overlap_kernel(uint32_t p, uint32_t k, uint32_t nd,
+                                                          const uint32_t* __restrict__ res, uint32_t splits,
+                                                          uint64_t T, uint8_t* __restrict__ out, uint64_t nout) {
+    __shared__ uint32_t sums[257][4];
     const uint32_t nw = (nd + 3) / 4;
-    for (uint64_t ci = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; ci < nout;
-         ci += uint64_t(gridDim.x) * blockDim.x) {
-        const uint64_t u = ci / k;
-        const uint32_t j = static_cast<uint32_t>(ci % k);
-        uint32_t v = 0;
-        for (uint32_t s = 0; s < splits; ++s) {
-            if (u < T) v += (res[(s * T + u) * nw + j / 4] >> (8 * (j % 4))) & 0xffu;
-            const uint32_t jh = j + k;
-            if (u >= 1 && jh < nd) v += (res[(s * T + u - 1) * nw + jh / 4] >> (8 * (jh % 4))) & 0xffu;
+    const uint64_t nchunks = (nout + k - 1) / k;
+    for (uint64_t u0 = uint64_t(blockIdx.x) * 256; u0 < nchunks; u0 += uint64_t(gridDim.x) * 256) {
+        // slot 0 holds chunk u0-1, slot i+1 chunk u0+i
+        for (int slot = threadIdx.x; slot < 257; slot += blockDim.x) {
+            const int64_t u = static_cast<int64_t>(u0) - 1 + slot;
+            uint32_t acc[4] = {0, 0, 0, 0};
+            if (u >= 0 && static_cast<uint64_t>(u) < T) {
+                for (uint32_t w = 0; w < nw; ++w) {
+                    const uint32_t* src = res + static_cast<uint64_t>(u) * nw + w;
+                    const uint64_t stride = T * nw;
+                    uint32_t sp = 0;
+                    for (; sp + 8 <= splits; sp += 8) {  // 8 independent loads in flight
+                        uint32_t v[8];
+#pragma unroll
+                        for (int x = 0; x < 8; ++x) v[x] = __ldg(src + (sp + x) * stride);
+#pragma unroll
+                        for (int x = 0; x < 8; ++x) acc[w] = add_mod_lanes(acc[w], v[x], p);
+                    }
+                    for (; sp < splits; ++sp) acc[w] = add_mod_lanes(acc[w], __ldg(src + sp * stride), p);
+                }
+            }
+            for (uint32_t w = 0; w < 4; ++w) sums[slot][w] = acc[w];
         }
-        out[ci] = static_cast<uint8_t>(v % p);
+        __syncthreads();
+        const uint64_t u = u0 + threadIdx.x;
+        if (u < nchunks) {
+            for (uint32_t j = 0; j < k; ++j) {
+                const uint64_t ci = u * k + j;
+                if (ci >= nout) break;
+                uint32_t v = (sums[threadIdx.x + 1][j / 4] >> (8 * (j % 4))) & 0xffu;
+                const uint32_t jh = j + k;
+                if (jh < nd) v += (sums[threadIdx.x][jh / 4] >> (8 * (jh % 4))) & 0xffu;
+                out[ci] = static_cast<uint8_t>(v >= p ? v - p : v);
+            }
+        }
+        __syncthreads();
     }
 }
 
@@ -448,7 +479,8 @@ cudaError_t launch_fqt_mul(const FqtParams& P, const uint8_t* a, uint64_t na, co
     }
     if (e != cudaSuccess) return e;
     const uint64_t nout = na + nb - 1;
-    fqt_overlap_kernel<<<static_cast<int>(std::min<uint64_t>((nout + 255) / 256, sms * 8)), 256, 0, s>>>(
+    const uint64_t nchunks = (nout + k - 1) / k;
+    fqt_overlap_kernel<<<static_cast<int>(std::min<uint64_t>((nchunks + 255) / 256, sms * 8)), 256, 0, s>>>(
         P.rq.p, k, nd, res, splits, T, out, nout);
     return cudaGetLastError();
 }
