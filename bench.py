@@ -518,7 +518,14 @@ def measure_secondary(Q, torch, dev):
         tf = 2 * nn ** 3 / (ms * 1e-3) / 1e12
         res[f"c{cfg.cid}_gfq_matmul"] = {"gf_ops_per_s": 2 * nn ** 3 / (ms * 1e-3), "ms": ms, "tflops": tf,
                                           "frac_dmma_probe": tf / fp64_peak, "frac_nominal_37": tf / 37.0,
-                                          "n": nn, "chunk": cfg.chunk}
+                                          "n": nn, "chunk": cfg.chunk, "repack": "redq"}
+        if cfg.cid == 5:
+            # the same product with the lane-fold re-pack (same C)
+            ms = time_it(lambda: f.matmul(A, B, nn, nn, nn, cfg.chunk, out=Cm, repack="fold"), 5, warm=2, cold=False)
+            tf = 2 * nn ** 3 / (ms * 1e-3) / 1e12
+            res["c5_gfq_matmul_fold"] = {"gf_ops_per_s": 2 * nn ** 3 / (ms * 1e-3), "ms": ms, "tflops": tf,
+                                         "frac_dmma_probe": tf / fp64_peak, "frac_nominal_37": tf / 37.0,
+                                         "n": nn, "chunk": cfg.chunk, "repack": "fold"}
         del A, B, Cm
     return res
 

@@ -42,10 +42,16 @@ void gfq_mul_batch(std::span<const std::uint8_t> a, std::span<const std::uint8_t
 void gfq_mul_batch(std::span<const GfqElt> a, std::span<const GfqElt> b, const GfqField& field,
                    std::span<GfqElt> out);
 
+// Delayed re-pack between K-chunks: `redq` re-packs every accumulated word
+// to sum mu_i q^i (REDQ + assemble, redq.cpp:178-182); `fold` (GF(3^3) at
+// q = 2^10) replaces each digit by a smaller one congruent mod p (see
+// DESIGN.md 5).  Both give the same product.
+enum class Repack : std::uint32_t { redq = 0, fold = 1 };
+
 // C = A*B of coefficient records: A is m x K x k, B is K x n x k, C m x n x k
 void gfq_matmul_coeffs(std::span<const std::uint8_t> A, std::span<const std::uint8_t> B, std::size_t m,
                        std::size_t K, std::size_t n, const GfqField& field, std::span<std::uint8_t> C,
-                       std::uint32_t chunk = 0, CostReport* cost = nullptr);
+                       std::uint32_t chunk = 0, CostReport* cost = nullptr, Repack repack = Repack::redq);
 
 // y = A x over GF(p^k) on reps: A is m x K (row-major), x has K entries, y
 // gets m.  Each y_i is fgdp_dot(A[i,:], x) (gfq.hpp:98-99, gfq.cpp:335-387).

@@ -151,6 +151,17 @@ QPK_API qpk_status qpk_gfq_matmul(qpk_field f, const uint8_t* A, const uint8_t* 
                                   uint64_t n, uint32_t chunk, uint8_t* C, void* stream);
 QPK_API qpk_status qpk_gfq_matmul_host(qpk_field f, const uint8_t* A, const uint8_t* B, uint64_t m, uint64_t K,
                                        uint64_t n, uint32_t chunk, uint8_t* C, qpk_cost* cost);
+/* as qpk_gfq_matmul with the delayed re-pack chosen: QPK_REPACK_REDQ (every
+ * word re-packed to sum mu_i q^i, redq + assemble, redq.cpp:178-182) or
+ * QPK_REPACK_FOLD (GF(3^3) at q = 2^10: digits folded to smaller values
+ * congruent mod p, chunk sized for the fold's digit bound); same C. */
+#define QPK_REPACK_REDQ 0u
+#define QPK_REPACK_FOLD 1u
+QPK_API qpk_status qpk_gfq_matmul_repack(qpk_field f, const uint8_t* A, const uint8_t* B, uint64_t m, uint64_t K,
+                                         uint64_t n, uint32_t chunk, uint32_t repack, uint8_t* C, void* stream);
+QPK_API qpk_status qpk_gfq_matmul_repack_host(qpk_field f, const uint8_t* A, const uint8_t* B, uint64_t m,
+                                              uint64_t K, uint64_t n, uint32_t chunk, uint32_t repack, uint8_t* C,
+                                              qpk_cost* cost);
 /* the reference signature on GfqMatrix data: reps (u32) in, reps out */
 QPK_API qpk_status qpk_gfq_matmul_rep(qpk_field f, const uint32_t* A, const uint32_t* B, uint64_t m, uint64_t K,
                                       uint64_t n, uint32_t* C, void* stream);

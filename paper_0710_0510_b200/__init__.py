@@ -118,6 +118,8 @@ SIGNATURES = {
     "qpk_gfq_mul_rep_host": (I, [VP, VP, VP, U64, VP]),
     "qpk_gfq_matmul": (I, [VP, VP, VP, U64, U64, U64, U32, VP, VP]),
     "qpk_gfq_matmul_host": (I, [VP, VP, VP, U64, U64, U64, U32, VP, PCost]),
+    "qpk_gfq_matmul_repack": (I, [VP, VP, VP, U64, U64, U64, U32, U32, VP, VP]),
+    "qpk_gfq_matmul_repack_host": (I, [VP, VP, VP, U64, U64, U64, U32, U32, VP, PCost]),
     "qpk_gfq_matmul_rep": (I, [VP, VP, VP, U64, U64, U64, VP, VP]),
     "qpk_gfq_matmul_rep_host": (I, [VP, VP, VP, U64, U64, U64, VP, PCost]),
     "qpk_gfq_gemv": (I, [VP, VP, VP, U64, U64, VP, VP, VP]),
@@ -419,20 +421,25 @@ class GfqField:
         _check(lib().qpk_gfq_mul_rep_host(self._h, _ptr(a), _ptr(b), a.size, _ptr(out)))
         return out
 
-    def matmul(self, A, B, m, K, n, chunk=0, out=None):
-        """C = A*B on coefficient records (A m x K x k, B K x n x k)."""
+    def matmul(self, A, B, m, K, n, chunk=0, out=None, repack="redq"):
+        """C = A*B on coefficient records (A m x K x k, B K x n x k).
+        repack: "redq" (delayed REDQ re-pack, the default) or "fold"
+        (GF(3^3) at q = 2^10 only; same C)."""
+        mode = {"redq": 0, "fold": 1}[repack]
         if _is_torch(A):
             import torch
             if out is None:
                 out = torch.empty((m, n, self.k), dtype=torch.uint8, device=A.device)
-            _check(lib().qpk_gfq_matmul(self._h, _ptr(A), _ptr(B), m, K, n, chunk, _ptr(out), _stream()))
+            _check(lib().qpk_gfq_matmul_repack(self._h, _ptr(A), _ptr(B), m, K, n, chunk, mode, _ptr(out),
+                                               _stream()))
             return out
         A = _host(A, np.uint8)
         B = _host(B, np.uint8)
         if out is None:
             out = np.empty((m, n, self.k), np.uint8)
         cost = Cost()
-        _check(lib().qpk_gfq_matmul_host(self._h, _ptr(A), _ptr(B), m, K, n, chunk, _ptr(out), C.byref(cost)))
+        _check(lib().qpk_gfq_matmul_repack_host(self._h, _ptr(A), _ptr(B), m, K, n, chunk, mode, _ptr(out),
+                                                C.byref(cost)))
         self.last_cost = cost.as_dict()
         return out
 

@@ -384,6 +384,36 @@ qpk_status qpk_gfq_matmul_host(qpk_field f, const uint8_t* A, const uint8_t* B, 
     });
 }
 
+qpk_status qpk_gfq_matmul_repack(qpk_field f, const uint8_t* A, const uint8_t* B, uint64_t m, uint64_t K,
+                                 uint64_t n, uint32_t chunk, uint32_t repack, uint8_t* C, void* stream) {
+    return guard([&] {
+        need(f != nullptr, "null field");
+        need((m == 0 || n == 0) || (A && B && C) || K == 0, "null buffer");
+        if (K == 0 && m && n) {
+            qpack::gpu::check(cudaMemsetAsync(C, 0, m * n * f->f.k(), as_stream(stream)), "memset");
+            return;
+        }
+        qpack::gpu::gfq_matmul_device(qpack::detail::device_field(f->f), f->f, A, B, m, K, n, chunk, C, false,
+                                      as_stream(stream), repack);
+    });
+}
+
+qpk_status qpk_gfq_matmul_repack_host(qpk_field f, const uint8_t* A, const uint8_t* B, uint64_t m, uint64_t K,
+                                      uint64_t n, uint32_t chunk, uint32_t repack, uint8_t* C, qpk_cost* cost) {
+    return guard([&] {
+        need(f != nullptr, "null field");
+        need((m == 0 || n == 0) || (A && B && C) || K == 0, "null buffer");
+        if (m && n) {
+            if (K == 0)
+                std::memset(C, 0, m * n * f->f.k());
+            else
+                qpack::gpu::gfq_matmul_host(qpack::detail::device_field(f->f), f->f, A, B, m, K, n, chunk, C, false,
+                                            repack);
+        }
+        put_cost(cost, qpack::gpu::matmul_cost(f->f, m, K, n));
+    });
+}
+
 qpk_status qpk_gfq_matmul_rep(qpk_field f, const uint32_t* A, const uint32_t* B, uint64_t m, uint64_t K, uint64_t n,
                               uint32_t* C, void* stream) {
     return guard([&] {

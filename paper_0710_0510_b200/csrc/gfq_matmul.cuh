@@ -80,6 +80,19 @@ __device__ __forceinline__ double redq_repack(const K& c, double r) {
     }
 }
 
+// Biased accumulators (the fold re-pack): the accumulator holds 2^52 + r,
+// an integer in [2^52, 2^53) where fp64 is exact with ulp 1, so its 52
+// mantissa bits are r itself -- the re-pack reads and writes r as bits with
+// no fp64 <-> integer conversions.  Words stay below 2^52 (mm_plan_safe).
+constexpr uint64_t kBiasBits = 0x4330000000000000ull;  // bits of 2^52
+
+template <int ND, uint32_t B>
+__host__ __device__ constexpr uint64_t lane_ones() {
+    uint64_t m = 0;
+    for (int i = 0; i < ND; ++i) m |= uint64_t(1) << (B * i);
+    return m;
+}
+
 // The same REDQ + re-pack for p = 3 and q = 2^B with B even (q == 1 mod 3),
 // computed lane-wise inside one 64-bit integer (lane i = bits [Bi, Bi+B)):
 //  * u_i in [0, 2] is fixed by its value mod 4, and
@@ -91,14 +104,12 @@ __device__ __forceinline__ double redq_repack(const K& c, double r) {
 //    (every lane stays non-negative, so no borrow crosses lanes);
 //  * the mu lanes already sit at q^i: the re-packed word, no assembly.
 // rop = floor(r/3) is still the one premultiplied fp64 floor of Lemma 1.
+// (Plain accumulators: the biased form of the fold below measured 2% slower
+// here -- r is needed as a double for the floor anyway.)
 template <int ND, uint32_t B>
 __device__ __forceinline__ double redq_repack_swar3(const RedqParams& P, double r) {
     static_assert(B % 2 == 0 && B >= 4 && B * (ND - 1) + 3 <= 52, "lanes of >= 4 bits below 2^52");
-    constexpr uint64_t M1 = [] {
-        uint64_t m = 0;
-        for (int i = 0; i < ND; ++i) m |= uint64_t(1) << (B * i);
-        return m;
-    }();
+    constexpr uint64_t M1 = lane_ones<ND, B>();
     constexpr uint64_t M3 = 3 * M1;
     const uint64_t rb = dbits(r + kTwo52);                          // low 52 bits = r
     const uint64_t ob = dbits(__dadd_rz(__dmul_ru(r, P.inv_p), kTwo52));  // low 52 bits = floor(r/3)
@@ -106,8 +117,31 @@ __device__ __forceinline__ double redq_repack_swar3(const RedqParams& P, double 
     const uint64_t v = u + 8 * M1 - (u >> B);                       // u_i + 8 - u_{i+1}
     const uint64_t g = (v >> 3) & M1;                               // [u_i >= u_{i+1}]
     const uint64_t mu = v - 5 * M1 - 3 * g;                         // (u_i - u_{i+1}) mod 3
-    return __longlong_as_double(static_cast<long long>(mu | 0x4330000000000000ull)) - kTwo52;
+    return __longlong_as_double(static_cast<long long>(mu | kBiasBits)) - kTwo52;
 }
+
+// Lane fold (repack mode QPK_REPACK_FOLD), p = 3 and q = 2^B: every digit
+// c_i = l_i + 2^S h_i (l_i < 2^S) is replaced by l_i + h_i, which is
+// congruent mod 3 because 2^S == 1 (mod 3) for even S.  Digits drop from
+// < q to <= (2^S - 1) + (2^(B-S) - 1) (78 for B = 10, S = 6) -- not the
+// canonical mu_i of REDQ, but the same value of every digit mod p, so the
+// final REDQ and the output are identical; the host sizes the chunk for the
+// larger post-fold digit bound.  On the biased accumulator this is pure
+// integer lane arithmetic: 2 masks, 1 shift, 1 add (no fp64 work).
+template <int ND, uint32_t B, uint32_t S>
+__device__ __forceinline__ double repack_fold3(double acc) {
+    static_assert(S % 2 == 0 && S < B && B * ND <= 52, "2^S == 1 mod 3, lanes below 2^52");
+    constexpr uint64_t M1 = lane_ones<ND, B>();
+    constexpr uint64_t ML = M1 * ((uint64_t(1) << S) - 1);
+    constexpr uint64_t MH = M1 * ((uint64_t(1) << (B - S)) - 1);
+    const uint64_t rb = dbits(acc);
+    const uint64_t f = (rb & ML) + ((rb >> S) & MH);
+    return __longlong_as_double(static_cast<long long>(f | kBiasBits));
+}
+
+// fold split S: the largest even S <= B - S + 2 (balances l_i and h_i)
+template <uint32_t B>
+constexpr uint32_t kFoldShift = ((B + 2) / 2) % 2 ? (B + 2) / 2 + 1 : (B + 2) / 2;
 
 template <class K>
 struct is_swar3 {
@@ -118,12 +152,23 @@ struct is_swar3<CtConst<3, QB>> {
     static constexpr bool value = (QB % 2 == 0) && QB >= 4;
 };
 
-template <int ND, class K>
+// accumulators carry the 2^52 bias exactly when the fold re-packs them
+template <class K, bool FOLD>
+struct mm_biased {
+    static constexpr bool value = is_swar3<K>::value && FOLD;
+};
+
+template <int ND, class K, bool FOLD>
 __device__ __forceinline__ double repack_one(const K& c, double r) {
-    if constexpr (is_swar3<K>::value)
-        return redq_repack_swar3<ND, K::kQbits>(c.P, r);
-    else
+    if constexpr (is_swar3<K>::value) {
+        if constexpr (FOLD)
+            return repack_fold3<ND, K::kQbits, kFoldShift<K::kQbits>>(r);
+        else
+            return redq_repack_swar3<ND, K::kQbits>(c.P, r);
+    } else {
+        static_assert(!FOLD, "the lane fold is compiled for p = 3, q = 2^(2m) only");
         return redq_repack<ND>(c, r);
+    }
 }
 
 __device__ __forceinline__ uint32_t add_mod_bytes_mm(uint32_t x, uint32_t y, uint32_t p) {
@@ -160,7 +205,9 @@ __device__ __forceinline__ uint32_t acc_to_coeffs(const K& c, uint32_t lh_radix,
 
 // REDQ_STAGE: re-pack at stage granularity (chunk a multiple of BK) rather
 // than per 4-step MMA (fields whose safe chunk is below BK)
-template <int KR, class K, bool REDQ_STAGE, int NST>
+// (9 warps: one SM sub-partition holds 3 of them, so 16384 / (3 * 32) caps
+// the kernel at 168 registers per thread)
+template <int KR, class K, bool REDQ_STAGE, int NST, bool FOLD>
 __global__ void __launch_bounds__(THREADS, 1)
     gfq_matmul_kernel(const GfqMatmulParams P, const double* __restrict__ at, const double* __restrict__ bm,
                       uint64_t m, uint64_t n, uint64_t K_pad, uint64_t m_pad, uint64_t n_pad,
@@ -214,19 +261,20 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int wm = (warp >> 2) * WM;  // 2 x 4 warp grid; warps w, w+4 share SMSP w%4
     const int wn = (warp & 3) * WN;
     const int lr = lane >> 2, lc4 = lane & 3;
+    constexpr double kBias = mm_biased<K, FOLD>::value ? kTwo52 : 0.0;
     double acc[MT][NT][2];
 #pragma unroll
     for (int i = 0; i < MT; ++i)
 #pragma unroll
-        for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+        for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = kBias;
 
     auto repack_all = [&]() {
 #pragma unroll
         for (int i = 0; i < MT; ++i)
 #pragma unroll
             for (int j = 0; j < NT; ++j) {
-                acc[i][j][0] = repack_one<ND>(c, acc[i][j][0]);
-                acc[i][j][1] = repack_one<ND>(c, acc[i][j][1]);
+                acc[i][j][0] = repack_one<ND, K, FOLD>(c, acc[i][j][0]);
+                acc[i][j][1] = repack_one<ND, K, FOLD>(c, acc[i][j][1]);
             }
     };
     // 4 MMA k-steps of one stage; per step 8 A and 4 B fragments -> 32 DMMA
@@ -302,7 +350,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 if (row < m && col + h < n) {
-                    const uint32_t cf = acc_to_coeffs<KR>(c, P.lh_radix, acc[i][j][h], lc_s, hc_s);
+                    const uint32_t cf = acc_to_coeffs<KR>(c, P.lh_radix, acc[i][j][h] - kBias, lc_s, hc_s);
                     if (out_c) {
                         uint8_t* dst = out_c + (row * n + col + h) * KR;
 #pragma unroll
@@ -319,7 +367,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
 }
 
-template <int KR, class K, bool REDQ_STAGE, int NST = 4>
+template <int KR, class K, bool REDQ_STAGE, int NST = 4, bool FOLD = false>
 cudaError_t run_matmul_t(const GfqMatmulParams& P, const double* at, const double* b, uint64_t m, uint64_t n,
                          uint64_t K_pad, uint64_t m_pad, uint64_t n_pad, uint8_t* oc, uint32_t* orp, cudaStream_t s) {
     uint32_t nlh = 1;
@@ -328,14 +376,14 @@ cudaError_t run_matmul_t(const GfqMatmulParams& P, const double* at, const doubl
     if (smem > 227 * 1024) return cudaErrorInvalidValue;
     static bool attr = false;
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(gfq_matmul_kernel<KR, K, REDQ_STAGE, NST>,
+        cudaError_t e = cudaFuncSetAttribute(gfq_matmul_kernel<KR, K, REDQ_STAGE, NST, FOLD>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         if (e != cudaSuccess) return e;
         attr = true;
     }
     dim3 grid(static_cast<unsigned>(n_pad / BN), static_cast<unsigned>(m_pad / BM));
-    gfq_matmul_kernel<KR, K, REDQ_STAGE, NST><<<grid, THREADS, smem, s>>>(P, at, b, m, n, K_pad, m_pad, n_pad, oc,
-                                                                          orp);
+    gfq_matmul_kernel<KR, K, REDQ_STAGE, NST, FOLD><<<grid, THREADS, smem, s>>>(P, at, b, m, n, K_pad, m_pad, n_pad,
+                                                                                oc, orp);
     return cudaGetLastError();
 }
 
@@ -358,7 +406,10 @@ cudaError_t run_matmul(const GfqMatmulParams& P, const double* at, const double*
         }
         if constexpr (KR == 3) {
             if (P.p == 3 && P.rq.qbits == 10 && mm_plan_safe(P.rq) && stage_ok)
-                return run_matmul_t<3, CtConst<3, 10>, true, 6>(P, at, b, m, n, K_pad, m_pad, n_pad, oc, orp, s);
+                return P.repack == kRepackFold
+                           ? run_matmul_t<3, CtConst<3, 10>, true, 6, true>(P, at, b, m, n, K_pad, m_pad, n_pad, oc,
+                                                                            orp, s)
+                           : run_matmul_t<3, CtConst<3, 10>, true, 6>(P, at, b, m, n, K_pad, m_pad, n_pad, oc, orp, s);
         }
         return cudaErrorNotSupported;
     } else {

@@ -575,11 +575,18 @@ namespace {
 u64 round_up(u64 v, u64 m) { return (v + m - 1) / m * m; }
 }  // namespace
 
-uint32_t resolve_chunk(const DeviceFieldCache& F, const GfqField& field, u64 K, uint32_t chunk) {
+uint32_t resolve_chunk(const DeviceFieldCache& F, const GfqField& field, u64 K, uint32_t chunk, uint32_t repack) {
     const u64 p = field.p(), k = field.k(), q = field.params().q;
     const u64 unit = k * (p - 1) * (p - 1);
-    // after a re-pack every digit is <= p-1; `safe` more products keep it < q
-    const u64 safe = unit ? (q - 1 - (p - 1)) / unit : K;
+    if (repack > qpk::kRepackFold) throw std::invalid_argument("gfq_matmul: unknown re-pack mode");
+    // the lane fold is compiled for the GF(3^3), q = 2^10 fast path (p = 3:
+    // 2^S == 1 mod 3 for even S)
+    if (repack == qpk::kRepackFold && !(p == 3 && k == 3 && q == 1024))
+        throw std::invalid_argument("gfq_matmul: the fold re-pack is provided for GF(3^3) at q = 2^10 only");
+    // after a re-pack every digit is <= p-1 (REDQ) or <= the fold bound;
+    // `safe` more products keep it < q
+    const u64 post = repack == qpk::kRepackFold ? qpk::fold_digit_bound(10) : p - 1;
+    const u64 safe = unit ? (q - 1 - post) / unit : K;
     (void)F;
     if (chunk == 0) {
         if (K <= field.params().n_q) return 0;  // one accumulation group: never reduce
@@ -595,7 +602,7 @@ uint32_t resolve_chunk(const DeviceFieldCache& F, const GfqField& field, u64 K, 
 
 // A, B, C device pointers: coefficient records (reps when `reps`)
 void gfq_matmul_device(DeviceFieldCache& F, const GfqField& field, const void* A, const void* B, u64 m, u64 K, u64 n,
-                       uint32_t chunk, void* C, bool reps, cudaStream_t s) {
+                       uint32_t chunk, void* C, bool reps, cudaStream_t s, uint32_t repack) {
     if (m == 0 || n == 0) return;
     const u64 mp = round_up(m, 128), np = round_up(n, 128), kp = round_up(std::max<u64>(K, 1), 16);
     StreamBuf wa(kp * mp * 8, s), wb(kp * np * 8, s);
@@ -615,14 +622,15 @@ void gfq_matmul_device(DeviceFieldCache& F, const GfqField& field, const void* A
               "pack B");
     }
     qpk::GfqMatmulParams M = F.mm;
-    M.chunk = resolve_chunk(F, field, K, chunk);
+    M.chunk = resolve_chunk(F, field, K, chunk, repack);
+    M.repack = M.chunk ? repack : qpk::kRepackRedq;
     check(qpk::launch_gfq_matmul(M, at, bt, m, n, kp, mp, np, reps ? nullptr : static_cast<uint8_t*>(C),
                                  reps ? static_cast<uint32_t*>(C) : nullptr, s),
           "gfq_matmul launch");
 }
 
 void gfq_matmul_host(DeviceFieldCache& F, const GfqField& field, const void* A, const void* B, u64 m, u64 K, u64 n,
-                     uint32_t chunk, void* C, bool reps) {
+                     uint32_t chunk, void* C, bool reps, uint32_t repack) {
     std::lock_guard<std::mutex> lock(F.mu);
     const u64 es = reps ? 4 : field.k();
     auto* da = F.io_a.ensure(m * K * es);
@@ -630,7 +638,7 @@ void gfq_matmul_host(DeviceFieldCache& F, const GfqField& field, const void* A, 
     auto* dc = F.io_c.ensure(m * n * es);
     check(cudaMemcpy(da, A, m * K * es, cudaMemcpyHostToDevice), "H2D");
     check(cudaMemcpy(db, B, K * n * es, cudaMemcpyHostToDevice), "H2D");
-    gfq_matmul_device(F, field, da, db, m, K, n, chunk, dc, reps, 0);
+    gfq_matmul_device(F, field, da, db, m, K, n, chunk, dc, reps, 0, repack);
     check(cudaMemcpy(C, dc, m * n * es, cudaMemcpyDeviceToHost), "D2H");
 }
 
@@ -709,11 +717,12 @@ GfqElt fgdp_dot(std::span<const GfqElt> v1, std::span<const GfqElt> v2, const Gf
 
 void gfq_matmul_coeffs(std::span<const std::uint8_t> A, std::span<const std::uint8_t> B, std::size_t m, std::size_t K,
                        std::size_t n, const GfqField& field, std::span<std::uint8_t> C, std::uint32_t chunk,
-                       CostReport* cost) {
+                       CostReport* cost, Repack repack) {
     const u64 k = field.k();
     if (A.size() != m * K * k || B.size() != K * n * k || C.size() < m * n * k)
         throw std::invalid_argument("gfq_matmul_coeffs: span sizes do not match m x K x k / K x n x k / m x n x k");
-    gfq_matmul_host(detail::device_field(field), field, A.data(), B.data(), m, K, n, chunk, C.data(), false);
+    gfq_matmul_host(detail::device_field(field), field, A.data(), B.data(), m, K, n, chunk, C.data(), false,
+                    static_cast<std::uint32_t>(repack));
     if (cost) *cost += matmul_cost(field, m, K, n);
 }
 

@@ -44,11 +44,13 @@ void gfq_mul_device(detail::DeviceFieldCache& F, const uint8_t* a, const uint8_t
 void gfq_mul_host(detail::DeviceFieldCache& F, const uint8_t* a, const uint8_t* b, u64 n, uint8_t* out, int path);
 void gfq_mul_rep_host(detail::DeviceFieldCache& F, const uint32_t* a, const uint32_t* b, u64 n, uint32_t* out);
 
-uint32_t resolve_chunk(const detail::DeviceFieldCache& F, const GfqField& field, u64 K, uint32_t chunk);
+// repack: qpk::kRepackRedq (canonical REDQ re-pack) or qpk::kRepackFold
+uint32_t resolve_chunk(const detail::DeviceFieldCache& F, const GfqField& field, u64 K, uint32_t chunk,
+                       uint32_t repack = 0);
 void gfq_matmul_device(detail::DeviceFieldCache& F, const GfqField& field, const void* A, const void* B, u64 m, u64 K,
-                       u64 n, uint32_t chunk, void* C, bool reps, cudaStream_t s);
+                       u64 n, uint32_t chunk, void* C, bool reps, cudaStream_t s, uint32_t repack = 0);
 void gfq_matmul_host(detail::DeviceFieldCache& F, const GfqField& field, const void* A, const void* B, u64 m, u64 K,
-                     u64 n, uint32_t chunk, void* C, bool reps);
+                     u64 n, uint32_t chunk, void* C, bool reps, uint32_t repack = 0);
 CostReport matmul_cost(const GfqField& field, u64 m, u64 K, u64 n);
 
 void gfq_gemv_device(detail::DeviceFieldCache& F, const GfqField& field, const uint32_t* A, const uint32_t* x, u64 m,

@@ -74,10 +74,21 @@ struct GfqElemParams {
 };
 
 // GF(p^k) matrix product (configs 4/5).
+constexpr uint32_t kRepackRedq = 0, kRepackFold = 1;
+
+// Post-re-pack digit bound of the lane fold for q = 2^B (gfq_matmul.cuh
+// repack_fold3): S = the even split kFoldShift<B>, bound (2^S-1) + (2^(B-S)-1).
+inline uint32_t fold_digit_bound(uint32_t B) {
+    uint32_t S = (B + 2) / 2;
+    if (S % 2) ++S;
+    return ((1u << S) - 1) + ((1u << (B - S)) - 1);
+}
+
 struct GfqMatmulParams {
     RedqParams rq;        // d = 2k-2, digits of one accumulated word
     uint32_t k, p, order, group, lh_radix;
     uint32_t chunk;       // delayed REDQ re-pack every `chunk` K-steps (0 = never)
+    uint32_t repack;      // kRepackRedq (canonical mu_i) or kRepackFold (lane fold, p = 3, q = 2^(2m))
     double qd;
     const uint32_t* lc;   // as GfqElemParams
     const uint32_t* hc;

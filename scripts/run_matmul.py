@@ -12,6 +12,7 @@ ap.add_argument("--cid", type=int, default=5)
 ap.add_argument("--n", type=int, default=0)
 ap.add_argument("--chunk", type=int, default=-1)
 ap.add_argument("--reps", type=int, default=3)
+ap.add_argument("--repack", default="redq")
 a = ap.parse_args()
 cfg = Q.CONFIGS[a.cid]
 n = a.n or cfg.n
@@ -26,8 +27,8 @@ Cm = torch.empty((n, n, k), dtype=torch.uint8, device="cuda")
 for _ in range(a.reps):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    f.matmul(A, B, n, n, n, chunk, out=Cm)
+    f.matmul(A, B, n, n, n, chunk, out=Cm, repack=a.repack)
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
-    print(f"n={n} k={k} chunk={chunk}: {ms:.3f} ms  {2 * n ** 3 / ms / 1e9:.2f} TFLOP/s")
+    print(f"n={n} k={k} chunk={chunk} repack={a.repack}: {ms:.3f} ms  {2 * n ** 3 / ms / 1e9:.2f} TFLOP/s")
