@@ -5,7 +5,10 @@
 //  * TMA bulk-copy (cp.async.bulk) + mbarrier wrappers, inline PTX
 #pragma once
 
+#include <cuda_runtime.h>
+
 #include <cstdint>
+#include <utility>
 
 namespace qpk {
 
@@ -122,5 +125,31 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 
 // ------------------------------------------------------------------- misc
 __device__ __forceinline__ uint32_t byte_of(uint32_t w, int i) { return (w >> (8 * i)) & 0xffu; }
+
+// Programmatic dependent launch (kernels launched with launch_pdl below):
+// pdl_launch lets the next kernel on the stream be scheduled as this grid's
+// CTAs retire; pdl_wait blocks until every prerequisite grid has completed
+// and its memory is visible.  A PDL kernel touches no data buffer before
+// pdl_wait (only constant plan tables uploaded before its predecessor ran).
+__device__ __forceinline__ void pdl_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+// host: launch with programmatic stream serialization (the kernel's prologue
+// overlaps the previous kernel's tail; its data accesses follow pdl_wait)
+template <class... KArgs, class... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 }  // namespace qpk

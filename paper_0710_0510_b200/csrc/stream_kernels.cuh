@@ -585,11 +585,16 @@ __global__ void __launch_bounds__(kThreads) stream_tma_kernel(const Op op, const
         if constexpr (G::B1 > 0) bulk_g2s_stream(dst + G::B0, in1 + tile * G::B1, G::B1, &bars[s], policy);
     };
     // thread 0 puts the first S tiles in flight before the table staging,
-    // so the per-CTA table copy overlaps the first loads
+    // so the per-CTA table copy overlaps the first loads; barrier setup runs
+    // before pdl_wait, overlapping the previous kernel's tail
+    pdl_launch();
     if (tid == 0) {
         for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
         fence_mbar_init();
         policy = policy_evict_first();
+    }
+    pdl_wait();
+    if (tid == 0) {
         for (int s = 0; s < S; ++s) {
             const uint64_t t = blockIdx.x + uint64_t(s) * gridDim.x;
             if (t < n_tiles) issue(s, t);
@@ -684,6 +689,8 @@ __global__ void __launch_bounds__(kThreads) stream_direct_kernel(const Op op, co
     extern __shared__ __align__(128) uint8_t smem[];
     uint32_t* s_tab = reinterpret_cast<uint32_t*>(smem);
     // first loads before the table staging, so both overlap
+    pdl_launch();
+    pdl_wait();
     uint64_t run = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     uint32_t a[G::W0 > 0 ? G::W0 : 1], b[G::W1 > 0 ? G::W1 : 1];
     if (run < n_runs) {
@@ -716,7 +723,9 @@ __global__ void __launch_bounds__(kThreads) stream_tail_kernel(const Op op, cons
     using G = Geometry<Op>;
     extern __shared__ __align__(128) uint8_t smem[];
     uint32_t* s_tab = reinterpret_cast<uint32_t*>(smem);
+    pdl_launch();
     stage_tables(op, s_tab);
+    pdl_wait();
     __syncthreads();
     const uint32_t tab = smem_addr(s_tab);
     uint32_t err = 0;
@@ -754,9 +763,8 @@ cudaError_t run_tail(const Op& op, const uint8_t* in0, const uint8_t* in1, uint8
     }
     const uint64_t groups = (n - first + G::R - 1) / G::R;
     const uint64_t grid = std::min<uint64_t>((groups + kThreads - 1) / kThreads, uint64_t(num_sms()) * 8);
-    stream_tail_kernel<Op><<<static_cast<unsigned>(grid), kThreads, tab_bytes, s>>>(op, in0, in1, out, first, n,
-                                                                                    status);
-    return cudaGetLastError();
+    return launch_pdl(stream_tail_kernel<Op>, dim3(static_cast<unsigned>(grid)), dim3(kThreads), tab_bytes, s, op, in0,
+                      in1, out, first, n, status);
 }
 
 template <class Op>
@@ -780,9 +788,10 @@ cudaError_t run_stream(const Op& op, const uint8_t* in0, const uint8_t* in1, uin
             attr_direct = true;
         }
         const uint64_t grid = std::min<uint64_t>((n_runs + kThreads - 1) / kThreads, uint64_t(sms) * 16);
-        stream_direct_kernel<Op><<<static_cast<unsigned>(grid), kThreads, tab_bytes, s>>>(op, in0, in1, out, n_runs,
-                                                                                          status);
-        if (cudaError_t e = cudaGetLastError(); e != cudaSuccess) return e;
+        if (cudaError_t e = launch_pdl(stream_direct_kernel<Op>, dim3(static_cast<unsigned>(grid)), dim3(kThreads),
+                                       tab_bytes, s, op, in0, in1, out, n_runs, status);
+            e != cudaSuccess)
+            return e;
         const uint64_t first = n_runs * G::R;
         if (first == n) return cudaSuccess;
         return run_tail(op, in0, in1, out, first, n, status, s);
@@ -809,9 +818,8 @@ cudaError_t run_stream(const Op& op, const uint8_t* in0, const uint8_t* in1, uin
             occ_per_sm = std::max(v, 1);
         }
         const uint64_t grid = std::min<uint64_t>(n_tiles, uint64_t(sms) * occ_per_sm);
-        stream_tma_kernel<Op>
-            <<<static_cast<unsigned>(grid), kThreads, smem, s>>>(op, in0, in1, out, n_tiles, status);
-        const cudaError_t e = cudaGetLastError();
+        const cudaError_t e = launch_pdl(stream_tma_kernel<Op>, dim3(static_cast<unsigned>(grid)), dim3(kThreads),
+                                         smem, s, op, in0, in1, out, n_tiles, status);
         if (e != cudaSuccess) return e;
     }
     const uint64_t first = n_tiles * G::TILE;
