@@ -32,6 +32,7 @@ CXX_FLAGS = f"-std=c++20 -O2 -fPIC -Wall -Wextra -I{CSRC} -I{ROOT}/include -I{CU
 CU_UNITS = [("stream_main.cu", None), ("gfq_matmul_main.cu", None), ("gfq_gemv.cu", None), ("fqt_conv.cu", None),
             ("probe.cu", None)]
 CU_UNITS += [("stream_inst.cu", i) for i in range(1, 9)]
+CU_UNITS += [("fqt_conv_inst.cu", nd) for nd in range(1, 16, 2)]
 CU_UNITS += [("gfq_matmul_inst.cu", (k, 0)) for k in range(1, 5)] + [("gfq_matmul_inst.cu", (k, 1)) for k in (2, 3)]
 CXX_UNITS = ["capi.cpp"] + [f"host/{f}" for f in
                             ("common.cpp", "params.cpp", "fpdiv.cpp", "dqt.cpp", "redq.cpp", "polymul.cpp",
