@@ -128,7 +128,7 @@ struct FqtSplit {
 };
 // DMMA kernel: each 1024-output tile's valid block shifts d cut into equal
 // ranges of at most kMmaCD, ~8 CTAs per SM (chunk = the range length)
-FqtSplit fqt_split_mma(uint64_t L1, uint64_t L2) {
+FqtSplit fqt_split_mma_uncached(uint64_t L1, uint64_t L2) {
     const uint64_t T = L1 + L2 - 1, tiles = (T + kMmaOut - 1) / kMmaOut;
     uint64_t total = 0, longest = 0;
     for (uint64_t x = 0; x < tiles; ++x) {
@@ -138,9 +138,38 @@ FqtSplit fqt_split_mma(uint64_t L1, uint64_t L2) {
         total += len;
         longest = std::max(longest, len);
     }
-    const uint64_t target = uint64_t(num_sms()) * 8;
-    const uint64_t cd = std::min<uint64_t>(std::max<uint64_t>((total + target - 1) / target, 32), kMmaCD);
-    return {static_cast<uint32_t>(std::max<uint64_t>((longest + cd - 1) / cd, 1)), cd};
+    // CTAs run in waves of kMmaCtasPerSm per SM over (nearly) equal shift
+    // ranges: pick cd minimising waves * (cd + per-CTA overhead) so the last
+    // wave is nearly full (a 2.06-wave split left the DMMA pipe 22% idle)
+    (void)total;
+    const uint64_t resident = uint64_t(num_sms()) * kMmaCtasPerSm;
+    uint64_t best_cd = kMmaCD;
+    double best = -1.0;
+    // (large products: many waves, the search is not worth its host time)
+    for (uint64_t cd = tiles > 4096 ? uint64_t(kMmaCD) : 16; cd <= uint64_t(kMmaCD); ++cd) {
+        uint64_t items = 0;
+        for (uint64_t x = 0; x < tiles; ++x) items += fqt_mma_tile_splits(x, L1, L2, cd);
+        const double cost = double((items + resident - 1) / resident) * double(cd + 6);
+        if (best < 0 || cost < best) {
+            best = cost;
+            best_cd = cd;
+        }
+    }
+    return {static_cast<uint32_t>(std::max<uint64_t>((longest + best_cd - 1) / best_cd, 1)), best_cd};
+}
+// the search above costs host microseconds: remember the last shapes
+FqtSplit fqt_split_mma(uint64_t L1, uint64_t L2) {
+    struct Entry {
+        uint64_t L1 = 0, L2 = 0;
+        FqtSplit sp{};
+    };
+    static thread_local Entry cache[4];
+    static thread_local unsigned next = 0;
+    for (const Entry& e : cache)
+        if (e.L1 == L1 && e.L2 == L2 && e.sp.splits) return e.sp;
+    Entry& e = cache[next++ % 4];
+    e = {L1, L2, fqt_split_mma_uncached(L1, L2)};
+    return e.sp;
 }
 FqtSplit fqt_split(uint64_t L1, uint64_t L2, uint32_t nq) {
     if (fqt_use_mma(nq)) return fqt_split_mma(L1, L2);

@@ -305,6 +305,7 @@ constexpr int kMmaWarps = 4;
 constexpr int kMmaA = kMmaWarps * 16;           // a-blocks per CTA
 constexpr int kMmaOut = kMmaA * kMmaBs;         // output chunks per CTA
 constexpr int kMmaCD = 128;                     // max block shifts per CTA
+constexpr int kMmaCtasPerSm = 4;                // resident CTAs per SM (launch bounds)
 constexpr int kMmaPLD = kMmaCD + kMmaA + 4;     // P row stride (== 4 mod 16)
 constexpr int kMmaQW = kMmaBs * kMmaCD + 31;    // Q window doubles (incl. the prefetched shift)
 static_assert(kMmaPLD % 16 == 4, "conflict-free B fragments");
@@ -332,7 +333,7 @@ __device__ __forceinline__ void dmma_f64(double& d0, double& d1, double a, doubl
 }
 
 template <int ND, int W, class K>
-__global__ void __launch_bounds__(kMmaWarps * 32) fqt_mma_kernel(const FqtParams P, const double* __restrict__ pw,
+__global__ void __launch_bounds__(kMmaWarps * 32, kMmaCtasPerSm) fqt_mma_kernel(const FqtParams P, const double* __restrict__ pw,
                                                                  uint64_t L1, const double* __restrict__ qw,
                                                                  uint64_t L2, uint64_t T, uint64_t cb,
                                                                  uint32_t* __restrict__ res) {
@@ -440,14 +441,18 @@ __global__ void __launch_bounds__(kMmaWarps * 32) fqt_mma_kernel(const FqtParams
             q += kMmaBs;
             --pp;
         };
+        // k-steps in the order 0, 2, 1, 3: consecutive DMMAs alternate
+        // accumulator sets, 8 issues between dependent ones
         auto mma = [&](int st) {
 #pragma unroll
-            for (int kt = 0; kt < 4; ++kt)
+            for (int kk = 0; kk < 4; ++kk) {
+                const int kt = (kk & 1) * 2 + (kk >> 1);
 #pragma unroll
                 for (int m = 0; m < 2; ++m)
 #pragma unroll
                     for (int j = 0; j < 2; ++j)
                         dmma_f64(acc[kt >> 1][m][j][0], acc[kt >> 1][m][j][1], af[st][m][kt], bf[st][j][kt]);
+            }
         };
         // groups of Gd shifts (16 Gd <= n_q products per output), branch-free
         // inside; the window always holds one spare shift (Qs/Ps margins)
