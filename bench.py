@@ -504,7 +504,10 @@ def measure_secondary(Q, torch, dev):
         wp = chunks * chunks / (ms * 1e-3)
         res["k6_fqt_mul"][name] = {"ms": ms, "coeff_products_per_s": n6 * n6 / (ms * 1e-3),
                                    "word_products_per_s": wp, "redq_per_s": wp / nq6,
-                                   "fp64_tflops": 2 * wp / 1e12, "frac_dfma_probe": 2 * wp / 1e12 / dfma_peak}
+                                   "fp64_tflops": 2 * wp / 1e12,
+                                   # n_q >= 16 runs on the fp64 tensor pipe (DMMA), n_q = 1 on CUDA cores
+                                   "kernel": "fqt_mma_kernel (DMMA)" if nq6 >= 16 else "fqt_conv_step_kernel (SWAR REDQ)",
+                                   "frac_fp64_probe": 2 * wp / 1e12 / (fp64_peak if nq6 >= 16 else dfma_peak)}
     # C4, C5: GF(p^k) matrix products (pack + contraction), GF ops/s = 2 n^3 / t
     for cfg in (Q.C4, Q.C5):
         nn, k = cfg.n, cfg.k
