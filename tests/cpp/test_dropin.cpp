@@ -190,6 +190,27 @@ static void gpu_tests() {
     CHECK(mm);
     CHECK(mc.mul_add == n * n * K && mc.divisions == n * n * ((K + f.params().n_q - 1) / f.params().n_q));
 
+    // coefficient-record API, both delayed re-packs (chunk 64, K > n_q): same C
+    {
+        std::vector<std::uint8_t> A(n * K * 3), B(K * n * 3), C1(n * n * 3), C2(n * n * 3);
+        for (std::size_t i = 0; i < n * K; ++i) {
+            const std::vector<u64> x = f.to_coeffs(a.data[i]), y = f.to_coeffs(b.data[i]);
+            for (int t = 0; t < 3; ++t) A[i * 3 + t] = static_cast<std::uint8_t>(x[t]), B[i * 3 + t] = static_cast<std::uint8_t>(y[t]);
+        }
+        gpu::gfq_matmul_coeffs(A, B, n, K, n, f, C1, 64, nullptr, gpu::Repack::redq);
+        gpu::gfq_matmul_coeffs(A, B, n, K, n, f, C2, 64, nullptr, gpu::Repack::fold);
+        bool same_c = C1 == C2;
+        for (std::size_t i = 0; i < n * n; ++i) {
+            const std::vector<u64> want = f.to_coeffs(c.data[i]);
+            for (int t = 0; t < 3; ++t) same_c &= C1[i * 3 + t] == want[t];
+        }
+        CHECK(same_c);
+        GfqField f9 = GfqField::build(3, 2, 64);
+        std::vector<std::uint8_t> A9(4 * 8 * 2), C9(4 * 4 * 2);
+        CHECK(throws<std::invalid_argument>(
+            [&] { gpu::gfq_matmul_coeffs(A9, A9, 4, 8, 4, f9, C9, 0, nullptr, gpu::Repack::fold); }));
+    }
+
     // elementwise GF products, both device paths == fgdp_dot on one pair
     GfqField f343 = GfqField::build(7, 3, 256);
     const std::size_t m = 5000;
