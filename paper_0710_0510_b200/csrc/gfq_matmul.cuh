@@ -80,7 +80,7 @@ __device__ __forceinline__ double redq_repack(const K& c, double r) {
     }
 }
 
-// Biased accumulators (the fold re-pack): the accumulator holds 2^52 + r,
+// Biased accumulators (the SWAR re-packs): the accumulator holds 2^52 + r,
 // an integer in [2^52, 2^53) where fp64 is exact with ulp 1, so its 52
 // mantissa bits are r itself -- the re-pack reads and writes r as bits with
 // no fp64 <-> integer conversions.  Words stay below 2^52 (mm_plan_safe).
@@ -103,21 +103,41 @@ __host__ __device__ constexpr uint64_t lane_ones() {
 //    V = u_i + 8 - u_{i+1} in [6, 10] and g = [V >= 8], mu_i = V - 5 - 3g
 //    (every lane stays non-negative, so no borrow crosses lanes);
 //  * the mu lanes already sit at q^i: the re-packed word, no assembly.
-// rop = floor(r/3) is still the one premultiplied fp64 floor of Lemma 1.
-// (Plain accumulators: the biased form of the fold below measured 2% slower
-// here -- r is needed as a double for the floor anyway.)
+// rop = floor(r/3) is exact integer arithmetic on the 32-bit halves of r
+// (div3_u64), and r itself is the mantissa of the 2^52-biased accumulator:
+// the re-pack issues no fp64 instruction.  (The Lemma-1 fp64 floor measured
+// 42.6 ms for C5 against 40.1 ms here: its DMUL/DADD compete with the
+// sibling warp's DMMA stream for the fp64 pipe.)
+// floor(r/3) from the halves r = rh 2^32 + rl: with rh = 3 qh + mh and
+// rl = 3 ql + rr, floor(r/3) = qh 2^32 + mh (2^32-1)/3 + ql + [mh + rr >= 3]
+// (2^32 == 1 mod 3; the low part stays below 2^32).
+__host__ __device__ __forceinline__ uint64_t div3_u64(uint64_t r) {
+    const uint32_t rh = static_cast<uint32_t>(r >> 32), rl = static_cast<uint32_t>(r);
+#ifdef __CUDA_ARCH__
+    const uint32_t qh = __umulhi(rh, 0xAAAAAAABu) >> 1, ql = __umulhi(rl, 0xAAAAAAABu) >> 1;
+#else
+    const uint32_t qh = static_cast<uint32_t>((uint64_t(rh) * 0xAAAAAAABu) >> 33);
+    const uint32_t ql = static_cast<uint32_t>((uint64_t(rl) * 0xAAAAAAABu) >> 33);
+#endif
+    const uint32_t mh = rh - 3 * qh, rr = rl - 3 * ql;
+    const uint32_t lo = mh * 0x55555555u + ql + ((mh + rr + 1) >> 2);
+    return (uint64_t(qh) << 32) | lo;
+}
+
+// (Computing floor(r/3) by the fp64 floor for half of the accumulators and
+// by div3_u64 for the other half measured 43.7 ms: worse than either.)
 template <int ND, uint32_t B>
-__device__ __forceinline__ double redq_repack_swar3(const RedqParams& P, double r) {
+__device__ __forceinline__ double redq_repack_swar3(double acc) {
     static_assert(B % 2 == 0 && B >= 4 && B * (ND - 1) + 3 <= 52, "lanes of >= 4 bits below 2^52");
     constexpr uint64_t M1 = lane_ones<ND, B>();
     constexpr uint64_t M3 = 3 * M1;
-    const uint64_t rb = dbits(r + kTwo52);                          // low 52 bits = r
-    const uint64_t ob = dbits(__dadd_rz(__dmul_ru(r, P.inv_p), kTwo52));  // low 52 bits = floor(r/3)
+    const uint64_t rb = dbits(acc) & ((uint64_t(1) << 52) - 1);  // acc = 2^52 + r: mantissa = r
+    const uint64_t ob = div3_u64(rb);                               // floor(r/3)
     const uint64_t u = ((rb & M3) + (ob & M3)) & M3;                // lane i = u_i
     const uint64_t v = u + 8 * M1 - (u >> B);                       // u_i + 8 - u_{i+1}
     const uint64_t g = (v >> 3) & M1;                               // [u_i >= u_{i+1}]
     const uint64_t mu = v - 5 * M1 - 3 * g;                         // (u_i - u_{i+1}) mod 3
-    return __longlong_as_double(static_cast<long long>(mu | kBiasBits)) - kTwo52;
+    return __longlong_as_double(static_cast<long long>(mu | kBiasBits));  // 2^52 + sum mu_i q^i
 }
 
 // Lane fold (repack mode QPK_REPACK_FOLD), p = 3 and q = 2^B: every digit
@@ -152,10 +172,10 @@ struct is_swar3<CtConst<3, QB>> {
     static constexpr bool value = (QB % 2 == 0) && QB >= 4;
 };
 
-// accumulators carry the 2^52 bias exactly when the fold re-packs them
+// accumulators carry the 2^52 bias exactly on the SWAR re-pack fast paths
 template <class K, bool FOLD>
 struct mm_biased {
-    static constexpr bool value = is_swar3<K>::value && FOLD;
+    static constexpr bool value = is_swar3<K>::value;  // both SWAR re-packs run on biased words
 };
 
 template <int ND, class K, bool FOLD>
@@ -164,7 +184,7 @@ __device__ __forceinline__ double repack_one(const K& c, double r) {
         if constexpr (FOLD)
             return repack_fold3<ND, K::kQbits, kFoldShift<K::kQbits>>(r);
         else
-            return redq_repack_swar3<ND, K::kQbits>(c.P, r);
+            return redq_repack_swar3<ND, K::kQbits>(r);
     } else {
         static_assert(!FOLD, "the lane fold is compiled for p = 3, q = 2^(2m) only");
         return redq_repack<ND>(c, r);
