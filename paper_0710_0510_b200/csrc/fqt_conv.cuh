@@ -333,10 +333,9 @@ __device__ __forceinline__ void dmma_f64(double& d0, double& d1, double a, doubl
 }
 
 template <int ND, int W, class K>
-__global__ void __launch_bounds__(kMmaWarps * 32, kMmaCtasPerSm) fqt_mma_kernel(const FqtParams P, const double* __restrict__ pw,
-                                                                 uint64_t L1, const double* __restrict__ qw,
-                                                                 uint64_t L2, uint64_t T, uint64_t cb,
-                                                                 uint32_t* __restrict__ res) {
+__global__ void __launch_bounds__(kMmaWarps * 32, kMmaCtasPerSm)
+    fqt_mma_kernel(const FqtParams P, const double* __restrict__ pw, uint64_t L1, const double* __restrict__ qw,
+                   uint64_t L2, uint64_t T, uint64_t cd, uint32_t* __restrict__ res) {
     constexpr int NW = (ND + 3) / 4;
     extern __shared__ __align__(16) uint8_t fq_smem[];
     double* Ps = reinterpret_cast<double*>(fq_smem);     // [16][kMmaPLD]
@@ -357,8 +356,8 @@ __global__ void __launch_bounds__(kMmaWarps * 32, kMmaCtasPerSm) fqt_mma_kernel(
     const int64_t A0 = int64_t(blockIdx.x) * kMmaA;
     int64_t dmin, dmax;
     fqt_mma_tile_shifts(blockIdx.x, L1, L2, dmin, dmax);
-    const int64_t d_lo = dmin + int64_t(blockIdx.y) * int64_t(cb);
-    const int64_t d_hi = std::min<int64_t>(dmax + 1, d_lo + int64_t(cb));
+    const int64_t d_lo = dmin + int64_t(blockIdx.y) * int64_t(cd);
+    const int64_t d_hi = std::min<int64_t>(dmax + 1, d_lo + int64_t(cd));
     const int64_t nd = d_hi > d_lo ? d_hi - d_lo : 0;
     const int64_t Pbase = A0 - d_hi;            // P column 0 is block Pbase (one spare column for the prefetch)
     const int64_t qbase = kMmaBs * d_lo - 15;   // Qs[x] = qw[qbase + x]
@@ -526,7 +525,7 @@ cudaError_t run_conv_k(const FqtParams& P, const double* pw, uint64_t L1, const 
 
 template <int ND, int W, class K>
 cudaError_t run_conv_mma(const FqtParams& P, const double* pw, uint64_t L1, const double* qw, uint64_t L2,
-                         uint64_t T, uint32_t splits, uint64_t cb, uint32_t* res, cudaStream_t s) {
+                         uint64_t T, uint32_t splits, uint64_t cd, uint32_t* res, cudaStream_t s) {
     const dim3 grid(static_cast<unsigned>((T + kMmaOut - 1) / kMmaOut), splits);
     const size_t smem = (size_t(kMmaBs) * kMmaPLD + kMmaQW) * 8 + (W > 0 ? size_t(P.rq.n_entries) * 4 : 0);
     if (smem > 200 * 1024) return cudaErrorInvalidValue;
@@ -538,7 +537,7 @@ cudaError_t run_conv_mma(const FqtParams& P, const double* pw, uint64_t L1, cons
             return e;
         cur = smem;
     }
-    return launch_pdl(fqt_mma_kernel<ND, W, K>, grid, dim3(kMmaWarps * 32), smem, s, P, pw, L1, qw, L2, T, cb, res);
+    return launch_pdl(fqt_mma_kernel<ND, W, K>, grid, dim3(kMmaWarps * 32), smem, s, P, pw, L1, qw, L2, T, cd, res);
 }
 
 template <int ND, int W, class K, int SWAR_B = 0>
