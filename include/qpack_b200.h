@@ -93,6 +93,11 @@ typedef struct qpk_polymul_plan_s* qpk_polymul_plan;
 /* params (p, q, k, n_q, m=53) checked as dqt_mul_poly / fqt_mul do
  *                                            dqt.cpp:81-83, polymul.cpp:81-89 */
 QPK_API qpk_status qpk_polymul_plan_create(uint64_t p, uint64_t q, uint32_t k, uint32_t n_q, qpk_polymul_plan* out);
+/* as above with the word width m (QadicParams::m, params.hpp:23-31): m > 53
+ * selects integer (u128) words for qpk_fqt_mul -- the reference's integer
+ * mode; the batched qpk_polymul_batch needs q^(2k-1) <= 2^53 */
+QPK_API qpk_status qpk_polymul_plan_create_m(uint64_t p, uint64_t q, uint32_t k, uint32_t n_q, uint32_t m,
+                                             qpk_polymul_plan* out);
 QPK_API void qpk_polymul_plan_destroy(qpk_polymul_plan plan);
 /* n pairs of k-coefficient records -> n records of 2k-1 residues
  * = fqt_mul(a_i, b_i, k-1, params, fqt_reduction_plan)   polymul.hpp:42-47

@@ -80,6 +80,7 @@ def oracle():
             _sig(lib, "qo_redq_trace", I, [U64, U64, U32, U64, U64, PU64, PU64, u64p, u64p])
             _sig(lib, "qo_polymul_batch", I, [U64, U32, u8p, u8p, U64, u8p])
             _sig(lib, "qo_fqt_mul", I, [U64, U32, U64, U32, u64p, U64, u64p, U64, u64p, u64p])
+            _sig(lib, "qo_fqt_mul_m", I, [U64, U32, U64, U32, U32, u64p, U64, u64p, U64, u64p, u64p])
             _sig(lib, "qo_field_build", VP, [U64, U32, U64, I])
             _sig(lib, "qo_field_free", None, [VP])
             _sig(lib, "qo_field_mul", U32, [VP, U32, U32])
@@ -117,6 +118,7 @@ def ref():
             _sig(lib, "ref_redq_trace", I, [U64, U64, U32, U64, U64, PU64, PU64, u64p, u64p, PU64, PU64])
             _sig(lib, "ref_polymul_batch", I, [U64, U32, u8p, u8p, U64, u8p, I, I, PU64, u64p])
             _sig(lib, "ref_fqt_mul", I, [U64, U32, U64, U32, u64p, U64, u64p, U64, u64p, u64p])
+            _sig(lib, "ref_fqt_mul_m", I, [U64, U32, U64, U32, U32, u64p, U64, u64p, U64, u64p, u64p])
             _sig(lib, "ref_field_build", VP, [U64, U32, U64, I])
             _sig(lib, "ref_field_free", None, [VP])
             _sig(lib, "ref_field_info", I, [VP, u64p, u64p, PU32, PU64, C.c_char_p, U64])
@@ -178,13 +180,13 @@ def polymul_batch(p, d, a, b):
     return out
 
 
-def fqt_mul(p, d, q, n_q, a, b):
+def fqt_mul(p, d, q, n_q, a, b, m=53):
     a = np.ascontiguousarray(a, np.uint64)
     b = np.ascontiguousarray(b, np.uint64)
     out = np.zeros(max(a.size + b.size - 1, 1), np.uint64)
     cost = np.zeros(4, np.uint64)
     lib = oracle()
-    _chk(lib, lib.qo_fqt_mul(p, d, q, n_q, a, a.size, b, b.size, out, cost))
+    _chk(lib, lib.qo_fqt_mul_m(p, d, q, n_q, m, a, a.size, b, b.size, out, cost))
     return out[: a.size + b.size - 1] if a.size and b.size else out[:0], cost
 
 

@@ -434,7 +434,13 @@ static u128 pack_digits(const u64* c, u32 n, u64 q) {
  * fqt_reduction_plan (polymul.cpp:67-74: integer mode, windowed table when
  * p does not divide q), overlap-add of the residues mod p. */
 int qo_fqt_mul(u64 p, u32 d, u64 q, u32 n_q, const u64* a, u64 la, const u64* b, u64 lb, u64* out, u64* cost) {
-    if (qo_validate(p, q, d + 1, n_q, 53) != 0) return err(QO_INVALID_ARGUMENT, "fqt_mul: invalid params");
+    return qo_fqt_mul_m(p, d, q, n_q, 53, a, la, b, lb, out, cost);
+}
+
+/* fqt_mul with word width m (u128 words up to m = 128, polymul.cpp u128 MAC) */
+int qo_fqt_mul_m(u64 p, u32 d, u64 q, u32 n_q, u32 m, const u64* a, u64 la, const u64* b, u64 lb, u64* out,
+                 u64* cost) {
+    if (qo_validate(p, q, d + 1, n_q, m) != 0) return err(QO_INVALID_ARGUMENT, "fqt_mul: invalid params");
     if (la == 0 || lb == 0) return QO_OK;
     qo_redq_plan pl;
     int rc = qo_redq_plan_build(p, q, 2 * d, 0, &pl);

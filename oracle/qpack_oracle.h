@@ -86,6 +86,9 @@ int qo_redq_run_u64(uint64_t p, uint64_t q, uint32_t d, int float_mode, uint32_t
 int qo_polymul_batch(uint64_t p, uint32_t d, const uint8_t* a, const uint8_t* b, uint64_t n, uint8_t* out);
 int qo_fqt_mul(uint64_t p, uint32_t d, uint64_t q, uint32_t n_q, const uint64_t* a, uint64_t la,
                const uint64_t* b, uint64_t lb, uint64_t* out, uint64_t* cost);
+/* the same with the word width m (u128 words up to m = 128) */
+int qo_fqt_mul_m(uint64_t p, uint32_t d, uint64_t q, uint32_t n_q, uint32_t m, const uint64_t* a, uint64_t la,
+                 const uint64_t* b, uint64_t lb, uint64_t* out, uint64_t* cost);
 
 /* ---- GF(p^k) (gfq.cpp) ---- */
 typedef struct {

@@ -277,10 +277,19 @@ int ref_polymul_batch(uint64_t p, uint32_t d, const uint8_t* a, const uint8_t* b
 }
 
 // General fqt_mul on one pair of polynomials (any length), for chunked-FQT parity.
+int ref_fqt_mul_m(uint64_t p, uint32_t d, uint64_t q, uint32_t n_q, uint32_t m, const uint64_t* a, uint64_t la,
+                  const uint64_t* b, uint64_t lb, uint64_t* out, uint64_t* cost);
+
 int ref_fqt_mul(uint64_t p, uint32_t d, uint64_t q, uint32_t n_q, const uint64_t* a, uint64_t la,
                 const uint64_t* b, uint64_t lb, uint64_t* out, uint64_t* cost) {
+    return ref_fqt_mul_m(p, d, q, n_q, 53, a, la, b, lb, out, cost);
+}
+
+// fqt_mul with word width m (the reference's u128 words up to m = 128)
+int ref_fqt_mul_m(uint64_t p, uint32_t d, uint64_t q, uint32_t n_q, uint32_t m, const uint64_t* a, uint64_t la,
+                  const uint64_t* b, uint64_t lb, uint64_t* out, uint64_t* cost) {
     try {
-        QadicParams params{p, q, d + 1, n_q, 53};
+        QadicParams params{p, q, d + 1, n_q, m};
         DensePoly pa{p, std::vector<u64>(a, a + la)}, pb{p, std::vector<u64>(b, b + lb)};
         CostReport c;
         DensePoly r = fqt_mul(pa, pb, d, params, &c);

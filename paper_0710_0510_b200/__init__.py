@@ -102,6 +102,7 @@ SIGNATURES = {
     "qpk_redq_sync": (I, [VP, VP]),
     "qpk_redq_cost": (I, [VP, U64, PCost]),
     "qpk_polymul_plan_create": (I, [U64, U64, U32, U32, C.POINTER(VP)]),
+    "qpk_polymul_plan_create_m": (I, [U64, U64, U32, U32, U32, C.POINTER(VP)]),
     "qpk_polymul_plan_destroy": (None, [VP]),
     "qpk_polymul_batch": (I, [VP, VP, VP, U64, VP, VP]),
     "qpk_polymul_batch_host": (I, [VP, VP, VP, U64, VP, PCost]),
@@ -257,10 +258,11 @@ class RedqPlan:
 class PolymulPlan:
     """Batched dqt_mul_poly / single-chunk fqt_mul (dqt.hpp:46, polymul.hpp:42)."""
 
-    def __init__(self, p, q, k, n_q=1):
+    def __init__(self, p, q, k, n_q=1, m=53):
+        """m > 53: integer (u128) words for fqt_mul, the reference's integer mode."""
         h = VP()
-        _check(lib().qpk_polymul_plan_create(p, q, k, n_q, C.byref(h)))
-        self._h, self.p, self.q, self.k = h, p, q, k
+        _check(lib().qpk_polymul_plan_create_m(p, q, k, n_q, m, C.byref(h)))
+        self._h, self.p, self.q, self.k, self.m = h, p, q, k, m
 
     def __del__(self):
         if getattr(self, "_h", None) and _lib is not None:

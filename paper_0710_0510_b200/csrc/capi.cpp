@@ -189,6 +189,16 @@ qpk_status qpk_polymul_plan_create(uint64_t p, uint64_t q, uint32_t k, uint32_t 
     });
 }
 
+qpk_status qpk_polymul_plan_create_m(uint64_t p, uint64_t q, uint32_t k, uint32_t n_q, uint32_t m,
+                                     qpk_polymul_plan* out) {
+    return guard([&] {
+        need(out != nullptr, "null output handle");
+        auto h = std::make_unique<qpk_polymul_plan_s>();
+        h->pl = std::make_unique<qpack::gpu::PolymulPlan>(qpack::QadicParams{p, q, k, n_q, m});
+        *out = h.release();
+    });
+}
+
 void qpk_polymul_plan_destroy(qpk_polymul_plan plan) { delete plan; }
 
 qpk_status qpk_fqt_mul(qpk_polymul_plan plan, const uint8_t* a, uint64_t na, const uint8_t* b, uint64_t nb,

@@ -112,6 +112,85 @@ __global__ void fqt_pack2_kernel(uint32_t p, uint32_t k, double qd, const uint8_
     }
 }
 
+// ---- wide words (m > 53): u128 packed words, one thread per output chunk ----
+using u128d = unsigned __int128;
+
+struct FqtWideParams {
+    uint32_t p, k, nq, nd, neg_q, qbits;  // qbits: log2 q when q is a power of two, else 0
+    uint64_t q;
+    u128d qpow[15];                       // q^i, i < nd
+};
+
+__global__ void fqt_wide_pack_kernel(uint32_t p, uint32_t k, uint64_t q, const uint8_t* __restrict__ a, uint64_t na,
+                                     uint64_t L1, u128d* __restrict__ wa, const uint8_t* __restrict__ b, uint64_t nb,
+                                     uint64_t L2, u128d* __restrict__ wb) {
+    pdl_launch();
+    pdl_wait();
+    for (uint64_t x = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; x < L1 + L2;
+         x += uint64_t(gridDim.x) * blockDim.x) {
+        const bool first = x < L1;
+        const uint64_t c = first ? x : x - L1, n = first ? na : nb;
+        const uint8_t* src = first ? a : b;
+        u128d v = 0;  // Horner (pack, dqt.cpp:23-37)
+        for (int j = static_cast<int>(k) - 1; j >= 0; --j) {
+            const uint64_t i = c * k + j;
+            v = v * q + (i < n ? src[i] % p : 0u);
+        }
+        (first ? wa : wb)[c] = v;
+    }
+}
+
+// integer-mode REDQ of one group sum (redq.cpp:44-58): rop = r / p,
+// u_i = r / q^i - p (rop / q^i), then mu_d = u_d, mu_i = (u_i + neg_q u_{i+1})
+// mod p (redq.cpp:63-65); the residues are added mod p into byte lanes
+__device__ __forceinline__ void fqt_wide_close(const FqtWideParams& P, u128d r, uint32_t (&racc)[4]) {
+    const u128d rop = r / P.p;
+    uint32_t u[15];
+    for (uint32_t i = 0; i < P.nd; ++i) {
+        u128d x, y;
+        if (P.qbits) {
+            x = r >> (P.qbits * i);
+            y = rop >> (P.qbits * i);
+        } else {
+            x = r / P.qpow[i];
+            y = rop / P.qpow[i];
+        }
+        u[i] = static_cast<uint32_t>(static_cast<uint64_t>(x) - P.p * static_cast<uint64_t>(y));
+    }
+    for (uint32_t i = 0; i < P.nd; ++i) {
+        const uint32_t mu = i + 1 < P.nd ? (u[i] + P.neg_q * u[i + 1]) % P.p : u[i];
+        const uint32_t w = i / 4, sh = 8 * (i % 4);
+        uint32_t lane = ((racc[w] >> sh) & 0xffu) + mu;
+        if (lane >= P.p) lane -= P.p;
+        racc[w] = (racc[w] & ~(0xffu << sh)) | (lane << sh);
+    }
+}
+
+// output chunk t = sum_i pw[i] qw[t-i] in u128, a REDQ every n_q products
+__global__ void __launch_bounds__(256) fqt_wide_conv_kernel(const FqtWideParams P, const u128d* __restrict__ pw,
+                                                            uint64_t L1, const u128d* __restrict__ qw, uint64_t L2,
+                                                            uint64_t T, uint32_t* __restrict__ res) {
+    pdl_launch();
+    pdl_wait();
+    const uint32_t nw = (P.nd + 3) / 4;
+    for (uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < T; t += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t lo = t + 1 > L2 ? t + 1 - L2 : 0, hi = t < L1 - 1 ? t : L1 - 1;
+        uint32_t racc[4] = {0, 0, 0, 0};
+        u128d acc = 0;
+        uint32_t cnt = 0;
+        for (uint64_t i = lo; i <= hi; ++i) {
+            acc += pw[i] * qw[t - i];  // exact: a group sum stays below q^(2k-1) < 2^m <= 2^128
+            if (++cnt == P.nq) {
+                fqt_wide_close(P, acc, racc);
+                acc = 0;
+                cnt = 0;
+            }
+        }
+        if (cnt) fqt_wide_close(P, acc, racc);
+        for (uint32_t w = 0; w < nw; ++w) res[t * nw + w] = racc[w];
+    }
+}
+
 }  // namespace
 
 
@@ -194,6 +273,49 @@ uint64_t fqt_workspace_bytes(uint32_t k, uint32_t nq, uint64_t na, uint64_t nb) 
     const uint64_t L1 = fqt_chunks(na, k), L2 = fqt_chunks(nb, k), T = L1 + L2 - 1;
     const uint32_t nd = 2 * k - 1, nw = (nd + 3) / 4;
     return align16(L1 * 8) + align16(L2 * 8) + uint64_t(fqt_split(L1, L2, nq).splits) * T * nw * 4;
+}
+
+uint64_t fqt_wide_workspace_bytes(uint32_t k, uint64_t na, uint64_t nb) {
+    const uint64_t L1 = fqt_chunks(na, k), L2 = fqt_chunks(nb, k), T = L1 + L2 - 1;
+    const uint32_t nw = (2 * k - 1 + 3) / 4;
+    return align16(L1 * 16) + align16(L2 * 16) + T * nw * 4;
+}
+
+cudaError_t launch_fqt_mul_wide(uint32_t p, uint64_t q, uint32_t k, uint32_t nq, const uint8_t* a, uint64_t na,
+                                const uint8_t* b, uint64_t nb, uint8_t* out, void* ws, cudaStream_t s) {
+    if (na == 0 || nb == 0) return cudaSuccess;
+    if (k < 1 || k > 8 || p < 2 || p > 256 || nq == 0) return cudaErrorInvalidValue;
+    FqtWideParams P{};
+    P.p = p;
+    P.k = k;
+    P.nq = nq;
+    P.nd = 2 * k - 1;
+    P.q = q;
+    P.neg_q = static_cast<uint32_t>((p - q % p) % p);
+    P.qbits = (q & (q - 1)) == 0 ? static_cast<uint32_t>(__builtin_ctzll(q)) : 0u;
+    u128d qp = 1;
+    for (uint32_t i = 0; i < P.nd; ++i, qp *= q) P.qpow[i] = qp;
+    const uint64_t L1 = fqt_chunks(na, k), L2 = fqt_chunks(nb, k), T = L1 + L2 - 1;
+    auto* base = static_cast<uint8_t*>(ws);
+    auto* pw = reinterpret_cast<u128d*>(base);
+    auto* qw = reinterpret_cast<u128d*>(base + align16(L1 * 16));
+    auto* res = reinterpret_cast<uint32_t*>(base + align16(L1 * 16) + align16(L2 * 16));
+    const int sms = num_sms();
+    if (cudaError_t e = launch_pdl(fqt_wide_pack_kernel,
+                                   dim3(static_cast<unsigned>(std::min<uint64_t>((L1 + L2 + 255) / 256, sms * 8))),
+                                   dim3(256), 0, s, p, k, q, a, na, L1, pw, b, nb, L2, qw);
+        e != cudaSuccess)
+        return e;
+    if (cudaError_t e = launch_pdl(fqt_wide_conv_kernel,
+                                   dim3(static_cast<unsigned>(std::min<uint64_t>((T + 255) / 256, sms * 16))),
+                                   dim3(256), 0, s, P, static_cast<const u128d*>(pw), L1, static_cast<const u128d*>(qw),
+                                   L2, T, res);
+        e != cudaSuccess)
+        return e;
+    const uint64_t nout = na + nb - 1, nchunks = (nout + k - 1) / k;
+    return launch_pdl(fqt_overlap_kernel, dim3(static_cast<unsigned>(std::min<uint64_t>((nchunks + 255) / 256, sms * 8))),
+                      dim3(kOvThreads), 0, s, p, k, 2 * k - 1, static_cast<const uint32_t*>(res), 1u, T, out, nout,
+                      uint64_t(0), L1, L2);
 }
 
 cudaError_t launch_fqt_mul(const FqtParams& P, const uint8_t* a, uint64_t na, const uint8_t* b, uint64_t nb,

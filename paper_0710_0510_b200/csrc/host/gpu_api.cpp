@@ -397,6 +397,11 @@ PolymulPlan::PolymulPlan(const QadicParams& pr) : params(pr) {
 void polymul_device(PolymulPlan& pl, const uint8_t* a, const uint8_t* b, u64 n, uint8_t* out, cudaStream_t s) {
     if (pl.params.k > static_cast<u32>(qpk::kMaxGfqK))
         throw std::invalid_argument("qpack-b200 polymul: the batched path packs at most k = 4 coefficients");
+    // the batched kernel multiplies packed words in fp64: exact while the
+    // product word q^(2k-1) fits 53 bits (m <= 53 guarantees it)
+    if (pl.params.m > 53 && (!pow_fits_u128(pl.params.q, 2 * pl.params.k - 1) ||
+                             checked_pow_u128(pl.params.q, 2 * pl.params.k - 1) > (u128(1) << 53)))
+        throw std::invalid_argument("qpack-b200 polymul: the batched path computes in fp64 words (q^(2k-1) <= 2^53)");
     DevicePlanCache& dp = detail::device_plan(pl.redq);
     check(qpk::launch_polymul(pl.P, a, b, n, out, dp.status.as<uint32_t>(), s), "polymul launch");
 }
@@ -432,8 +437,6 @@ void fqt_check(const RedqPlan& plan, const QadicParams& params) {
     if (params.p > 256) throw std::invalid_argument("qpack-b200 fqt_mul: coefficients are uint8, p must be <= 256");
     if (params.k < 1 || params.k > 8)
         throw std::invalid_argument("qpack-b200 fqt_mul: the device path packs 1..8 coefficients per chunk");
-    if (params.m > 53)
-        throw std::invalid_argument("qpack-b200 fqt_mul: the device path computes in fp64 words (m <= 53)");
     if (plan.p != params.p || plan.q != params.q || plan.d != 2 * (params.k - 1))
         throw std::invalid_argument("fqt_mul: reduction plan does not match the params");
 }
@@ -442,6 +445,14 @@ void fqt_mul_device(const RedqPlan& plan, const QadicParams& params, const uint8
                     u64 nb, uint8_t* out, cudaStream_t s) {
     fqt_check(plan, params);
     if (na == 0 || nb == 0) return;
+    if (params.m > 53) {
+        // integer words beyond fp64 (the reference's u128 mode): u128 kernel
+        StreamBuf ws(qpk::fqt_wide_workspace_bytes(params.k, na, nb), s);
+        check(qpk::launch_fqt_mul_wide(static_cast<uint32_t>(params.p), params.q, params.k,
+                                       static_cast<uint32_t>(std::max<u64>(params.n_q, 1)), a, na, b, nb, out, ws.ptr, s),
+              "fqt_mul (u128 words) launch");
+        return;
+    }
     DevicePlanCache& dp = detail::device_plan(plan);
     qpk::FqtParams F{};
     F.rq = dp.prm;

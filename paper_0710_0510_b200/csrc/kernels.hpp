@@ -154,6 +154,14 @@ cudaError_t launch_gfq_gemv(const GfqGemvParams& P, const uint32_t* A, const uin
                             uint32_t splits, void* ws, uint32_t* y_rep, uint8_t* y_coeff, cudaStream_t s);
 
 // K6: out (na+nb-1 coefficients) = a * b mod p, coefficients as uint8;
+// FQT product with integer words beyond fp64 (the reference's u128 mode,
+// m up to 128: polymul.cpp:97-146 with u128 MAC): packed words and group
+// sums as unsigned __int128, integer-mode REDQ per group (redq.cpp:44-58)
+// and the direct correction.  ws: fqt_wide_workspace_bytes.
+uint64_t fqt_wide_workspace_bytes(uint32_t k, uint64_t na, uint64_t nb);
+cudaError_t launch_fqt_mul_wide(uint32_t p, uint64_t q, uint32_t k, uint32_t nq, const uint8_t* a, uint64_t na,
+                                const uint8_t* b, uint64_t nb, uint8_t* out, void* ws, cudaStream_t s);
+
 // ws: fqt_workspace_bytes (packed chunks and per-chunk residue partials).
 uint64_t fqt_workspace_bytes(uint32_t k, uint32_t nq, uint64_t na, uint64_t nb);
 cudaError_t launch_fqt_mul(const FqtParams& P, const uint8_t* a, uint64_t na, const uint8_t* b, uint64_t nb,

@@ -114,10 +114,7 @@ static void host_tests() {
         }
     }
 
-    // FQT (test_polymul.cpp:42-58): u128 words (m = 128) stay on the host;
-    // fp64 words run on the device (gpu_tests)
-    CHECK((fqt_mul(DensePoly{5, {3, 2, 1}}, DensePoly{5, {1, 0, 4}}, 2, QadicParams{5, 10000, 3, 1, 128}) ==
-           DensePoly{5, {3, 2, 3, 3, 4}}));
+    // FQT: every word width runs on the device (gpu_tests)
     CHECK(packed_degree(500, 4) == 100);
 
     // GF(9) (test_gfq.cpp:23-36, 108-115)
@@ -171,6 +168,11 @@ static void gpu_tests() {
     CHECK(cost.divisions == words.size() && cost.table_accesses == 2 * words.size());
     words[5] = 1e300;
     CHECK(throws<std::domain_error>([&] { gpu::redq_residues_batch(words, plan, res); }));
+
+    // FQT with u128 words (test_polymul.cpp:42-58, m = 128): the device's
+    // integer-word kernel
+    CHECK((fqt_mul(DensePoly{5, {3, 2, 1}}, DensePoly{5, {1, 0, 4}}, 2, QadicParams{5, 10000, 3, 1, 128}) ==
+           DensePoly{5, {3, 2, 3, 3, 4}}));
 
     // GPU gfq_matmul == the triple loop of field ops (acceptance.cpp:361-374)
     GfqField f = GfqField::build(3, 3, 1024);

@@ -205,6 +205,22 @@ def test_oracle_vs_reference_fields(orc):
 
 
 @need_ref
+@pytest.mark.skipif(__import__("oracle").ref() is None, reason="oracle/_ref not built")
+def test_oracle_vs_reference_fqt_u128_words(orc):
+    # the reference's integer mode: u128 words up to m = 128 (polymul.cpp u128 MAC)
+    rng = np.random.default_rng(128)
+    for p, d, q, nq, m in [(5, 2, 10000, 1, 128), (3, 3, 1 << 16, 1000, 128), (251, 1, 1 << 40, 1000, 128),
+                           (7, 2, 10 ** 7, 5000, 128), (3, 1, 1 << 30, 7, 96), (2, 7, 1 << 8, 3, 128)]:
+        for n in (1, 10, 57):
+            a = rng.integers(0, p, n + 1).astype(np.uint64)
+            b = rng.integers(0, p, n + 3).astype(np.uint64)
+            got, cost = orc.fqt_mul(p, d, q, nq, a, b, m)
+            want = np.zeros(2 * n + 3, np.uint64)
+            rc = np.zeros(4, np.uint64)
+            assert orc.ref().ref_fqt_mul_m(p, d, q, nq, m, a, a.size, b, b.size, want, rc) == 0
+            assert (got == want).all() and cost.tolist() == rc.tolist()
+
+
 def test_oracle_vs_reference_chunked_fqt(orc):
     # acceptance.cpp:154-170 style: multi-chunk FQT products, counters too
     rng = np.random.default_rng(408)
