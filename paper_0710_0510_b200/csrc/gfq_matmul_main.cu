@@ -2,6 +2,7 @@
 // the K4 launch dispatcher; the K4 kernel templates are in gfq_matmul.cuh.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "device_common.cuh"
@@ -24,6 +25,39 @@ QPK_DECL_MM(3, 1)
 #undef QPK_DECL_MM
 
 namespace {
+
+// 32x32 shared-memory tile transpose of u32 (coalesced both ways)
+__global__ void transpose_u32_kernel(const uint32_t* __restrict__ src, uint64_t rows, uint64_t cols,
+                                     uint32_t* __restrict__ dst) {
+    __shared__ uint32_t tile[32][33];
+    const uint64_t r0 = uint64_t(blockIdx.y) * 32, c0 = uint64_t(blockIdx.x) * 32;
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    for (int i = ty; i < 32; i += 8)
+        if (r0 + i < rows && c0 + tx < cols) tile[i][tx] = src[(r0 + i) * cols + c0 + tx];
+    __syncthreads();
+    for (int i = ty; i < 32; i += 8)
+        if (c0 + i < cols && r0 + tx < rows) dst[(c0 + i) * rows + r0 + tx] = tile[tx][i];
+}
+
+// coefficient record (k bytes, reduced mod p as from_coeffs) -> rep
+// (gfq.cpp:296-314: index sum c_i p^i, then the log table)
+__global__ void coeffs_to_reps_kernel(uint32_t p, uint32_t k, const uint32_t* __restrict__ log,
+                                      const uint8_t* __restrict__ src, uint64_t n, uint32_t* __restrict__ dst) {
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
+        uint32_t idx = 0;
+        for (int j = static_cast<int>(k) - 1; j >= 0; --j) idx = idx * p + src[i * k + j] % p;
+        dst[i] = log[idx];
+    }
+}
+
+// rep -> coefficient bytes (to_coeffs; the zero sentinel maps to 0)
+__global__ void reps_to_coeffs_kernel(uint32_t k, const uint32_t* __restrict__ alog, const uint32_t* __restrict__ src,
+                                      uint64_t n, uint8_t* __restrict__ dst) {
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
+        const uint32_t w = alog[src[i]];
+        for (uint32_t j = 0; j < k; ++j) dst[i * k + j] = static_cast<uint8_t>(w >> (8 * j));
+    }
+}
 
 // ---------------------------------------------------------------- K1 packs
 // 32x32 tiles through shared memory so both the record reads and the
@@ -101,6 +135,31 @@ cudaError_t launch_gfq_matmul(const GfqMatmulParams& P, const double* at, const 
         case 4: return matmul_launch_k4_v0(P, at, b, m, n, K_pad, m_pad, n_pad, out_coeffs, out_reps, s);
         default: return cudaErrorInvalidValue;
     }
+}
+
+int num_sms();
+
+cudaError_t launch_transpose_u32(const uint32_t* src, uint64_t rows, uint64_t cols, uint32_t* dst, cudaStream_t s) {
+    if (rows == 0 || cols == 0) return cudaSuccess;
+    dim3 grid(static_cast<unsigned>((cols + 31) / 32), static_cast<unsigned>((rows + 31) / 32));
+    transpose_u32_kernel<<<grid, dim3(32, 8), 0, s>>>(src, rows, cols, dst);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_coeffs_to_reps(uint32_t p, uint32_t k, const uint32_t* log, const uint8_t* src, uint64_t n,
+                                  uint32_t* dst, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((n + 255) / 256, uint64_t(num_sms()) * 8));
+    coeffs_to_reps_kernel<<<grid, 256, 0, s>>>(p, k, log, src, n, dst);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_reps_to_coeffs(uint32_t k, const uint32_t* alog, const uint32_t* src, uint64_t n, uint8_t* dst,
+                                  cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((n + 255) / 256, uint64_t(num_sms()) * 8));
+    reps_to_coeffs_kernel<<<grid, 256, 0, s>>>(k, alog, src, n, dst);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_pack_coeffs(uint32_t p, uint32_t k, double qd, const uint8_t* src, uint64_t rows, uint64_t cols,

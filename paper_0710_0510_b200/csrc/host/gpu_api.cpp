@@ -612,9 +612,50 @@ uint32_t resolve_chunk(const DeviceFieldCache& F, const GfqField& field, u64 K, 
 }
 
 // A, B, C device pointers: coefficient records (reps when `reps`)
+// Fields whose safe group is below one fp64 MMA step (4 products, e.g.
+// GF(7^3) at q = 2^8, n_q = 2): C = A B as n GEMVs (K5, groups of n_q
+// products per lane like the reference's fgdp_dot) over B's columns,
+// through rep layouts: A as reps, B^T as reps, C^T rows, transposed back.
+void gfq_matmul_by_columns(DeviceFieldCache& F, const GfqField& field, const void* A, const void* B, u64 m, u64 K,
+                           u64 n, void* C, bool reps, cudaStream_t s) {
+    const qpk::GfqElemParams& E = F.elem;
+    StreamBuf wa(reps ? 0 : m * K * 4, s), wb(reps ? 0 : K * n * 4, s), wbt(n * K * 4, s), wct(n * m * 4, s),
+        wc(reps ? 0 : m * n * 4, s);
+    const uint32_t* ar = static_cast<const uint32_t*>(A);
+    const uint32_t* br = static_cast<const uint32_t*>(B);
+    if (!reps) {
+        check(qpk::launch_coeffs_to_reps(E.p, E.k, E.log, static_cast<const uint8_t*>(A), m * K, wa.as<uint32_t>(), s),
+              "coeffs -> reps");
+        check(qpk::launch_coeffs_to_reps(E.p, E.k, E.log, static_cast<const uint8_t*>(B), K * n, wb.as<uint32_t>(), s),
+              "coeffs -> reps");
+        ar = wa.as<uint32_t>();
+        br = wb.as<uint32_t>();
+    }
+    check(qpk::launch_transpose_u32(br, K, n, wbt.as<uint32_t>(), s), "transpose B");
+    for (u64 j = 0; j < n; ++j)
+        gfq_gemv_device(F, field, ar, wbt.as<uint32_t>() + j * K, m, K, wct.as<uint32_t>() + j * m, nullptr, s);
+    uint32_t* cr = reps ? static_cast<uint32_t*>(C) : wc.as<uint32_t>();
+    check(qpk::launch_transpose_u32(wct.as<uint32_t>(), n, m, cr, s), "transpose C");
+    if (!reps)
+        check(qpk::launch_reps_to_coeffs(E.k, E.alog, cr, m * n, static_cast<uint8_t*>(C), s), "reps -> coeffs");
+}
+
 void gfq_matmul_device(DeviceFieldCache& F, const GfqField& field, const void* A, const void* B, u64 m, u64 K, u64 n,
                        uint32_t chunk, void* C, bool reps, cudaStream_t s, uint32_t repack) {
     if (m == 0 || n == 0) return;
+    {
+        const u64 p = field.p(), unit = field.k() * (p - 1) * (p - 1), q = field.params().q;
+        const u64 safe = unit ? (q - 1 - (p - 1)) / unit : K;
+        if (K > field.params().n_q && safe < 4) {
+            if (chunk > safe)
+                throw std::invalid_argument("gfq_matmul: chunk " + std::to_string(chunk) +
+                                            " lets digit sums reach q (max " + std::to_string(safe) + ")");
+            if (repack != qpk::kRepackRedq)
+                throw std::invalid_argument("gfq_matmul: the fold re-pack is provided for GF(3^3) at q = 2^10 only");
+            gfq_matmul_by_columns(F, field, A, B, m, K, n, C, reps, s);
+            return;
+        }
+    }
     const u64 mp = round_up(m, 128), np = round_up(n, 128), kp = round_up(std::max<u64>(K, 1), 16);
     StreamBuf wa(kp * mp * 8, s), wb(kp * np * 8, s);
     auto* at = wa.as<double>();

@@ -134,6 +134,14 @@ cudaError_t launch_gfq_mul_rep(uint32_t group, const uint32_t* a, const uint32_t
 cudaError_t launch_pack_coeffs(uint32_t p, uint32_t k, double qd, const uint8_t* src, uint64_t rows,
                                uint64_t cols, double* dst, uint64_t ld, bool transpose, cudaStream_t s);
 // Zech/dlog tabulated pack (K1b): reps -> float_eval(rep) via a smem table.
+// layout helpers of the GEMV-column matmul route (fields whose n_q is below
+// one fp64 MMA step): u32 transpose, coefficient records <-> reps through
+// the field's log / antilog-to-bytes tables (GfqElemParams log, alog)
+cudaError_t launch_transpose_u32(const uint32_t* src, uint64_t rows, uint64_t cols, uint32_t* dst, cudaStream_t s);
+cudaError_t launch_coeffs_to_reps(uint32_t p, uint32_t k, const uint32_t* log, const uint8_t* src, uint64_t n,
+                                  uint32_t* dst, cudaStream_t s);
+cudaError_t launch_reps_to_coeffs(uint32_t k, const uint32_t* alog, const uint32_t* src, uint64_t n, uint8_t* dst,
+                                  cudaStream_t s);
 cudaError_t launch_pack_reps(const double* fval, uint32_t order, const uint32_t* src, uint64_t rows,
                              uint64_t cols, double* dst, uint64_t ld, bool transpose, cudaStream_t s);
 
