@@ -557,7 +557,10 @@ __device__ __forceinline__ void report(uint32_t err, uint32_t* status) {
     if (err && (threadIdx.x & 31) == 0 && status) atomicOr(status, err);
 }
 
-template <class Op>
+// ASYNC: 16-byte cp.async copies (the TMA kernel, where a CTA streams for
+// tens of microseconds); the one-pass direct/tail kernels keep the plain
+// loop (measured: cp.async cost C1's hot launch 6.31 -> 6.65 us)
+template <class Op, bool ASYNC = true>
 __device__ __forceinline__ void stage_tables(const Op& op, uint32_t* dst) {
     // 16-byte cp.async copies, every one in flight at once (a per-thread
     // load/store loop serialises one L2 round trip per 256 words: measured
@@ -565,7 +568,7 @@ __device__ __forceinline__ void stage_tables(const Op& op, uint32_t* dst) {
     const uint32_t nt = op.tables_words();
     const uint32_t* src = op.tables_src();
     uint32_t head = 0;
-    if (((reinterpret_cast<uintptr_t>(src) | smem_addr(dst)) & 15u) == 0) {
+    if (ASYNC && ((reinterpret_cast<uintptr_t>(src) | smem_addr(dst)) & 15u) == 0) {
         const uint32_t n4 = nt / 4;
         for (uint32_t i = threadIdx.x; i < n4; i += blockDim.x)
             asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst + 4 * i)), "l"(src + 4 * i)
@@ -573,7 +576,7 @@ __device__ __forceinline__ void stage_tables(const Op& op, uint32_t* dst) {
         head = 4 * n4;
     }
     for (uint32_t i = head + threadIdx.x; i < nt; i += blockDim.x) dst[i] = src[i];
-    asm volatile("cp.async.wait_all;" ::: "memory");
+    if (ASYNC) asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
 template <class Op>
@@ -711,7 +714,7 @@ __global__ void __launch_bounds__(kThreads) stream_direct_kernel(const Op op, co
         ldg_run<G::W0>(in0 + run * (G::R * Op::IN0), a);
         ldg_run<G::W1>(in1 + run * (G::R * Op::IN1), b);
     }
-    stage_tables(op, s_tab);
+    stage_tables<Op, false>(op, s_tab);
     __syncthreads();
     const uint32_t tab = smem_addr(s_tab);
     uint32_t err = 0;
@@ -738,7 +741,7 @@ __global__ void __launch_bounds__(kThreads) stream_tail_kernel(const Op op, cons
     extern __shared__ __align__(128) uint8_t smem[];
     uint32_t* s_tab = reinterpret_cast<uint32_t*>(smem);
     pdl_launch();
-    stage_tables(op, s_tab);
+    stage_tables<Op, false>(op, s_tab);
     pdl_wait();
     __syncthreads();
     const uint32_t tab = smem_addr(s_tab);
