@@ -332,7 +332,7 @@ __device__ __forceinline__ void dmma_f64(double& d0, double& d1, double a, doubl
                  : "d"(a), "d"(b));
 }
 
-template <int ND, int W, class K>
+template <int ND, int W, class K, bool INT>
 __global__ void __launch_bounds__(kMmaWarps * 32, kMmaCtasPerSm)
     fqt_mma_kernel(const FqtParams P, const double* __restrict__ pw, uint64_t L1, const double* __restrict__ qw,
                    uint64_t L2, uint64_t T, uint64_t cd, uint32_t* __restrict__ res) {
@@ -382,6 +382,11 @@ __global__ void __launch_bounds__(kMmaWarps * 32, kMmaCtasPerSm)
     __syncthreads();
 
     // accumulators: two sets (k-steps 0,1 and 2,3) x 2 m-tiles x 2 n-tiles
+    // INT: both accumulator sets start at 2^52 (integers in [2^52, 2^53) are
+    // exact with ulp 1), so a group sum is the integer sum of two mantissas
+    // and the close issues no fp64 instruction (the fp64 floor and the set
+    // sum competed with the other warps' DMMAs for the fp64 pipe)
+    constexpr double kB = INT ? kTwo52 : 0.0;
     double acc[2][2][2][2];
     uint32_t racc[8][NW];
 #pragma unroll
@@ -394,7 +399,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, kMmaCtasPerSm)
 #pragma unroll
             for (int m = 0; m < 2; ++m)
 #pragma unroll
-                for (int j = 0; j < 2; ++j) acc[a][m][j][0] = acc[a][m][j][1] = 0.0;
+                for (int j = 0; j < 2; ++j) acc[a][m][j][0] = acc[a][m][j][1] = kB;
     };
     zero_acc();
     auto close_groups = [&]() {
@@ -404,9 +409,20 @@ __global__ void __launch_bounds__(kMmaWarps * 32, kMmaCtasPerSm)
             for (int j = 0; j < 2; ++j)
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
-                    const double r = acc[0][m][j][h] + acc[1][m][j][h];  // exact: integers < 2^53
                     uint32_t u[ND], mu[ND];
-                    redq_raw_digits<ND>(c, r, u);
+                    if constexpr (INT) {
+                        // floor(r/p) = mulhi(r, ceil(2^64/p)): exact for r < 2^53, p < 2^11
+                        const uint64_t r = (dbits(acc[0][m][j][h]) & kMask52) + (dbits(acc[1][m][j][h]) & kMask52);
+                        const uint64_t rop = __umul64hi(r, P.p_magic);
+#pragma unroll
+                        for (int i = 0; i < ND; ++i) {
+                            const uint32_t sh = c.qbits() * i;
+                            u[i] = static_cast<uint32_t>(r >> sh) - c.p() * static_cast<uint32_t>(rop >> sh);
+                        }
+                    } else {
+                        const double r = acc[0][m][j][h] + acc[1][m][j][h];  // exact: integers < 2^53
+                        redq_raw_digits<ND>(c, r, u);
+                    }
                     redq_correct<ND, W>(c, u, mu, [&](uint32_t idx) { return lds_u32(tab_s + 4 * idx); });
                     const int x = (m * 2 + j) * 2 + h;
 #pragma unroll
@@ -523,7 +539,7 @@ cudaError_t run_conv_k(const FqtParams& P, const double* pw, uint64_t L1, const 
     return launch_pdl(fqt_conv_kernel<ND, W, K>, grid, dim3(kFqtT), smem, s, P, pw, L1, qw, L2, T, isplit, res);
 }
 
-template <int ND, int W, class K>
+template <int ND, int W, class K, bool INT = false>
 cudaError_t run_conv_mma(const FqtParams& P, const double* pw, uint64_t L1, const double* qw, uint64_t L2,
                          uint64_t T, uint32_t splits, uint64_t cd, uint32_t* res, cudaStream_t s) {
     const dim3 grid(static_cast<unsigned>((T + kMmaOut - 1) / kMmaOut), splits);
@@ -531,13 +547,13 @@ cudaError_t run_conv_mma(const FqtParams& P, const double* pw, uint64_t L1, cons
     if (smem > 200 * 1024) return cudaErrorInvalidValue;
     static size_t cur = 0;
     if (smem > 48 * 1024 && smem > cur) {
-        if (cudaError_t e = cudaFuncSetAttribute(fqt_mma_kernel<ND, W, K>,
+        if (cudaError_t e = cudaFuncSetAttribute(fqt_mma_kernel<ND, W, K, INT>,
                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
             e != cudaSuccess)
             return e;
         cur = smem;
     }
-    return launch_pdl(fqt_mma_kernel<ND, W, K>, grid, dim3(kMmaWarps * 32), smem, s, P, pw, L1, qw, L2, T, cd, res);
+    return launch_pdl(fqt_mma_kernel<ND, W, K, INT>, grid, dim3(kMmaWarps * 32), smem, s, P, pw, L1, qw, L2, T, cd, res);
 }
 
 template <int ND, int W, class K, int SWAR_B = 0>
@@ -575,9 +591,12 @@ cudaError_t run_conv_w(const FqtParams& P, const double* pw, uint64_t L1, const 
     if (P.nq < 8)
         return P.rq.qbits ? run_conv_step<ND, W, RtConst<true>>(P, pw, L1, qw, L2, T, splits, isplit, res, s)
                           : run_conv_step<ND, W, RtConst<false>>(P, pw, L1, qw, L2, T, splits, isplit, res, s);
-    if (fqt_use_mma(P.nq))
-        return P.rq.qbits ? run_conv_mma<ND, W, RtConst<true>>(P, pw, L1, qw, L2, T, splits, isplit, res, s)
-                          : run_conv_mma<ND, W, RtConst<false>>(P, pw, L1, qw, L2, T, splits, isplit, res, s);
+    if (fqt_use_mma(P.nq)) {
+        if (P.rq.qbits)
+            return P.mma_int ? run_conv_mma<ND, W, RtConst<true>, true>(P, pw, L1, qw, L2, T, splits, isplit, res, s)
+                             : run_conv_mma<ND, W, RtConst<true>>(P, pw, L1, qw, L2, T, splits, isplit, res, s);
+        return run_conv_mma<ND, W, RtConst<false>>(P, pw, L1, qw, L2, T, splits, isplit, res, s);
+    }
     return P.rq.qbits ? run_conv_k<ND, W, RtConst<true>>(P, pw, L1, qw, L2, T, splits, isplit, res, s)
                       : run_conv_k<ND, W, RtConst<false>>(P, pw, L1, qw, L2, T, splits, isplit, res, s);
 }

@@ -458,6 +458,11 @@ void fqt_mul_device(const RedqPlan& plan, const QadicParams& params, const uint8
     F.rq = dp.prm;
     F.k = params.k;
     F.nq = static_cast<uint32_t>(std::max<u64>(params.n_q, 1));
+    // integer group REDQ in the DMMA kernel: q = 2^b and every group word
+    // below 2^52 (biased accumulators), p <= 256 (mulhi floor exact)
+    const u64 nd = 2 * u64(params.k) - 1;
+    F.mma_int = (dp.prm.qbits != 0 && dp.prm.qbits * nd <= 52) ? 1u : 0u;
+    F.p_magic = ~u64(0) / params.p + 1;  // ceil(2^64 / p) for p not a power of two; 2^64/p exactly otherwise
     StreamBuf ws(qpk::fqt_workspace_bytes(params.k, F.nq, na, nb), s);
     check(qpk::launch_fqt_mul(F, a, na, b, nb, out, ws.ptr, s), "fqt_mul launch");
 }

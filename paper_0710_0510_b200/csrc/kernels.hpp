@@ -112,6 +112,10 @@ struct FqtParams {
     RedqParams rq;  // fqt_reduction_plan: d = 2k-2 (ND = 2k-1 <= 15)
     uint32_t k;     // coefficients per chunk (d+1)
     uint32_t nq;    // products per REDQ group (params.n_q)
+    // DMMA kernel, q = 2^b with q^(2k-1) <= 2^52: accumulators biased by 2^52
+    // and the group REDQ in integers, floor(r/p) = mulhi64(r, p_magic)
+    uint32_t mma_int;
+    uint64_t p_magic;  // ceil(2^64 / p)
 };
 
 // ---- launchers (return cudaError_t of the launch) ----
