@@ -39,7 +39,6 @@ __global__ void __launch_bounds__(kOvThreads) fqt_overlap_kernel(uint32_t p, uin
                                                                  uint64_t nout, uint64_t mma_cd, uint64_t L1,
                                                                  uint64_t L2) {
     __shared__ uint32_t sums[257][4];
-    pdl_launch();
     pdl_wait();
     const uint32_t nw = (nd + 3) / 4;
     const uint64_t nchunks = (nout + k - 1) / k;
@@ -95,7 +94,6 @@ __global__ void __launch_bounds__(kOvThreads) fqt_overlap_kernel(uint32_t p, uin
 __global__ void fqt_pack2_kernel(uint32_t p, uint32_t k, double qd, const uint8_t* __restrict__ a, uint64_t na,
                                  uint64_t L1, double* __restrict__ wa, const uint8_t* __restrict__ b, uint64_t nb,
                                  uint64_t L2, double* __restrict__ wb) {
-    pdl_launch();
     pdl_wait();
     for (uint64_t x = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; x < L1 + L2;
          x += uint64_t(gridDim.x) * blockDim.x) {
@@ -124,7 +122,6 @@ struct FqtWideParams {
 __global__ void fqt_wide_pack_kernel(uint32_t p, uint32_t k, uint64_t q, const uint8_t* __restrict__ a, uint64_t na,
                                      uint64_t L1, u128d* __restrict__ wa, const uint8_t* __restrict__ b, uint64_t nb,
                                      uint64_t L2, u128d* __restrict__ wb) {
-    pdl_launch();
     pdl_wait();
     for (uint64_t x = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; x < L1 + L2;
          x += uint64_t(gridDim.x) * blockDim.x) {
@@ -170,7 +167,6 @@ __device__ __forceinline__ void fqt_wide_close(const FqtWideParams& P, u128d r, 
 __global__ void __launch_bounds__(256) fqt_wide_conv_kernel(const FqtWideParams P, const u128d* __restrict__ pw,
                                                             uint64_t L1, const u128d* __restrict__ qw, uint64_t L2,
                                                             uint64_t T, uint32_t* __restrict__ res) {
-    pdl_launch();
     pdl_wait();
     const uint32_t nw = (P.nd + 3) / 4;
     for (uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < T; t += uint64_t(gridDim.x) * blockDim.x) {

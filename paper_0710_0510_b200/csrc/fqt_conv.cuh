@@ -73,7 +73,6 @@ __global__ void __launch_bounds__(kFqtT) fqt_conv_step_kernel(const FqtParams P,
         for (uint32_t i = tid; i < P.rq.n_entries; i += blockDim.x) tab[i] = P.rq.table[i];
     const K c{P.rq};
     const uint32_t tab_s = smem_addr(tab);
-    pdl_launch();
     pdl_wait();  // pw / qw come from the preceding pack launch
 
     const uint64_t t0 = uint64_t(blockIdx.x) * kFqtT, t = t0 + tid;
@@ -191,7 +190,6 @@ __global__ void __launch_bounds__(kFqtT) fqt_conv_kernel(const FqtParams P, cons
         for (uint32_t i = tid; i < P.rq.n_entries; i += blockDim.x) tab[i] = P.rq.table[i];
     const K c{P.rq};
     const uint32_t tab_s = smem_addr(tab);
-    pdl_launch();
     pdl_wait();  // pw / qw come from the preceding pack launch
 
     const uint64_t t0 = uint64_t(blockIdx.x) * kFqtOut;
@@ -347,7 +345,6 @@ __global__ void __launch_bounds__(kMmaWarps * 32, kMmaCtasPerSm)
         for (uint32_t i = tid; i < P.rq.n_entries; i += blockDim.x) tab[i] = P.rq.table[i];
     const K c{P.rq};
     const uint32_t tab_s = smem_addr(tab);
-    pdl_launch();
     pdl_wait();  // pw / qw come from the preceding pack launch
 
     // this CTA: a-blocks [A0, A0 + kMmaA) x shifts [d_lo, d_hi) (range

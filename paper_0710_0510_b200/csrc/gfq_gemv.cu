@@ -71,6 +71,7 @@ struct Acc<false> {
 template <bool INT>
 __global__ void gemv_prep_x_kernel(const double* __restrict__ fval, const uint32_t* __restrict__ x, uint64_t K,
                                    typename Acc<INT>::V* __restrict__ xv) {
+    pdl_wait();
     for (uint64_t j = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < K; j += uint64_t(gridDim.x) * blockDim.x)
         xv[j] = Acc<INT>::from(fval[x[j]]);
 }
@@ -95,6 +96,8 @@ __global__ void __launch_bounds__(kGemvThreads) gfq_gemv_kernel(const GfqGemvPar
     for (int i = 0; i < KR; ++i) nlh *= P.lh_radix;
     for (uint32_t i = threadIdx.x; i < nval; i += blockDim.x) tv[i] = AC::from(P.fval[REPL ? i >> 5 : i]);
     for (uint32_t i = threadIdx.x; i < 2 * nlh; i += blockDim.x) tabs[i] = P.lc[i];
+    // PDL: the field tables above are constant; A and x follow the previous launch
+    pdl_wait();
     __syncthreads();
     const uint32_t lc_s = smem_addr(tabs), hc_s = lc_s + 4 * nlh;
 
@@ -213,6 +216,7 @@ __device__ __forceinline__ void gemv_emit(uint32_t p, uint32_t k, const uint32_t
 __global__ void gemv_finish_rows_kernel(uint32_t p, uint32_t k, const uint32_t* __restrict__ log,
                                         const uint32_t* __restrict__ ws, uint64_t m, uint32_t splits,
                                         uint32_t* __restrict__ out_rep, uint8_t* __restrict__ out_coeff) {
+    pdl_wait();
     for (uint64_t row = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; row < m;
          row += uint64_t(gridDim.x) * blockDim.x) {
         uint32_t cf = ws[row];
@@ -227,6 +231,7 @@ __global__ void __launch_bounds__(256) gemv_finish_cta_kernel(uint32_t p, uint32
                                                               uint32_t splits, uint32_t* __restrict__ out_rep,
                                                               uint8_t* __restrict__ out_coeff) {
     __shared__ uint32_t part[8];
+    pdl_wait();
     for (uint64_t row = blockIdx.x; row < m; row += gridDim.x) {
         uint32_t cf = 0;
         for (uint32_t s = threadIdx.x; s < splits; s += blockDim.x) cf = add_mod_bytes_mm(cf, ws[s * m + row], p);
@@ -266,15 +271,14 @@ cudaError_t run_gemv_v(const GfqGemvParams& P, const uint32_t* A, const void* xv
     if (vec) {
         if (cudaError_t e = allow_smem(gfq_gemv_kernel<KR, K, true, INT, REPL, XREP>, smem, attr[1]); e != cudaSuccess)
             return e;
-        gfq_gemv_kernel<KR, K, true, INT, REPL, XREP>
-            <<<grid, kGemvThreads, smem, s>>>(P, A, xv, m, Kd, splits, ksplit, ws);
+        return launch_pdl(gfq_gemv_kernel<KR, K, true, INT, REPL, XREP>, dim3(grid), dim3(kGemvThreads), smem, s, P,
+                          A, xv, m, Kd, splits, ksplit, ws);
     } else {
         if (cudaError_t e = allow_smem(gfq_gemv_kernel<KR, K, false, INT, REPL, XREP>, smem, attr[0]); e != cudaSuccess)
             return e;
-        gfq_gemv_kernel<KR, K, false, INT, REPL, XREP>
-            <<<grid, kGemvThreads, smem, s>>>(P, A, xv, m, Kd, splits, ksplit, ws);
+        return launch_pdl(gfq_gemv_kernel<KR, K, false, INT, REPL, XREP>, dim3(grid), dim3(kGemvThreads), smem, s, P,
+                          A, xv, m, Kd, splits, ksplit, ws);
     }
-    return cudaGetLastError();
 }
 
 template <int KR, class K>
@@ -339,11 +343,12 @@ cudaError_t launch_gfq_gemv(const GfqGemvParams& P, const uint32_t* A, const uin
     const bool xrep = m <= kXrepRows;
     if (Kd && !xrep) {
         const int g = static_cast<int>(std::min<uint64_t>((Kd + 255) / 256, uint64_t(num_sms()) * 8));
-        if (P.vals32)
-            gemv_prep_x_kernel<true><<<g, 256, 0, s>>>(P.fval, x, Kd, reinterpret_cast<uint32_t*>(xv));
-        else
-            gemv_prep_x_kernel<false><<<g, 256, 0, s>>>(P.fval, x, Kd, reinterpret_cast<double*>(xv));
-        if (cudaError_t e = cudaGetLastError(); e != cudaSuccess) return e;
+        const cudaError_t e =
+            P.vals32 ? launch_pdl(gemv_prep_x_kernel<true>, dim3(g), dim3(256), 0, s, P.fval, x, Kd,
+                                  reinterpret_cast<uint32_t*>(xv))
+                     : launch_pdl(gemv_prep_x_kernel<false>, dim3(g), dim3(256), 0, s, P.fval, x, Kd,
+                                  reinterpret_cast<double*>(xv));
+        if (e != cudaSuccess) return e;
     }
     // split length: a multiple of 128 (one warp-wide 16-byte vector row)
     uint64_t ksplit = (Kd + splits - 1) / splits;
@@ -363,12 +368,12 @@ cudaError_t launch_gfq_gemv(const GfqGemvParams& P, const uint32_t* A, const uin
     const uint32_t parts = splits >= 64 && splits % 8 == 0 ? splits / 8 : splits;  // the kernel's CTA reduction
     if (parts >= 64) {
         const int fgrid = static_cast<int>(std::min<uint64_t>(m, uint64_t(num_sms()) * 8));
-        gemv_finish_cta_kernel<<<fgrid, 256, 0, s>>>(P.p, P.k, P.log, part, m, parts, out_rep, out_coeff);
-    } else {
-        const int fgrid = static_cast<int>(std::min<uint64_t>((m + 255) / 256, uint64_t(num_sms()) * 4));
-        gemv_finish_rows_kernel<<<fgrid, 256, 0, s>>>(P.p, P.k, P.log, part, m, parts, out_rep, out_coeff);
+        return launch_pdl(gemv_finish_cta_kernel, dim3(fgrid), dim3(256), 0, s, P.p, P.k, P.log,
+                          static_cast<const uint32_t*>(part), m, parts, out_rep, out_coeff);
     }
-    return cudaGetLastError();
+    const int fgrid = static_cast<int>(std::min<uint64_t>((m + 255) / 256, uint64_t(num_sms()) * 4));
+    return launch_pdl(gemv_finish_rows_kernel, dim3(fgrid), dim3(256), 0, s, P.p, P.k, P.log,
+                      static_cast<const uint32_t*>(part), m, parts, out_rep, out_coeff);
 }
 
 }  // namespace qpk

@@ -706,7 +706,6 @@ __global__ void __launch_bounds__(kThreads) stream_direct_kernel(const Op op, co
     extern __shared__ __align__(128) uint8_t smem[];
     uint32_t* s_tab = reinterpret_cast<uint32_t*>(smem);
     // first loads before the table staging, so both overlap
-    pdl_launch();
     pdl_wait();
     uint64_t run = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     uint32_t a[G::W0 > 0 ? G::W0 : 1], b[G::W1 > 0 ? G::W1 : 1];
@@ -740,7 +739,6 @@ __global__ void __launch_bounds__(kThreads) stream_tail_kernel(const Op op, cons
     using G = Geometry<Op>;
     extern __shared__ __align__(128) uint8_t smem[];
     uint32_t* s_tab = reinterpret_cast<uint32_t*>(smem);
-    pdl_launch();
     stage_tables<Op, false>(op, s_tab);
     pdl_wait();
     __syncthreads();
