@@ -604,7 +604,6 @@ __global__ void __launch_bounds__(kThreads) stream_tma_kernel(const Op op, const
     // thread 0 puts the first S tiles in flight before the table staging,
     // so the per-CTA table copy overlaps the first loads; barrier setup runs
     // before pdl_wait, overlapping the previous kernel's tail
-    pdl_launch();
     if (tid == 0) {
         for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
         fence_mbar_init();
