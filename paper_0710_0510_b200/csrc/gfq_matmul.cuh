@@ -111,18 +111,6 @@ __host__ __device__ constexpr uint64_t lane_ones() {
 // floor(r/3) from the halves r = rh 2^32 + rl: with rh = 3 qh + mh and
 // rl = 3 ql + rr, floor(r/3) = qh 2^32 + mh (2^32-1)/3 + ql + [mh + rr >= 3]
 // (2^32 == 1 mod 3; the low part stays below 2^32).
-__host__ __device__ __forceinline__ uint64_t div3_u64(uint64_t r) {
-    const uint32_t rh = static_cast<uint32_t>(r >> 32), rl = static_cast<uint32_t>(r);
-#ifdef __CUDA_ARCH__
-    const uint32_t qh = __umulhi(rh, 0xAAAAAAABu) >> 1, ql = __umulhi(rl, 0xAAAAAAABu) >> 1;
-#else
-    const uint32_t qh = static_cast<uint32_t>((uint64_t(rh) * 0xAAAAAAABu) >> 33);
-    const uint32_t ql = static_cast<uint32_t>((uint64_t(rl) * 0xAAAAAAABu) >> 33);
-#endif
-    const uint32_t mh = rh - 3 * qh, rr = rl - 3 * ql;
-    const uint32_t lo = mh * 0x55555555u + ql + ((mh + rr + 1) >> 2);
-    return (uint64_t(qh) << 32) | lo;
-}
 
 // (Computing floor(r/3) by the fp64 floor for half of the accumulators and
 // by div3_u64 for the other half measured 43.7 ms: worse than either.)
