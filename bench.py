@@ -364,6 +364,17 @@ def secondary_cpu_refs(sec):
         sec["k6_fqt_mul"]["cpu_ref_q32_d3_nq1"] = {
             "value": n * n / dt, "unit": "coefficient products/s", "cores": 1, "kind": "reference",
             "sample": f"one fqt_mul of two {n}-coefficient polynomials over F_3 (single call, single thread)"}
+    # ... and the wide-group parameters of the DMMA kernel (q = 2^13, d = 1, n_q = 409)
+    n = 1 << 14
+    a = O.draws(0x6, 2 * n, 3).astype(np.uint64)
+    out = np.zeros(2 * n - 1, np.uint64)
+    t0 = time.perf_counter()
+    O.ref().ref_fqt_mul(3, 1, 1 << 13, 409, a[:n], n, a[n:], n, out, cost)
+    dt = time.perf_counter() - t0
+    if "k6_fqt_mul" in sec:
+        sec["k6_fqt_mul"]["cpu_ref_q8192_d1_nq409"] = {
+            "value": n * n / dt, "unit": "coefficient products/s", "cores": 1, "kind": "reference",
+            "sample": f"one fqt_mul of two {n}-coefficient polynomials over F_3, q=2^13, n_q=409 (single call, single thread)"}
 
 
 def measure_secondary(Q, torch, dev):
