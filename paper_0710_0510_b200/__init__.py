@@ -297,14 +297,14 @@ class PolymulPlan:
         if _is_torch(a):
             import torch
             na, nb = a.numel(), b.numel()
-            if out is None:
-                out = torch.empty((max(na + nb - 1, 0),), dtype=torch.uint8, device=a.device)
+            if out is None:  # an empty operand gives the empty product (polymul.cpp:81-88)
+                out = torch.empty((na + nb - 1 if na and nb else 0,), dtype=torch.uint8, device=a.device)
             _check(lib().qpk_fqt_mul(self._h, _ptr(a), na, _ptr(b), nb, _ptr(out), _stream()))
             return out
         a = _host(a, np.uint8).reshape(-1)
         b = _host(b, np.uint8).reshape(-1)
         if out is None:
-            out = np.empty((max(a.size + b.size - 1, 0),), np.uint8)
+            out = np.empty((a.size + b.size - 1 if a.size and b.size else 0,), np.uint8)
         cost = Cost()
         _check(lib().qpk_fqt_mul_host(self._h, _ptr(a), a.size, _ptr(b), b.size, _ptr(out), C.byref(cost)))
         self.last_cost = cost.as_dict()
