@@ -375,6 +375,11 @@ def secondary_cpu_refs(sec):
         sec["k6_fqt_mul"]["cpu_ref_q8192_d1_nq409"] = {
             "value": n * n / dt, "unit": "coefficient products/s", "cores": 1, "kind": "reference",
             "sample": f"one fqt_mul of two {n}-coefficient polynomials over F_3, q=2^13, n_q=409 (single call, single thread)"}
+    if "k6_fqt_mul_large" in sec:
+        sec["k6_fqt_mul_large"]["cpu_ref"] = {
+            "value": n * n / dt, "unit": "coefficient products/s", "cores": 1, "kind": "reference",
+            "sample": f"one fqt_mul of two {n}-coefficient polynomials, same params (the rate is size-independent: "
+                      "the reference loop is quadratic), single thread"}
 
 
 def measure_secondary(Q, torch, dev):
@@ -519,6 +524,19 @@ def measure_secondary(Q, torch, dev):
                                    # n_q >= 16 runs on the fp64 tensor pipe (DMMA), n_q = 1 on CUDA cores
                                    "kernel": "fqt_mma_kernel (DMMA)" if nq6 >= 16 else "fqt_conv_step_kernel (SWAR REDQ)",
                                    "frac_fp64_probe": 2 * wp / 1e12 / (fp64_peak if nq6 >= 16 else dfma_peak)}
+    # K6 at scale: 2^20-coefficient operands on the DMMA kernel (the 2^16
+    # case above is launch/latency dominated)
+    nL = 1 << 20
+    aL = torch.randint(0, 3, (nL,), dtype=torch.uint8, device=dev, generator=gen)
+    bL = torch.randint(0, 3, (nL,), dtype=torch.uint8, device=dev, generator=gen)
+    oL = torch.empty((2 * nL - 1,), dtype=torch.uint8, device=dev)
+    pmL = Q.PolymulPlan(3, 1 << 13, 2, 409)
+    ms = time_it(lambda: pmL.fqt_mul(aL, bL, out=oL), 3, warm=1, cold=False)
+    wp = (nL // 2) ** 2 / (ms * 1e-3)
+    res["k6_fqt_mul_large"] = {"n": nL, "p": 3, "q": 1 << 13, "d": 1, "n_q": 409, "ms": ms,
+                               "coeff_products_per_s": nL * nL / (ms * 1e-3), "fp64_tflops": 2 * wp / 1e12,
+                               "kernel": "fqt_mma_kernel (DMMA)", "frac_fp64_probe": 2 * wp / 1e12 / fp64_peak}
+    del aL, bL, oL
     # C4, C5: GF(p^k) matrix products (pack + contraction), GF ops/s = 2 n^3 / t
     for cfg in (Q.C4, Q.C5):
         nn, k = cfg.n, cfg.k
