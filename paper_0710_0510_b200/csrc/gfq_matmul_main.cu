@@ -61,22 +61,37 @@ __global__ void reps_to_coeffs_kernel(uint32_t k, const uint32_t* __restrict__ a
 
 // ---------------------------------------------------------------- K1 packs
 // 32x32 tiles through shared memory so both the record reads and the
-// (possibly transposed) double writes are coalesced.
-__global__ void pack_coeffs_kernel(uint32_t p, uint32_t k, double qd, const uint8_t* __restrict__ src, uint64_t rows,
+// (possibly transposed) double writes are coalesced.  KR (record width) is a
+// template parameter: unrolled byte loads and Horner steps, and the runtime
+// reduction mod p only for bytes >= p (ncu: the runtime-k loop with an
+// unconditional `% p` spent ~110 instructions per element, issue-bound at
+// 2.5 TB/s: 68 -> 55 us per C4 operand).
+template <int KR>
+__global__ void pack_coeffs_kernel(uint32_t p, double qd, const uint8_t* __restrict__ src, uint64_t rows,
                                    uint64_t cols, double* __restrict__ dst, uint64_t ld, bool transpose) {
     __shared__ double tile[32][33];
     const uint64_t r0 = uint64_t(blockIdx.y) * 32, c0 = uint64_t(blockIdx.x) * 32;
     const int tx = threadIdx.x, ty = threadIdx.y;
+    const bool cin = c0 + tx < cols;
+    const uint8_t* base = src + (r0 * cols + c0 + tx) * KR;
+#pragma unroll
     for (int i = ty; i < 32; i += 8) {
-        const uint64_t r = r0 + i, c = c0 + tx;
         double v = 0.0;
-        if (r < rows && c < cols) {
-            const uint8_t* e = src + (r * cols + c) * k;
-            for (int t = static_cast<int>(k) - 1; t >= 0; --t) v = fma(v, qd, static_cast<double>(e[t] % p));
+        if (cin && r0 + i < rows) {
+            const uint8_t* e = base + uint64_t(i) * cols * KR;
+            uint32_t x[KR];
+#pragma unroll
+            for (int t = 0; t < KR; ++t) x[t] = e[t];
+#pragma unroll
+            for (int t = 0; t < KR; ++t)
+                if (x[t] >= p) x[t] %= p;  // unreduced bytes are reduced as from_coeffs does
+#pragma unroll
+            for (int t = KR - 1; t >= 0; --t) v = fma(v, qd, static_cast<double>(x[t]));
         }
         tile[i][tx] = v;
     }
     __syncthreads();
+#pragma unroll
     for (int i = ty; i < 32; i += 8) {
         if (transpose) {
             const uint64_t c = c0 + i, r = r0 + tx;
@@ -166,7 +181,13 @@ cudaError_t launch_pack_coeffs(uint32_t p, uint32_t k, double qd, const uint8_t*
                                double* dst, uint64_t ld, bool transpose, cudaStream_t s) {
     if (rows == 0 || cols == 0) return cudaSuccess;
     dim3 grid(static_cast<unsigned>((cols + 31) / 32), static_cast<unsigned>((rows + 31) / 32));
-    pack_coeffs_kernel<<<grid, dim3(32, 8), 0, s>>>(p, k, qd, src, rows, cols, dst, ld, transpose);
+    switch (k) {
+        case 1: pack_coeffs_kernel<1><<<grid, dim3(32, 8), 0, s>>>(p, qd, src, rows, cols, dst, ld, transpose); break;
+        case 2: pack_coeffs_kernel<2><<<grid, dim3(32, 8), 0, s>>>(p, qd, src, rows, cols, dst, ld, transpose); break;
+        case 3: pack_coeffs_kernel<3><<<grid, dim3(32, 8), 0, s>>>(p, qd, src, rows, cols, dst, ld, transpose); break;
+        case 4: pack_coeffs_kernel<4><<<grid, dim3(32, 8), 0, s>>>(p, qd, src, rows, cols, dst, ld, transpose); break;
+        default: return cudaErrorInvalidValue;
+    }
     return cudaGetLastError();
 }
 
