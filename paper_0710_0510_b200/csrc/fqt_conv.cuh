@@ -8,10 +8,14 @@
 //    exact double;
 //  * product: output chunk t is sum_i pw[i] * qw[t-i] -- a 1-D convolution
 //    of packed words, each fp64 product carrying a (d+1)x(d+1) block of
-//    coefficient products.  A CTA sweeps i through shared-memory tiles (pw
-//    broadcast, qw sliding window) for 2048 consecutive t, 8 per thread in
-//    registers (n_q >= 8), or 256 t, one per thread, when a REDQ follows
-//    nearly every product (n_q < 8); grid.y splits the i range;
+//    coefficient products.  Three kernels by group size: n_q >= 16 on the
+//    fp64 tensor cores (fqt_mma_kernel, a block-Toeplitz GEMM per block
+//    shift); 8 <= n_q < 16 register-blocked FFMA (fqt_conv_kernel: a CTA
+//    sweeps i through shared-memory tiles, pw broadcast, qw sliding window,
+//    2048 consecutive t, 8 per thread); n_q < 8 one t per thread
+//    (fqt_conv_step_kernel, a REDQ after nearly every product); grid.y
+//    splits the i (or block-shift) range.  Words beyond fp64 (m > 53) run
+//    fqt_wide_conv_kernel in fqt_conv.cu;
 //  * groups of at most n_q products are closed by REDQ (Alg. 2/3): the 2d+1
 //    residues are added mod p into the thread's byte lanes, exactly as the
 //    reference's per-group redq_residues_into + overlap-add;
