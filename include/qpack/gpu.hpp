@@ -25,6 +25,10 @@ void redq_residues_batch(std::span<const double> words, const RedqPlan& plan, st
 // integer mode, restricted to 64-bit words)
 void redq_residues_batch(std::span<const std::uint64_t> words, const RedqPlan& plan, std::span<std::uint8_t> out,
                          CostReport* cost = nullptr);
+// ... and over u128 words below q^(d+1) (the reference's integer mode in
+// full, redq.cpp:44-58)
+void redq_residues_batch(std::span<const u128> words, const RedqPlan& plan, std::span<std::uint8_t> out,
+                         CostReport* cost = nullptr);
 
 // n products of degree-<k polynomials (records of k coefficients) -> n*(2k-1)
 // residues, via pack -> fp64 product -> REDQ.  (dqt_mul_poly dqt.hpp:46,

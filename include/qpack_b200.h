@@ -81,6 +81,12 @@ QPK_API qpk_status qpk_redq_residues_u64(qpk_redq_plan plan, const uint64_t* wor
                                          void* stream);
 QPK_API qpk_status qpk_redq_residues_u64_host(qpk_redq_plan plan, const uint64_t* words, uint64_t n,
                                               uint8_t* residues, qpk_cost* cost);
+/* u128 words as (lo, hi) uint64 pairs, below q^(d+1) <= 2^128: the
+ * reference's integer mode in full (redq.cpp:44-58)                       */
+QPK_API qpk_status qpk_redq_residues_u128(qpk_redq_plan plan, const uint64_t* words, uint64_t n, uint8_t* residues,
+                                          void* stream);
+QPK_API qpk_status qpk_redq_residues_u128_host(qpk_redq_plan plan, const uint64_t* words, uint64_t n,
+                                               uint8_t* residues, qpk_cost* cost);
 /* wait for `stream`, then report (and clear) latched data errors:
  * QPK_ERR_DOMAIN = a word not below q^(d+1) / not an exact double (redq.cpp:27-28) */
 QPK_API qpk_status qpk_redq_sync(qpk_redq_plan plan, void* stream);

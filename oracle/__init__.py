@@ -77,6 +77,7 @@ def oracle():
             _sig(lib, "qo_correction_table", I, [U64, U64, U32, I, U64, C.POINTER(PU64), PU64, PU64])
             _sig(lib, "qo_redq_run_f64", I, [U64, U64, U32, I, U32, I, f64p, U64, u8p])
             _sig(lib, "qo_redq_run_u64", I, [U64, U64, U32, I, U32, I, u64p, U64, u64p])
+            _sig(lib, "qo_redq_run_u128", I, [U64, U64, U32, I, U32, I, u64p, U64, u64p])
             _sig(lib, "qo_redq_trace", I, [U64, U64, U32, U64, U64, PU64, PU64, u64p, u64p])
             _sig(lib, "qo_polymul_batch", I, [U64, U32, u8p, u8p, U64, u8p])
             _sig(lib, "qo_fqt_mul", I, [U64, U32, U64, U32, u64p, U64, u64p, U64, u64p, u64p])
@@ -168,6 +169,16 @@ def redq_u64(p, q, d, words, float_mode=False, window=0, binary_shift=False):
     lib = oracle()
     _chk(lib, lib.qo_redq_run_u64(p, q, d, int(float_mode), window, int(binary_shift), w, w.size, out))
     return out.reshape(w.size, d + 1)
+
+
+def redq_u128(p, q, d, words, float_mode=False, window=0, binary_shift=False):
+    """words: (n, 2) uint64 (lo, hi) halves of u128 words."""
+    w = np.ascontiguousarray(words, np.uint64).reshape(-1, 2)
+    out = np.empty(w.shape[0] * (d + 1), np.uint64)
+    lib = oracle()
+    _chk(lib, lib.qo_redq_run_u128(p, q, d, int(float_mode), window, int(binary_shift), w.reshape(-1), w.shape[0],
+                                   out))
+    return out.reshape(w.shape[0], d + 1)
 
 
 def polymul_batch(p, d, a, b):

@@ -411,6 +411,18 @@ int qo_redq_run_u64(u64 p, u64 q, u32 d, int float_mode, u32 window, int binary_
     return rc;
 }
 
+/* the same over u128 words given as (lo, hi) u64 pairs */
+int qo_redq_run_u128(u64 p, u64 q, u32 d, int float_mode, u32 window, int binary_shift, const u64* words, u64 n,
+                     u64* out) {
+    qo_redq_plan pl;
+    int rc = qo_redq_plan_build(p, q, d, float_mode, &pl);
+    if (!rc && window) rc = qo_redq_attach_table(&pl, window, binary_shift);
+    for (u64 i = 0; !rc && i < n; ++i)
+        rc = qo_redq_word(&pl, ((u128)words[2 * i + 1] << 64) | words[2 * i], NULL, out + i * (d + 1));
+    qo_redq_plan_free(&pl);
+    return rc;
+}
+
 /* ------------------------------------------------------------ DQT / FQT */
 /* polymul.cpp:18-23: largest window w in 4..2 with p^w <= 2^20 */
 static u32 choose_window(u64 p) {

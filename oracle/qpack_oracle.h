@@ -81,6 +81,8 @@ int qo_redq_trace(uint64_t p, uint64_t q, uint32_t d, uint64_t r_lo, uint64_t r_
                   uint64_t* rop_hi, uint64_t* u, uint64_t* mu);
 int qo_redq_run_u64(uint64_t p, uint64_t q, uint32_t d, int float_mode, uint32_t window, int binary_shift,
                     const uint64_t* words, uint64_t n, uint64_t* out);
+int qo_redq_run_u128(uint64_t p, uint64_t q, uint32_t d, int float_mode, uint32_t window, int binary_shift,
+                     const uint64_t* words, uint64_t n, uint64_t* out);
 
 /* ---- DQT + FQT (dqt.cpp, polymul.cpp) ---- */
 int qo_polymul_batch(uint64_t p, uint32_t d, const uint8_t* a, const uint8_t* b, uint64_t n, uint8_t* out);

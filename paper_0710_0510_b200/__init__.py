@@ -99,6 +99,8 @@ SIGNATURES = {
     "qpk_redq_residues_f64_host": (I, [VP, VP, U64, VP, PCost]),
     "qpk_redq_residues_u64": (I, [VP, VP, U64, VP, VP]),
     "qpk_redq_residues_u64_host": (I, [VP, VP, U64, VP, PCost]),
+    "qpk_redq_residues_u128": (I, [VP, VP, U64, VP, VP]),
+    "qpk_redq_residues_u128_host": (I, [VP, VP, U64, VP, PCost]),
     "qpk_redq_sync": (I, [VP, VP]),
     "qpk_redq_cost": (I, [VP, U64, PCost]),
     "qpk_polymul_plan_create": (I, [U64, U64, U32, U32, C.POINTER(VP)]),
@@ -216,19 +218,32 @@ class RedqPlan:
         return self
 
     def residues(self, words, out=None):
-        """redq_residues_into over a batch: words (n,) float64 -> (n, d+1) uint8.
+        """redq_residues_into over a batch: words (n,) float64 -> (n, d+1) uint8;
+        (n,) uint64 / int64 integer words, (n, 2) uint64 / int64 u128 words as
+        (lo, hi) pairs.
         numpy in -> host path (synchronous); CUDA tensor in -> device path on
         torch's current stream (call .sync() to surface data errors)."""
         nd = self.d + 1
         if _is_torch(words):
             import torch
-            n = words.numel()
+            wide = words.dtype in (torch.int64, torch.uint64) and words.dim() == 2 and words.shape[-1] == 2
+            n = words.shape[0] if wide else words.numel()  # u128 words as (lo, hi) pairs
             if out is None:
                 out = torch.empty((n, nd), dtype=torch.uint8, device=words.device)
-            if words.dtype in (torch.int64, torch.uint64):  # integer words (two's-complement bits as u64)
+            if wide:
+                _check(lib().qpk_redq_residues_u128(self._h, _ptr(words), n, _ptr(out), _stream()))
+            elif words.dtype in (torch.int64, torch.uint64):  # integer words (two's-complement bits as u64)
                 _check(lib().qpk_redq_residues_u64(self._h, _ptr(words), n, _ptr(out), _stream()))
             else:
                 _check(lib().qpk_redq_residues_f64(self._h, _ptr(words), n, _ptr(out), _stream()))
+            return out
+        if isinstance(words, np.ndarray) and words.dtype == np.uint64 and words.ndim == 2 and words.shape[1] == 2:
+            w = np.ascontiguousarray(words)  # u128 words as (lo, hi) pairs
+            if out is None:
+                out = np.empty((w.shape[0], nd), np.uint8)
+            cost = Cost()
+            _check(lib().qpk_redq_residues_u128_host(self._h, _ptr(w), w.shape[0], _ptr(out), C.byref(cost)))
+            self.last_cost = cost.as_dict()
             return out
         if isinstance(words, np.ndarray) and words.dtype == np.uint64:
             w = np.ascontiguousarray(words).reshape(-1)

@@ -164,6 +164,28 @@ qpk_status qpk_redq_residues_u64_host(qpk_redq_plan plan, const uint64_t* words,
     });
 }
 
+qpk_status qpk_redq_residues_u128(qpk_redq_plan plan, const uint64_t* words, uint64_t n, uint8_t* residues,
+                                  void* stream) {
+    return guard([&] {
+        need(plan != nullptr, "null plan");
+        need(n == 0 || (words && residues), "null buffer");
+        need(plan->plan.p <= 256, "residues are uint8: p must be <= 256");
+        auto& dp = qpack::detail::device_plan(plan->plan);
+        qpack::gpu::redq_device_u128(dp, words, n, residues, as_stream(stream));
+    });
+}
+
+qpk_status qpk_redq_residues_u128_host(qpk_redq_plan plan, const uint64_t* words, uint64_t n, uint8_t* residues,
+                                       qpk_cost* cost) {
+    return guard([&] {
+        need(plan != nullptr, "null plan");
+        need(n == 0 || (words && residues), "null buffer");
+        need(plan->plan.p <= 256, "residues are uint8: p must be <= 256");
+        qpack::gpu::redq_host_u128(qpack::detail::device_plan(plan->plan), words, n, residues);
+        put_cost(cost, qpack::detail::redq_batch_cost(plan->plan, n));
+    });
+}
+
 qpk_status qpk_redq_sync(qpk_redq_plan plan, void* stream) {
     return guard([&] {
         need(plan != nullptr, "null plan");

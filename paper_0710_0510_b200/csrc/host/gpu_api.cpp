@@ -310,6 +310,34 @@ void redq_device_u64(DevicePlanCache& dp, const uint64_t* d_words, u64 n, uint8_
     check(qpk::launch_redq_u64(dp.prm, d_words, n, d_out, dp.status.as<uint32_t>(), s), "redq launch");
 }
 
+void redq_device_u128(DevicePlanCache& dp, const uint64_t* d_words, u64 n, uint8_t* d_out, cudaStream_t s) {
+    check(qpk::launch_redq_u128(dp.prm, d_words, n, d_out, dp.status.as<uint32_t>(), s), "redq launch");
+}
+
+// u128 words as (lo, hi) pairs, same chunked pipeline as the u64 words
+void redq_host_u128(DevicePlanCache& dp, const uint64_t* h_words, u64 n, uint8_t* h_out) {
+    std::lock_guard<std::mutex> lock(dp.mu);
+    if (!dp.staging) dp.staging = std::make_unique<Staging>();
+    Staging& S = *dp.staging;
+    const u64 nd = dp.prm.d + 1, chunk = u64(1) << 20;
+    for (int sl = 0; sl < Staging::kSlots; ++sl) {
+        S.in0[sl].ensure(chunk * 16);
+        S.out[sl].ensure(chunk * nd);
+    }
+    S.run(
+        n, chunk,
+        [&](int sl, u64 off, u64 cnt, cudaStream_t s) {
+            check(cudaMemcpyAsync(S.in0[sl].ptr, h_words + 2 * off, cnt * 16, cudaMemcpyHostToDevice, s), "H2D");
+        },
+        [&](int sl, u64, u64 cnt, cudaStream_t s) {
+            redq_device_u128(dp, S.in0[sl].as<uint64_t>(), cnt, S.out[sl].as<uint8_t>(), s);
+        },
+        [&](int sl, u64 off, u64 cnt, cudaStream_t s) {
+            check(cudaMemcpyAsync(h_out + off * nd, S.out[sl].ptr, cnt * nd, cudaMemcpyDeviceToHost, s), "D2H");
+        });
+    raise_status(take_status(dp, S.sk));
+}
+
 void redq_host_u64(DevicePlanCache& dp, const uint64_t* h_words, u64 n, uint8_t* h_out) {
     std::lock_guard<std::mutex> lock(dp.mu);
     if (!dp.staging) dp.staging = std::make_unique<Staging>();
@@ -379,6 +407,21 @@ void redq_residues_batch(std::span<const std::uint64_t> words, const RedqPlan& p
         throw std::invalid_argument("redq_residues_batch: output span holds fewer than n*(d+1) residues");
     DevicePlanCache& dp = detail::device_plan(plan);
     redq_host_u64(dp, words.data(), words.size(), out.data());
+    if (cost) *cost += detail::redq_batch_cost(plan, words.size());
+}
+
+void redq_residues_batch(std::span<const u128> words, const RedqPlan& plan, std::span<std::uint8_t> out,
+                         CostReport* cost) {
+    if (out.size() < words.size() * (plan.d + 1))
+        throw std::invalid_argument("redq_residues_batch: output span holds fewer than n*(d+1) residues");
+    if (plan.p > 256) throw std::invalid_argument("qpack-b200 redq: residues are uint8, p must be <= 256");
+    std::vector<uint64_t> halves(2 * words.size());
+    for (std::size_t i = 0; i < words.size(); ++i) {
+        halves[2 * i] = static_cast<uint64_t>(words[i]);
+        halves[2 * i + 1] = static_cast<uint64_t>(words[i] >> 64);
+    }
+    DevicePlanCache& dp = detail::device_plan(plan);
+    redq_host_u128(dp, halves.data(), words.size(), out.data());
     if (cost) *cost += detail::redq_batch_cost(plan, words.size());
 }
 

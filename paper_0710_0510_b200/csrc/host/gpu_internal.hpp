@@ -20,6 +20,8 @@ void redq_device(detail::DevicePlanCache& dp, const double* d_words, u64 n, uint
 void redq_host(detail::DevicePlanCache& dp, const double* h_words, u64 n, uint8_t* h_out);
 void redq_device_u64(detail::DevicePlanCache& dp, const uint64_t* d_words, u64 n, uint8_t* d_out, cudaStream_t s);
 void redq_host_u64(detail::DevicePlanCache& dp, const uint64_t* h_words, u64 n, uint8_t* h_out);
+void redq_device_u128(detail::DevicePlanCache& dp, const uint64_t* d_words, u64 n, uint8_t* d_out, cudaStream_t s);
+void redq_host_u128(detail::DevicePlanCache& dp, const uint64_t* h_words, u64 n, uint8_t* h_out);
 
 // fqt_mul / dqt_mul_poly over a batch of single-chunk pairs
 struct PolymulPlan {

@@ -166,6 +166,12 @@ cudaError_t launch_gfq_gemv(const GfqGemvParams& P, const uint32_t* A, const uin
                             uint32_t splits, void* ws, uint32_t* y_rep, uint8_t* y_coeff, cudaStream_t s);
 
 // K6: out (na+nb-1 coefficients) = a * b mod p, coefficients as uint8;
+// REDQ of u128 integer words ((lo, hi) u64 pairs, the reference's integer
+// mode up to q^(d+1) <= 2^128, redq.cpp:44-58): u128 arithmetic, direct
+// correction.  limit: q^(d+1) as (lo, hi), or 0/0 when it exceeds 2^128.
+cudaError_t launch_redq_u128(const RedqParams& P, const uint64_t* words, uint64_t n, uint8_t* out, uint32_t* status,
+                             cudaStream_t s);
+
 // FQT product with integer words beyond fp64 (the reference's u128 mode,
 // m up to 128: polymul.cpp:97-146 with u128 MAC): packed words and group
 // sums as unsigned __int128, integer-mode REDQ per group (redq.cpp:44-58)

@@ -102,6 +102,43 @@ __global__ void redq_u64_kernel(const RedqParams P, const uint64_t* __restrict__
     report_g(err, status);
 }
 
+// REDQ of u128 words (one per thread): rop = r / p, u_j = r/q^j - p (rop/q^j)
+// (shifts for q = 2^b, u128 divisions by q^j otherwise), direct correction
+__global__ void redq_u128_kernel(const RedqParams P, const unsigned __int128* __restrict__ words, uint64_t n,
+                                 unsigned __int128 limit, uint8_t* __restrict__ out, uint32_t* status) {
+    using u128d = unsigned __int128;
+    pdl_wait();
+    uint32_t err = 0;
+    const uint32_t nd = P.d + 1;
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
+        u128d r = words[i];
+        if (limit && r >= limit) {
+            err |= kErrDomain;
+            r = 0;
+        }
+        const u128d rop = r / P.p;
+        uint32_t u[kMaxDigits];
+        u128d qj = 1;
+        for (uint32_t j = 0; j < nd; ++j) {
+            u128d x, y;
+            if (P.qbits) {
+                const uint32_t sh = P.qbits * j;
+                x = sh < 128 ? r >> sh : 0;
+                y = sh < 128 ? rop >> sh : 0;
+            } else {
+                x = r / qj;
+                y = rop / qj;
+                qj *= P.q;
+            }
+            u[j] = static_cast<uint32_t>(static_cast<uint64_t>(x) - P.p * static_cast<uint64_t>(y));
+        }
+        if (P.neg_q)
+            for (uint32_t j = 0; j + 1 < nd; ++j) u[j] = mod_small_g(u[j] + P.neg_q * u[j + 1], P.p, P.mod_magic);
+        for (uint32_t j = 0; j < nd; ++j) out[i * nd + j] = static_cast<uint8_t>(u[j]);
+    }
+    report_g(err, status);
+}
+
 __global__ void gfq_mul_rep_kernel(uint32_t group, const uint32_t* __restrict__ a, const uint32_t* __restrict__ b,
                                    uint64_t n, uint32_t* __restrict__ out) {
     for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
@@ -176,6 +213,20 @@ cudaError_t launch_redq_u64(const RedqParams& P, const uint64_t* words, uint64_t
     if (P.d + 1 > uint32_t(kMaxDigits)) return cudaErrorInvalidValue;
     redq_u64_kernel<<<grid_for(n), 256, 0, s>>>(P, words, n, out, status);
     return cudaGetLastError();
+}
+
+cudaError_t launch_redq_u128(const RedqParams& P, const uint64_t* words, uint64_t n, uint8_t* out, uint32_t* status,
+                             cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    if (P.d + 1 > uint32_t(kMaxDigits) || P.p > 256) return cudaErrorInvalidValue;
+    // q^(d+1) as u128, 0 when it exceeds 2^128 (every u128 word then qualifies)
+    unsigned __int128 limit = 1;
+    for (uint32_t j = 0; j <= P.d && limit; ++j) {
+        const unsigned __int128 next = limit * P.q;
+        limit = (P.q != 0 && next / P.q == limit) ? next : 0;
+    }
+    return launch_pdl(redq_u128_kernel, dim3(grid_for(n)), dim3(256), 0, s, P,
+                      reinterpret_cast<const unsigned __int128*>(words), n, limit, out, status);
 }
 
 cudaError_t launch_polymul(const PolymulParams& P, const uint8_t* a, const uint8_t* b, uint64_t n, uint8_t* out,
