@@ -169,6 +169,26 @@ static void gpu_tests() {
     words[5] = 1e300;
     CHECK(throws<std::domain_error>([&] { gpu::redq_residues_batch(words, plan, res); }));
 
+    // u128 words (the reference's integer mode, p = 23, q = 10^6, d = 3:
+    // words up to 10^24 > 2^64) == the scalar redq_residues per word
+    {
+        const RedqPlan wide = RedqPlan::build(23, 1000000, 3);
+        std::vector<u128> w128(3001);
+        for (auto& w : w128) w = (u128(rng.next()) << 64 | rng.next()) % (u128(1000000) * 1000000 * 1000000 * 1000000);
+        w128[0] = 0;
+        w128[1] = u128(1000000) * 1000000 * 1000000 * 1000000 - 1;
+        std::vector<std::uint8_t> r128(w128.size() * 4);
+        gpu::redq_residues_batch(std::span<const u128>(w128), wide, r128);
+        bool ok = true;
+        for (std::size_t i = 0; i < w128.size(); ++i) {
+            const std::vector<u64> mu = redq_residues(w128[i], wide);
+            for (int j = 0; j < 4; ++j) ok &= r128[i * 4 + j] == mu[j];
+        }
+        CHECK(ok);
+        w128[9] = u128(1000000) * 1000000 * 1000000 * 1000000;
+        CHECK(throws<std::domain_error>([&] { gpu::redq_residues_batch(std::span<const u128>(w128), wide, r128); }));
+    }
+
     // FQT with u128 words (test_polymul.cpp:42-58, m = 128): the device's
     // integer-word kernel
     CHECK((fqt_mul(DensePoly{5, {3, 2, 1}}, DensePoly{5, {1, 0, 4}}, 2, QadicParams{5, 10000, 3, 1, 128}) ==
