@@ -136,9 +136,12 @@ QPK_API qpk_status qpk_field_describe(qpk_field f, char* buf, uint64_t cap);
 /* host copies of the field tables, p^k entries each (L/H: lh_radix^k) */
 QPK_API qpk_status qpk_field_tables(qpk_field f, uint32_t* log, uint64_t* antilog, uint32_t* plus1, double* fval,
                                     uint32_t* low, uint32_t* high);
-/* GfqField::mul / add / neg / inverse on reps, scalar (host)   gfq.cpp:260-294
- * op 0 mul, 1 add, 2 neg, 3 inverse */
+/* GfqField::mul / add / neg / inverse on reps         gfq.cpp:260-294
+ * op 0 mul, 1 add, 2 neg, 3 inverse.  qpk_field_op: n elements on the
+ * device (host buffers in and out); qpk_field_op1: one element, the
+ * reference's scalar call (host code, like every per-element call) */
 QPK_API qpk_status qpk_field_op(qpk_field f, int op, const uint32_t* a, const uint32_t* b, uint64_t n, uint32_t* out);
+QPK_API qpk_status qpk_field_op1(qpk_field f, int op, uint32_t a, uint32_t b, uint32_t* out);
 /* fgdp_dot on reps (host, reference Alg. 4)     gfq.hpp:98-99, gfq.cpp:335-387 */
 QPK_API qpk_status qpk_fgdp_dot(qpk_field f, const uint32_t* v1, const uint32_t* v2, uint64_t n, uint32_t* out,
                                 qpk_cost* cost);

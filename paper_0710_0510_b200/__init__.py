@@ -115,6 +115,7 @@ SIGNATURES = {
     "qpk_field_describe": (I, [VP, C.c_char_p, U64]),
     "qpk_field_tables": (I, [VP, VP, VP, VP, VP, VP, VP]),
     "qpk_field_op": (I, [VP, I, VP, VP, U64, VP]),
+    "qpk_field_op1": (I, [VP, I, U32, U32, C.POINTER(C.c_uint32)]),
     "qpk_fgdp_dot": (I, [VP, VP, VP, U64, PU32, PCost]),
     "qpk_gfq_mul_batch": (I, [VP, VP, VP, U64, VP, I, VP]),
     "qpk_gfq_mul_batch_host": (I, [VP, VP, VP, U64, VP, I]),
@@ -392,11 +393,18 @@ class GfqField:
         return out
 
     def op(self, op, a, b=None):
+        """n elements on the device (qpk_field_op)."""
         a = _host(a, np.uint32).reshape(-1)
         bb = _host(b, np.uint32).reshape(-1) if b is not None else None
         out = np.empty_like(a)
         _check(lib().qpk_field_op(self._h, op, _ptr(a), _ptr(bb), a.size, _ptr(out)))
         return out
+
+    def op1(self, op, a, b=0):
+        """One element through the reference's scalar call (host)."""
+        r = C.c_uint32()
+        _check(lib().qpk_field_op1(self._h, op, int(a), int(b), C.byref(r)))
+        return r.value
 
     def mul(self, a, b):
         return self.op(0, a, b)

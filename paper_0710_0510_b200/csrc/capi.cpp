@@ -331,19 +331,28 @@ qpk_status qpk_field_op(qpk_field f, int op, const uint32_t* a, const uint32_t* 
         need(op >= 0 && op <= 3, "op must be 0..3");
         need(op >= 2 || n == 0 || b != nullptr, "binary op needs b");
         const auto& F = f->f;
-        for (uint64_t i = 0; i < n; ++i) {
-            const qpack::GfqElt x{a[i]};
-            qpack::GfqElt r;
-            if (op == 0)
-                r = F.mul(x, qpack::GfqElt{b[i]});
-            else if (op == 1)
-                r = F.add(x, qpack::GfqElt{b[i]});
-            else if (op == 2)
-                r = F.neg(x);
-            else
-                r = F.inverse(x);
-            out[i] = r.rep;
-        }
+        for (uint64_t i = 0; i < n; ++i)  // reps must name field elements (GfqElt contract)
+            need(a[i] < F.order() && (op >= 2 || b[i] < F.order()), "rep outside the field");
+        qpack::gpu::gfq_rep_op_host(qpack::detail::device_field(F), F, op, a, op < 2 ? b : nullptr, n, out);
+    });
+}
+
+qpk_status qpk_field_op1(qpk_field f, int op, uint32_t a, uint32_t b, uint32_t* out) {
+    return guard([&] {
+        need(f != nullptr && out != nullptr, "null argument");
+        need(op >= 0 && op <= 3, "op must be 0..3");
+        const auto& F = f->f;
+        const qpack::GfqElt x{a};
+        qpack::GfqElt r;
+        if (op == 0)
+            r = F.mul(x, qpack::GfqElt{b});
+        else if (op == 1)
+            r = F.add(x, qpack::GfqElt{b});
+        else if (op == 2)
+            r = F.neg(x);
+        else
+            r = F.inverse(x);
+        *out = r.rep;
     });
 }
 

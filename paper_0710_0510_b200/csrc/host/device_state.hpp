@@ -110,6 +110,8 @@ struct DevicePlanCache {
 struct DeviceFieldCache {
     gpu::DevBuf tables;  // lc | hc | log | alog  (u32)
     gpu::DevBuf fval;    // rep -> q-adic double
+    gpu::DevBuf zech;    // plus-one table (GfqField::add), uploaded on first use
+    gpu::DevBuf status;  // data-error flag of the rep ops (inverse of zero)
     qpk::GfqElemParams elem{};
     qpk::GfqMatmulParams mm{};
     qpk::GfqGemvParams gemv{};

@@ -618,6 +618,39 @@ void gfq_mul_rep_host(DeviceFieldCache& F, const uint32_t* a, const uint32_t* b,
     check(cudaMemcpy(out, dc.ptr, n * 4, cudaMemcpyDeviceToHost), "D2H");
 }
 
+// GfqField::mul / add / neg / inverse over host rep arrays, on the device
+void gfq_rep_op_host(DeviceFieldCache& F, const GfqField& field, int op, const uint32_t* a, const uint32_t* b, u64 n,
+                     uint32_t* out) {
+    if (n == 0) return;
+    std::lock_guard<std::mutex> lock(F.mu);
+    const u64 group = field.order() - 1;
+    if (op == 1 && !F.zech.ptr) {
+        const std::vector<u32>& z = detail::FieldAccess::zech(field);
+        F.zech.ensure(z.size() * 4);
+        check(cudaMemcpy(F.zech.ptr, z.data(), z.size() * 4, cudaMemcpyHostToDevice), "zech upload");
+    }
+    if (!F.status.ptr) {
+        F.status.ensure(4);
+        check(cudaMemset(F.status.ptr, 0, 4), "status clear");
+    }
+    F.io_a.ensure(n * 4);
+    F.io_b.ensure(n * 4);
+    F.io_c.ensure(n * 4);
+    check(cudaMemcpy(F.io_a.ptr, a, n * 4, cudaMemcpyHostToDevice), "H2D");
+    if (op < 2) check(cudaMemcpy(F.io_b.ptr, b, n * 4, cudaMemcpyHostToDevice), "H2D");
+    check(qpk::launch_gfq_rep_op(op, static_cast<uint32_t>(field.p()), static_cast<uint32_t>(group),
+                                 F.zech.as<uint32_t>(), F.io_a.as<uint32_t>(), F.io_b.as<uint32_t>(), n,
+                                 F.io_c.as<uint32_t>(), F.status.as<uint32_t>(), 0),
+          "gfq rep op launch");
+    check(cudaMemcpy(out, F.io_c.ptr, n * 4, cudaMemcpyDeviceToHost), "D2H");
+    uint32_t st = 0;
+    check(cudaMemcpy(&st, F.status.ptr, 4, cudaMemcpyDeviceToHost), "status read");
+    if (st) {
+        check(cudaMemset(F.status.ptr, 0, 4), "status clear");
+        throw std::domain_error("GfqField: zero has no inverse");
+    }
+}
+
 void gfq_mul_batch(std::span<const GfqElt> a, std::span<const GfqElt> b, const GfqField& field,
                    std::span<GfqElt> out) {
     if (a.size() != b.size() || out.size() < a.size()) throw std::invalid_argument("gfq_mul_batch: length mismatch");

@@ -45,6 +45,8 @@ void gfq_mul_device(detail::DeviceFieldCache& F, const uint8_t* a, const uint8_t
                     cudaStream_t s);
 void gfq_mul_host(detail::DeviceFieldCache& F, const uint8_t* a, const uint8_t* b, u64 n, uint8_t* out, int path);
 void gfq_mul_rep_host(detail::DeviceFieldCache& F, const uint32_t* a, const uint32_t* b, u64 n, uint32_t* out);
+void gfq_rep_op_host(detail::DeviceFieldCache& F, const GfqField& field, int op, const uint32_t* a, const uint32_t* b,
+                     u64 n, uint32_t* out);
 
 // repack: qpk::kRepackRedq (canonical REDQ re-pack) or qpk::kRepackFold
 uint32_t resolve_chunk(const detail::DeviceFieldCache& F, const GfqField& field, u64 K, uint32_t chunk,

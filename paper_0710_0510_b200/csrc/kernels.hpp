@@ -169,6 +169,11 @@ cudaError_t launch_gfq_gemv(const GfqGemvParams& P, const uint32_t* A, const uin
 // REDQ of u128 integer words ((lo, hi) u64 pairs, the reference's integer
 // mode up to q^(d+1) <= 2^128, redq.cpp:44-58): u128 arithmetic, direct
 // correction.  limit: q^(d+1) as (lo, hi), or 0/0 when it exceeds 2^128.
+// GfqField::mul / add / neg / inverse over reps (gfq.cpp:260-294), op 0..3;
+// add reads the Zech (plus-one) table zech[g+1] (zero sentinel g); inverse
+// of zero latches kErrDomain in *status
+cudaError_t launch_gfq_rep_op(int op, uint32_t p, uint32_t group, const uint32_t* zech, const uint32_t* a,
+                              const uint32_t* b, uint64_t n, uint32_t* out, uint32_t* status, cudaStream_t s);
 cudaError_t launch_redq_u128(const RedqParams& P, const uint64_t* words, uint64_t n, uint8_t* out, uint32_t* status,
                              cudaStream_t s);
 

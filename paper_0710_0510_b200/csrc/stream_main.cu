@@ -139,6 +139,39 @@ __global__ void redq_u128_kernel(const RedqParams P, const unsigned __int128* __
     report_g(err, status);
 }
 
+// field ops over reps (gfq.cpp:260-294); the zero element is rep g
+__global__ void gfq_rep_op_kernel(int op, uint32_t p, uint32_t group, const uint32_t* __restrict__ zech,
+                                  const uint32_t* __restrict__ a, const uint32_t* __restrict__ b, uint64_t n,
+                                  uint32_t* __restrict__ out, uint32_t* status) {
+    pdl_wait();
+    uint32_t err = 0;
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
+        const uint32_t x = a[i];
+        uint32_t r;
+        if (op == 0) {  // mul: (a + b) mod g, zero absorbs
+            const uint32_t y = b[i];
+            r = (x == group || y == group) ? group : (x + y >= group ? x + y - group : x + y);
+        } else if (op == 1) {  // add through the Zech table: a + plus1[(b - a) mod g]
+            const uint32_t y = b[i];
+            if (x == group) {
+                r = y;
+            } else if (y == group) {
+                r = x;
+            } else {
+                const uint32_t t = zech[y >= x ? y - x : y + group - x];
+                r = t == group ? group : (x + t >= group ? x + t - group : x + t);
+            }
+        } else if (op == 2) {  // neg: a + g/2 (p odd), identity for p = 2
+            r = (x == group || p == 2) ? x : (x + group / 2 >= group ? x + group / 2 - group : x + group / 2);
+        } else {  // inverse: (g - a) mod g
+            if (x == group) err |= kErrDomain;
+            r = x == 0 ? 0 : group - x;
+        }
+        out[i] = r;
+    }
+    report_g(err, status);
+}
+
 __global__ void gfq_mul_rep_kernel(uint32_t group, const uint32_t* __restrict__ a, const uint32_t* __restrict__ b,
                                    uint64_t n, uint32_t* __restrict__ out) {
     for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
@@ -213,6 +246,13 @@ cudaError_t launch_redq_u64(const RedqParams& P, const uint64_t* words, uint64_t
     if (P.d + 1 > uint32_t(kMaxDigits)) return cudaErrorInvalidValue;
     redq_u64_kernel<<<grid_for(n), 256, 0, s>>>(P, words, n, out, status);
     return cudaGetLastError();
+}
+
+cudaError_t launch_gfq_rep_op(int op, uint32_t p, uint32_t group, const uint32_t* zech, const uint32_t* a,
+                              const uint32_t* b, uint64_t n, uint32_t* out, uint32_t* status, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    if (op < 0 || op > 3) return cudaErrorInvalidValue;
+    return launch_pdl(gfq_rep_op_kernel, dim3(grid_for(n)), dim3(256), 0, s, op, p, group, zech, a, b, n, out, status);
 }
 
 cudaError_t launch_redq_u128(const RedqParams& P, const uint64_t* words, uint64_t n, uint8_t* out, uint32_t* status,
