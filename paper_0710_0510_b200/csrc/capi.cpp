@@ -332,7 +332,8 @@ qpk_status qpk_field_op(qpk_field f, int op, const uint32_t* a, const uint32_t* 
         need(op >= 2 || n == 0 || b != nullptr, "binary op needs b");
         const auto& F = f->f;
         for (uint64_t i = 0; i < n; ++i)  // reps must name field elements (GfqElt contract)
-            need(a[i] < F.order() && (op >= 2 || b[i] < F.order()), "rep outside the field");
+            if (a[i] >= F.order() || (op < 2 && b[i] >= F.order()))
+                throw std::out_of_range("GfqField: rep outside the field");
         qpack::gpu::gfq_rep_op_host(qpack::detail::device_field(F), F, op, a, op < 2 ? b : nullptr, n, out);
     });
 }
