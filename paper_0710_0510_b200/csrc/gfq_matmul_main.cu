@@ -62,33 +62,63 @@ __global__ void reps_to_coeffs_kernel(uint32_t k, const uint32_t* __restrict__ a
 // ---------------------------------------------------------------- K1 packs
 // 32x32 tiles through shared memory so both the record reads and the
 // (possibly transposed) double writes are coalesced.  KR (record width) is a
-// template parameter: unrolled byte loads and Horner steps, and the runtime
-// reduction mod p only for bytes >= p (ncu: the runtime-k loop with an
-// unconditional `% p` spent ~110 instructions per element, issue-bound at
-// 2.5 TB/s: 68 -> 55 us per C4 operand).
+// template parameter; a thread reads 4 records with one vector load and the
+// runtime reduction mod p runs only for bytes >= p (ncu: a runtime-k byte
+// loop with an unconditional `% p` spent ~110 instructions per element at
+// 2.5 TB/s: 68 -> 55 us per C4 operand with the template, less with the
+// vector loads).
 template <int KR>
 __global__ void pack_coeffs_kernel(uint32_t p, double qd, const uint8_t* __restrict__ src, uint64_t rows,
                                    uint64_t cols, double* __restrict__ dst, uint64_t ld, bool transpose) {
     __shared__ double tile[32][33];
     const uint64_t r0 = uint64_t(blockIdx.y) * 32, c0 = uint64_t(blockIdx.x) * 32;
     const int tx = threadIdx.x, ty = threadIdx.y;
-    const bool cin = c0 + tx < cols;
-    const uint8_t* base = src + (r0 * cols + c0 + tx) * KR;
+    // reads: each thread takes 4 consecutive records of one row (4 KR bytes,
+    // one vector load when aligned): 8 threads per row, 32 rows
+    {
+        const int lin = ty * 32 + tx, rr = lin >> 3, cc = (lin & 7) * 4;
+        const uint64_t r = r0 + rr, c = c0 + cc;
+        uint32_t x[4][KR];
+        const uint8_t* e = src + (r * cols + c) * KR;
+        const bool full = r < rows && c + 4 <= cols;
+        if (full && (reinterpret_cast<uintptr_t>(e) % (KR == 3 ? 4 : 4 * KR)) == 0) {
+            uint32_t w[KR];  // 4 KR bytes as KR words
+            if constexpr (KR == 1) {
+                w[0] = *reinterpret_cast<const uint32_t*>(e);
+            } else if constexpr (KR == 2) {
+                const uint2 v = *reinterpret_cast<const uint2*>(e);
+                w[0] = v.x, w[1] = v.y;
+            } else if constexpr (KR == 3) {
 #pragma unroll
-    for (int i = ty; i < 32; i += 8) {
-        double v = 0.0;
-        if (cin && r0 + i < rows) {
-            const uint8_t* e = base + uint64_t(i) * cols * KR;
-            uint32_t x[KR];
+                for (int t = 0; t < 3; ++t) w[t] = reinterpret_cast<const uint32_t*>(e)[t];
+            } else {
+                const uint4 v = *reinterpret_cast<const uint4*>(e);
+                w[0] = v.x, w[1] = v.y, w[2] = v.z, w[3] = v.w;
+            }
 #pragma unroll
-            for (int t = 0; t < KR; ++t) x[t] = e[t];
+            for (int j = 0; j < 4; ++j)
 #pragma unroll
-            for (int t = 0; t < KR; ++t)
-                if (x[t] >= p) x[t] %= p;  // unreduced bytes are reduced as from_coeffs does
+                for (int t = 0; t < KR; ++t) {
+                    const int byte = j * KR + t;
+                    x[j][t] = (w[byte >> 2] >> (8 * (byte & 3))) & 0xffu;
+                }
+        } else {
 #pragma unroll
-            for (int t = KR - 1; t >= 0; --t) v = fma(v, qd, static_cast<double>(x[t]));
+            for (int j = 0; j < 4; ++j)
+#pragma unroll
+                for (int t = 0; t < KR; ++t) x[j][t] = (r < rows && c + j < cols) ? e[j * KR + t] : 0u;
         }
-        tile[i][tx] = v;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            double v = 0.0;
+#pragma unroll
+            for (int t = KR - 1; t >= 0; --t) {
+                uint32_t xt = x[j][t];
+                if (xt >= p) xt %= p;  // unreduced bytes are reduced as from_coeffs does
+                v = fma(v, qd, static_cast<double>(xt));
+            }
+            tile[rr][cc + j] = v;
+        }
     }
     __syncthreads();
 #pragma unroll
