@@ -7,7 +7,8 @@
 //    accumulators in registers;
 //  * a producer warp streams 16-deep K slices of A^T and B with TMA bulk
 //    copies (one 1 KB row per lane) into padded shared rows (conflict-free
-//    fragment loads), 4-stage full/empty mbarrier pipeline.  (Measured on
+//    fragment loads), full/empty mbarrier pipeline (6 stages on the fast paths,
+//    4 on the generic kernels).  (Measured on
 //    B200, scripts/mm_variants.cu: the dedicated producer sustains 35.6
 //    TFLOP/s = 96% of the DMMA probe; letting the last consumer warp refill
 //    a stage instead reaches only 26.8 -- that warp becomes a straggler.);
@@ -17,7 +18,12 @@
 //    outside the stage loop (so they are never predicated into every stage)
 //    and staggered so the two consumer warps of an SM sub-partition never
 //    re-pack in the same stage: one warp's integer work overlaps the other
-//    warp's MMAs;
+//    warp's MMAs.  On the fast paths (p = 3, q = 2^(2m)) the accumulators
+//    carry a 2^52 bias so the word is the accumulator's mantissa, and the
+//    re-pack is integer-only: the SWAR REDQ (floor(r/3) by div3_u64) or,
+//    with repack = fold, a congruent lane fold (7 instructions);
+//  * the REDQ-re-pack kernel walks tiles in groups of 8 tile rows (L2 reuse
+//    of B), the fold kernel row-major (measured best for each);
 //  * epilogue: final REDQ digits -> low/high half tables in coefficient form
 //    (gfq.cpp:218-248) -> bytes, or -> rep through the log table.
 //
