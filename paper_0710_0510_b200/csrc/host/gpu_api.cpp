@@ -185,8 +185,12 @@ DeviceFieldCache& device_field(const GfqField& f) {
     // re-indexed by the 9-bit hash of the digit bytes (kernels.hpp kHash9)
     const bool bin = p <= 8 && k == 3;
     const u64 base_words = 2 * nlh + 2 * order;
+    // the hash-indexed blocks start 16-byte aligned (cp.async staging)
+    const u64 bin_off = (base_words + 3) / 4 * 4;
     const u64 group = order - 1;
-    const u64 words = base_words + (bin ? 3 * 512 + 2 * group : 0);
+    const u64 bin_words = (3 * 512 + 2 * group + 3) / 4 * 4;
+    const u64 nc = qpk::kDlogCopies;
+    const u64 words = bin ? bin_off + bin_words + nc * (512 + 2 * group) : base_words;
     if (words * 4 > 96 * 1024)
         throw std::invalid_argument("qpack-b200 GF(p^k): field tables exceed the shared-memory budget");
     // coefficient-form tables: rep -> packed coefficient bytes
@@ -206,7 +210,7 @@ DeviceFieldCache& device_field(const GfqField& f) {
         host[2 * nlh + order + i] = bytes_of(static_cast<u32>(i));
     }
     if (bin) {
-        uint32_t* hl = host.data() + base_words;
+        uint32_t* hl = host.data() + bin_off;
         uint32_t* hh = hl + 512;
         uint32_t* hg = hl + 1024;
         uint32_t* al2 = hl + 1536;
@@ -225,6 +229,12 @@ DeviceFieldCache& device_field(const GfqField& f) {
                 }
         for (u64 i = 0; i + 1 < 2 * group; ++i) al2[i] = bytes_of(static_cast<u32>(i % group));
         al2[2 * group - 1] = 0;
+        uint32_t* lgR = hl + bin_words;
+        uint32_t* alR = lgR + nc * 512;
+        for (u64 c = 0; c < nc; ++c) {
+            for (u64 h = 0; h < 512; ++h) lgR[h * nc + c] = static_cast<uint32_t>(nc * hg[h]);
+            for (u64 i = 0; i < 2 * group; ++i) alR[i * nc + c] = al2[i];
+        }
     }
     c->tables.ensure(words * 4);
     check(cudaMemcpy(c->tables.ptr, host.data(), words * 4, cudaMemcpyHostToDevice), "field tables upload");
@@ -248,7 +258,8 @@ DeviceFieldCache& device_field(const GfqField& f) {
     E.log = tb + 2 * nlh;
     E.alog = tb + 2 * nlh + order;
     E.tables_words = static_cast<uint32_t>(words);
-    E.bin_off = bin ? static_cast<uint32_t>(base_words) : 0u;
+    E.bin_off = bin ? static_cast<uint32_t>(bin_off) : 0u;
+    E.dlog_off = bin ? static_cast<uint32_t>(bin_off + bin_words) : 0u;
     if (k == 3) {
         const std::vector<u64> xv = {0, 1, 0};
         const GfqElt x = f.from_coeffs(xv);

@@ -56,6 +56,13 @@ struct PolymulParams {
 constexpr uint32_t kHash9 = 13115393u;
 constexpr uint32_t hash9_host(uint32_t y) { return ((y * kHash9) & 0xffffffu) >> 15; }
 
+// The dlog path of those fields reads its log and antilog tables from
+// kDlogCopies interleaved copies (entry e, copy c at word e*kDlogCopies + c);
+// lane l reads copy l mod kDlogCopies, so only the 32/kDlogCopies lanes of
+// one copy share its 32/kDlogCopies banks (random lookups: ~2 wavefronts
+// per warp-wide load instead of ~3.5 over one copy).
+constexpr uint32_t kDlogCopies = 8;
+
 // GF(p^k) elementwise product (config 3).
 struct GfqElemParams {
     RedqParams rq;          // d = 2k-2, mode float
@@ -69,6 +76,9 @@ struct GfqElemParams {
     uint32_t bin_off;       // word offset of the hash-indexed tables (p <= 8, k = 3), else 0:
                             //   lcH[512] | hcH[512] | logH[512] (4*log, zero -> 4*(2g-1)) | alog2[2g]
                             //   alog2[i] = coefficients of rep i mod g (i < 2g-1), alog2[2g-1] = 0
+    uint32_t dlog_off;      // word offset of the interleaved dlog block (hash-indexed fields), else 0:
+                            //   logR[512 * kDlogCopies] (4*kDlogCopies*log, zero -> 4*kDlogCopies*(2g-1))
+                            //   | alogR[2g * kDlogCopies] (alog2 interleaved)
     uint32_t col3, col4;    // k = 3: coefficient bytes of x^3 and x^4 mod the field polynomial
     int mode;               // 0 packed (DQT/REDQ/L-H), 1 dlog/Zech
 };

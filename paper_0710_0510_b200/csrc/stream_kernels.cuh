@@ -274,9 +274,11 @@ __device__ __forceinline__ uint32_t lh_product_hash(const C&, double inv_p, uint
 // dlog product on hash-indexed tables: logH holds 4*log (zero -> 4*(2g-1)),
 // so rep(a) + rep(b) indexes the doubled antilog table with no reduction
 // mod g, and any sum involving zero clamps to its zero entry (gfq.cpp:260-264)
+// (stride = kDlogCopies on the interleaved copies: logH and alog2 already
+// point at this lane's copy and the logs are pre-scaled by the stride)
 __device__ __forceinline__ uint32_t dlog_product_hash(uint32_t ya, uint32_t yb, uint32_t logH, uint32_t alog2,
-                                                      uint32_t zero4) {
-    const uint32_t s = lds_u32(logH + 4 * hash9(ya)) + lds_u32(logH + 4 * hash9(yb));
+                                                      uint32_t zero4, uint32_t stride) {
+    const uint32_t s = lds_u32(logH + 4 * stride * hash9(ya)) + lds_u32(logH + 4 * stride * hash9(yb));
     return lds_u32(alog2 + min(s, zero4));
 }
 
@@ -381,11 +383,19 @@ struct GfqElemOp {
     // hash-indexed fast path (GF(p^3), p < 8, q = 2^8) when the host built its tables
     static constexpr bool kHashable = K_ == 3 && ct_small_p<K>() && R % 4 == 0;
     __host__ __device__ bool hashed() const { return kHashable && P.bin_off != 0; }
-    // staged tables: lc|hc|log|alog, or only the hash-indexed block
-    __host__ __device__ uint32_t tables_words() const { return P.tables_words - (hashed() ? P.bin_off : 0u); }
-    __host__ __device__ const uint32_t* tables_src() const { return P.lc + (hashed() ? P.bin_off : 0u); }
-
-    __device__ __forceinline__ bool packed() const { return MODE < 0 ? P.mode == 0 : MODE == 0; }
+    __host__ __device__ __forceinline__ bool packed() const { return MODE < 0 ? P.mode == 0 : MODE == 0; }
+    // dlog products on the hash-indexed fields read the interleaved copies
+    __host__ __device__ bool dlog_copies() const { return hashed() && !packed() && P.dlog_off != 0; }
+    // staged tables: lc|hc|log|alog, the hash-indexed block, or (dlog) only
+    // the interleaved log/antilog copies
+    __host__ __device__ uint32_t tables_words() const {
+        if (dlog_copies()) return P.tables_words - P.dlog_off;
+        const uint32_t end = P.dlog_off ? P.dlog_off : P.tables_words;  // the copies are dlog-only
+        return hashed() ? end - P.bin_off : P.bin_off ? P.bin_off : P.tables_words;
+    }
+    __host__ __device__ const uint32_t* tables_src() const {
+        return P.lc + (dlog_copies() ? P.dlog_off : hashed() ? P.bin_off : 0u);
+    }
 
     // groups of 4 records = 3 packed words
     __device__ __forceinline__ void apply_hashed(const uint32_t* a, const uint32_t* b, uint32_t (&ow)[R * OUT / 4],
@@ -419,7 +429,13 @@ struct GfqElemOp {
                 return;
             }
         }
-        const uint32_t zero4 = 4 * (2 * P.group - 1);
+        const bool copies = dlog_copies();
+        const uint32_t zero4 = 4 * (2 * P.group - 1) * (copies ? kDlogCopies : 1u);
+        // interleaved copies: this lane's copy offset; the log block is 512 entries
+        const uint32_t lane4 = copies ? 4 * (threadIdx.x % kDlogCopies) : 0u;
+        const uint32_t logb = copies ? tab + lane4 : tab + 4096;
+        const uint32_t alogb = copies ? tab + 4 * 512 * kDlogCopies + lane4 : tab + 6144;
+        const uint32_t stride = copies ? kDlogCopies : 1u;
 #pragma unroll
         for (int g = 0; g < R / 4; ++g) {
             uint32_t res[4];
@@ -429,7 +445,7 @@ struct GfqElemOp {
                 if (packed()) {
                     res[r] = lh_product_hash(c, P.rq.inv_p, ya & 0xffffffu, yb & 0xffffffu, tab, tab + 2048);
                 } else {
-                    res[r] = dlog_product_hash(ya, yb, tab + 4096, tab + 6144, zero4);
+                    res[r] = dlog_product_hash(ya, yb, logb, alogb, zero4, stride);
                 }
             }
             ow[3 * g] = res[0] | (res[1] << 24);
