@@ -576,7 +576,8 @@ __device__ __forceinline__ void report(uint32_t err, uint32_t* status) {
 // ASYNC: 16-byte cp.async copies (the TMA kernel, where a CTA streams for
 // tens of microseconds); the one-pass direct/tail kernels keep the plain
 // loop (measured: cp.async cost C1's hot launch 6.31 -> 6.65 us)
-template <class Op, bool ASYNC = true>
+// WAIT = false leaves the cp.async copies in flight (the caller waits)
+template <class Op, bool ASYNC = true, bool WAIT = true>
 __device__ __forceinline__ void stage_tables(const Op& op, uint32_t* dst) {
     // 16-byte cp.async copies, every one in flight at once (a per-thread
     // load/store loop serialises one L2 round trip per 256 words: measured
@@ -592,7 +593,7 @@ __device__ __forceinline__ void stage_tables(const Op& op, uint32_t* dst) {
         head = 4 * n4;
     }
     for (uint32_t i = head + threadIdx.x; i < nt; i += blockDim.x) dst[i] = src[i];
-    if (ASYNC) asm volatile("cp.async.wait_all;" ::: "memory");
+    if (ASYNC && WAIT) asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
 template <class Op>
@@ -617,14 +618,17 @@ __global__ void __launch_bounds__(kThreads) stream_tma_kernel(const Op op, const
         bulk_g2s_stream(dst, in0 + tile * G::B0, G::B0, &bars[s], policy);
         if constexpr (G::B1 > 0) bulk_g2s_stream(dst + G::B0, in1 + tile * G::B1, G::B1, &bars[s], policy);
     };
-    // thread 0 puts the first S tiles in flight before the table staging,
-    // so the per-CTA table copy overlaps the first loads; barrier setup runs
-    // before pdl_wait, overlapping the previous kernel's tail
+    // barrier setup and the table staging run before pdl_wait, overlapping
+    // the previous kernel's tail: the tables are plan constants, uploaded
+    // when the plan or field was built, never written by a preceding launch;
+    // thread 0 then puts the first S tiles in flight while the table copies
+    // complete
     if (tid == 0) {
         for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
         fence_mbar_init();
         policy = policy_evict_first();
     }
+    stage_tables<Op, true, false>(op, s_tab);
     pdl_wait();
     if (tid == 0) {
         for (int s = 0; s < S; ++s) {
@@ -632,7 +636,7 @@ __global__ void __launch_bounds__(kThreads) stream_tma_kernel(const Op op, const
             if (t < n_tiles) issue(s, t);
         }
     }
-    stage_tables(op, s_tab);
+    asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
 
     uint32_t err = 0;
