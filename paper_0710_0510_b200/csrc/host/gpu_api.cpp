@@ -83,6 +83,13 @@ namespace qpack::detail {
 
 using gpu::check;
 
+// Plan/field constants and status words are written by cudaMemcpy/cudaMemset
+// on the legacy stream; a pageable cudaMemcpy may return before its DMA lands
+// and cudaMemset is asynchronous, while the kernels that read them run on the
+// caller's (possibly non-blocking) stream -- and the stream kernels stage
+// their tables before the PDL wait.  Wait for those writes once, at build.
+void settle_uploads() { check(cudaStreamSynchronize(nullptr), "upload sync"); }
+
 qpk::RedqParams make_redq_params(const RedqPlan& plan, gpu::DevBuf* table) {
     if (plan.p > 256) throw std::invalid_argument("qpack-b200 REDQ: residues are emitted as uint8, p must be <= 256");
     if (plan.d + 1 > static_cast<unsigned>(qpk::kMaxDigits))
@@ -152,6 +159,7 @@ DevicePlanCache& device_plan(const RedqPlan& plan) {
         c->prm = make_redq_params(plan, &c->table);
         c->status.ensure(4);
         check(cudaMemset(c->status.ptr, 0, 4), "status init");
+        settle_uploads();
         plan.device = std::move(c);
     }
     return *plan.device;
@@ -240,6 +248,7 @@ DeviceFieldCache& device_field(const GfqField& f) {
     check(cudaMemcpy(c->tables.ptr, host.data(), words * 4, cudaMemcpyHostToDevice), "field tables upload");
     c->fval.ensure(order * 8);
     check(cudaMemcpy(c->fval.ptr, FieldAccess::fval(f).data(), order * 8, cudaMemcpyHostToDevice), "fval upload");
+    settle_uploads();
     c->nlh = static_cast<uint32_t>(nlh);
 
     const RedqPlan digits = RedqPlan::build(p, FieldAccess::q(f), 2 * k - 2, RedqMode::integer);
@@ -304,7 +313,10 @@ uint32_t take_status(DevicePlanCache& dp, cudaStream_t s) {
     check(cudaStreamSynchronize(s), "stream sync");
     uint32_t st = 0;
     check(cudaMemcpy(&st, dp.status.ptr, 4, cudaMemcpyDeviceToHost), "status read");
-    if (st) check(cudaMemset(dp.status.ptr, 0, 4), "status clear");
+    if (st) {
+        check(cudaMemset(dp.status.ptr, 0, 4), "status clear");
+        detail::settle_uploads();
+    }
     return st;
 }
 
@@ -639,10 +651,12 @@ void gfq_rep_op_host(DeviceFieldCache& F, const GfqField& field, int op, const u
         const std::vector<u32>& z = detail::FieldAccess::zech(field);
         F.zech.ensure(z.size() * 4);
         check(cudaMemcpy(F.zech.ptr, z.data(), z.size() * 4, cudaMemcpyHostToDevice), "zech upload");
+        detail::settle_uploads();
     }
     if (!F.status.ptr) {
         F.status.ensure(4);
         check(cudaMemset(F.status.ptr, 0, 4), "status clear");
+        detail::settle_uploads();
     }
     F.io_a.ensure(n * 4);
     F.io_b.ensure(n * 4);
