@@ -61,7 +61,10 @@ constexpr uint32_t hash9_host(uint32_t y) { return ((y * kHash9) & 0xffffffu) >>
 // lane l reads copy l mod kDlogCopies, so only the 32/kDlogCopies lanes of
 // one copy share its 32/kDlogCopies banks (random lookups: ~2 wavefronts
 // per warp-wide load instead of ~3.5 over one copy).
-constexpr uint32_t kDlogCopies = 8;
+#ifndef QPK_DLOG_COPIES
+#define QPK_DLOG_COPIES 8
+#endif
+constexpr uint32_t kDlogCopies = QPK_DLOG_COPIES;
 
 // GF(p^k) elementwise product (config 3).
 struct GfqElemParams {
