@@ -34,7 +34,10 @@ namespace qpk {
 namespace {
 
 constexpr int kGemvThreads = 256;
-constexpr int kGemvUnroll = 4;     // 16-byte loads of A in flight per lane
+#ifndef QPK_GEMV_UNROLL
+#define QPK_GEMV_UNROLL 4
+#endif
+constexpr int kGemvUnroll = QPK_GEMV_UNROLL;  // 16-byte loads of A in flight per lane
 constexpr uint32_t kReplMax = 64;  // replicate the value table up to this order (8 KB)
 constexpr uint64_t kXrepRows = 4;  // up to this many rows x is looked up per use
 
