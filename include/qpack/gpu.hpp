@@ -36,7 +36,11 @@ void redq_residues_batch(std::span<const u128> words, const RedqPlan& plan, std:
 void polymul_batch(std::span<const std::uint8_t> a, std::span<const std::uint8_t> b, const QadicParams& params,
                    std::span<std::uint8_t> out, CostReport* cost = nullptr);
 
-enum class GfqPath { packed = 0, dlog = 1 };
+// packed: DQT pack, fp64 product, REDQ, L/H tables (gfq.cpp:353-384);
+// dlog: GfqField::mul on the Zech/discrete-log representation (gfq.cpp:260-264);
+// linear: GF(7^3) at q = 2^8 only -- integer word product and lane-wise mod 7
+// through x^3, x^4 (an extra; every other field runs `packed`)
+enum class GfqPath { packed = 0, dlog = 1, linear = 2 };
 
 // elementwise GF(p^k) products of coefficient records (k bytes each)
 void gfq_mul_batch(std::span<const std::uint8_t> a, std::span<const std::uint8_t> b, const GfqField& field,

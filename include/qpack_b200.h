@@ -148,7 +148,9 @@ QPK_API qpk_status qpk_fgdp_dot(qpk_field f, const uint32_t* v1, const uint32_t*
 
 /* elementwise products of k-byte coefficient records (K3)
  * path 0 = DQT/REDQ/L-H   (fgdp_dot on length-1 vectors, gfq.cpp:335-387)
- * path 1 = dlog/Zech      (GfqField::mul, gfq.cpp:260-264)                */
+ * path 1 = dlog/Zech      (GfqField::mul, gfq.cpp:260-264)
+ * path 2 = linear         (GF(7^3) at q = 2^8: integer word product, lane-wise
+ *                          mod 7 through x^3, x^4; other fields run path 0)  */
 QPK_API qpk_status qpk_gfq_mul_batch(qpk_field f, const uint8_t* a, const uint8_t* b, uint64_t n, uint8_t* out,
                                      int path, void* stream);
 QPK_API qpk_status qpk_gfq_mul_batch_host(qpk_field f, const uint8_t* a, const uint8_t* b, uint64_t n,

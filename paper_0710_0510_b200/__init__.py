@@ -328,7 +328,7 @@ class PolymulPlan:
 
 
 # ------------------------------------------------------------- GF(p^k)
-PACKED, DLOG = 0, 1
+PACKED, DLOG, LINEAR = 0, 1, 2
 
 
 class GfqField:

@@ -374,7 +374,7 @@ qpk_status qpk_gfq_mul_batch(qpk_field f, const uint8_t* a, const uint8_t* b, ui
                              void* stream) {
     return guard([&] {
         need(f != nullptr && (n == 0 || (a && b && out)), "null argument");
-        need(path == 0 || path == 1, "path must be 0 (packed) or 1 (dlog)");
+        need(path >= 0 && path <= 2, "path must be 0 (packed), 1 (dlog) or 2 (linear)");
         qpack::gpu::gfq_mul_device(qpack::detail::device_field(f->f), a, b, n, out, path, as_stream(stream));
     });
 }
@@ -383,7 +383,7 @@ qpk_status qpk_gfq_mul_batch_host(qpk_field f, const uint8_t* a, const uint8_t* 
                                   int path) {
     return guard([&] {
         need(f != nullptr && (n == 0 || (a && b && out)), "null argument");
-        need(path == 0 || path == 1, "path must be 0 (packed) or 1 (dlog)");
+        need(path >= 0 && path <= 2, "path must be 0 (packed), 1 (dlog) or 2 (linear)");
         qpack::gpu::gfq_mul_host(qpack::detail::device_field(f->f), a, b, n, out, path);
     });
 }

@@ -198,8 +198,14 @@ DeviceFieldCache& device_field(const GfqField& f) {
     const u64 group = order - 1;
     const u64 bin_words = (3 * 512 + 2 * group + 3) / 4 * 4;
     const u64 nc = qpk::kDlogCopies;
-    const u64 words = bin ? bin_off + bin_words + nc * (512 + 2 * group) : base_words;
-    if (words * 4 > 96 * 1024)
+    const u64 lh_off = bin_off + bin_words + nc * (512 + 2 * group);
+    const u64 p3 = p * p * p;
+    const u64 lh_words = (p3 + 1) / 2 + p3;
+    const u64 words = bin ? lh_off + lh_words : base_words;
+    // a launch stages the block its path reads (hash-indexed fields: the L/H
+    // or the dlog copies; else every table)
+    const u64 staged = bin ? std::max(nc * (512 + 2 * group), 32 * lh_words) : base_words;
+    if (staged * 4 > 96 * 1024)
         throw std::invalid_argument("qpack-b200 GF(p^k): field tables exceed the shared-memory budget");
     // coefficient-form tables: rep -> packed coefficient bytes
     auto bytes_of = [&](u32 rep) {
@@ -243,6 +249,20 @@ DeviceFieldCache& device_field(const GfqField& f) {
             for (u64 h = 0; h < 512; ++h) lgR[h * nc + c] = static_cast<uint32_t>(nc * hg[h]);
             for (u64 i = 0; i < 2 * group; ++i) alR[i * nc + c] = al2[i];
         }
+        // compact L|H block at the base-p index of three digits: L (degree < 2:
+        // coefficient bytes 0, 1) as u16, then H as u32 coefficient bytes (the
+        // kernel makes 32 lane-private copies)
+        auto* l16 = reinterpret_cast<uint16_t*>(host.data() + lh_off);
+        uint32_t* h32 = host.data() + lh_off + (p3 + 1) / 2;
+        for (u64 d2 = 0; d2 < p; ++d2)
+            for (u64 d1 = 0; d1 < p; ++d1)
+                for (u64 d0 = 0; d0 < p; ++d0) {
+                    const u64 lh_idx = d0 + lh * (d1 + lh * d2);
+                    const u64 e = d0 + p * (d1 + p * d2);
+                    if (host[lh_idx] >> 16) throw std::logic_error("qpack-b200: low-half table entry of degree >= 2");
+                    l16[e] = static_cast<uint16_t>(host[lh_idx]);
+                    h32[e] = host[nlh + lh_idx];
+                }
     }
     c->tables.ensure(words * 4);
     check(cudaMemcpy(c->tables.ptr, host.data(), words * 4, cudaMemcpyHostToDevice), "field tables upload");
@@ -269,6 +289,7 @@ DeviceFieldCache& device_field(const GfqField& f) {
     E.tables_words = static_cast<uint32_t>(words);
     E.bin_off = bin ? static_cast<uint32_t>(bin_off) : 0u;
     E.dlog_off = bin ? static_cast<uint32_t>(bin_off + bin_words) : 0u;
+    E.lh_off = bin ? static_cast<uint32_t>(lh_off) : 0u;
     if (k == 3) {
         const std::vector<u64> xv = {0, 1, 0};
         const GfqElt x = f.from_coeffs(xv);
@@ -590,6 +611,8 @@ void polymul_batch(std::span<const std::uint8_t> a, std::span<const std::uint8_t
 void gfq_mul_device(DeviceFieldCache& F, const uint8_t* a, const uint8_t* b, u64 n, uint8_t* out, int path,
                     cudaStream_t s) {
     qpk::GfqElemParams E = F.elem;
+    if (path < qpk::kGfqPacked || path > qpk::kGfqLinear)
+        throw std::invalid_argument("gfq_mul: path must be 0 (packed), 1 (dlog) or 2 (linear)");
     E.mode = path;
     check(qpk::launch_gfq_elem(E, a, b, n, out, s), "gfq_mul launch");
 }

@@ -65,6 +65,11 @@ constexpr uint32_t hash9_host(uint32_t y) { return ((y * kHash9) & 0xffffffu) >>
 #define QPK_DLOG_COPIES 8
 #endif
 constexpr uint32_t kDlogCopies = QPK_DLOG_COPIES;
+// GF elementwise product paths (qpk_gfq_mul_batch `path`)
+constexpr int kGfqPacked = 0;  // DQT pack, fp64 product, REDQ, L/H tables (gfq.cpp:353-384)
+constexpr int kGfqDlog = 1;    // dlog/Zech representation (gfq.cpp:260-264)
+constexpr int kGfqLinear = 2;  // GF(7^3), q = 2^8 only: integer word product + lane-wise mod 7 (an extra;
+                               // other fields run kGfqPacked)
 
 // GF(p^k) elementwise product (config 3).
 struct GfqElemParams {
@@ -82,8 +87,11 @@ struct GfqElemParams {
     uint32_t dlog_off;      // word offset of the interleaved dlog block (hash-indexed fields), else 0:
                             //   logR[512 * kDlogCopies] (4*kDlogCopies*log, zero -> 4*kDlogCopies*(2g-1))
                             //   | alogR[2g * kDlogCopies] (alog2 interleaved)
+    uint32_t lh_off;        // word offset of the compact L|H block (hash-indexed fields), else 0:
+                            //   at the base-p index of three digits, L as p^3 u16 (coefficient
+                            //   bytes 0, 1; padded to whole words), then H as p^3 u32
     uint32_t col3, col4;    // k = 3: coefficient bytes of x^3 and x^4 mod the field polynomial
-    int mode;               // 0 packed (DQT/REDQ/L-H), 1 dlog/Zech
+    int mode;               // kGfqPacked, kGfqDlog or kGfqLinear
 };
 
 // GF(p^k) matrix product (configs 4/5).

@@ -210,4 +210,11 @@ __device__ __forceinline__ uint32_t lds_u32(uint32_t saddr) {
     return v;
 }
 
+// shared-memory u16 load (zero-extended)
+__device__ __forceinline__ uint32_t lds_u16(uint32_t saddr) {
+    unsigned short v;
+    asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(saddr));
+    return v;
+}
+
 }  // namespace qpk

@@ -24,6 +24,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <type_traits>
 
 #include "device_common.cuh"
 #include "kernels.hpp"
@@ -32,6 +33,8 @@
 namespace qpk {
 
 namespace {
+
+constexpr int kThreads = 256;  // threads per CTA of the stream kernels (default)
 
 // records -> contiguous byte stream -> u32 words (all indices constexpr)
 template <int R, int OUT>
@@ -251,24 +254,46 @@ __device__ __forceinline__ uint32_t bytes_mod_p(uint32_t w, uint32_t p, uint32_t
     return r;
 }
 
-// GF(p^k) product for q = 2^8, k = 3, p < 8, all REDQ digits in one
-// register: u_i in [0, p-1] is fixed by its value mod 8 and
-// u_i = (w >> 8i) - p (rop >> 8i) == a_i + (-p mod 8) b_i (mod 8) with a_i, b_i
-// the low 3 bits of byte i of w and rop -- one masked multiply-add gives the
-// five digits as byte lanes (no lane carries: 7 + 7*7 < 256), and the L/H
-// tables are read at the 9-bit hash of digit lanes 0..2 and 2..4.
+// GF(p^k) product for q = 2^8, k = 3, p < 8 through the reference's
+// pipeline (gfq.cpp:353-384 with one term): DQT pack, fp64 product, REDQ,
+// L/H tables.  A record of 3 coefficient bytes IS its DQT word at q = 2^8
+// (dqt.cpp:23-37), exact as a double; the fp64 product is exact (< 2^48).
+// REDQ: rop = floor(r/p) by the premultiplied reciprocal (Lemma 1, RU
+// multiply + RZ magic add), then the raw digits u_i = (r >> 8i) - p (rop >> 8i)
+// (redq.cpp:31-60).  u_i in [0, p-1] is fixed by its value mod 8, i.e. by the
+// low 3 bits of byte i of r and rop: u_i == a_i + (-p mod 8) b_i (mod 8) --
+// one masked multiply-add gives all five digits as byte lanes (no lane
+// carries: 7 + 7*7 < 256).  The L and H tables are indexed by the base-p
+// value of digit lanes 0..2 and 2..4 (one dp4a each; lane 3 has weight 0)
+// in this lane's private copies (every lookup of a warp is one
+// conflict-free wavefront): L as u16 (its low half has degree < k-1 = 2, so
+// two coefficient bytes), entry e at byte 128 (e >> 1) + 2 (e & 1) + 4 lane;
+// H as u32 coefficient bytes at byte hoff + 128 e + 4 lane.
 template <class C>
-__device__ __forceinline__ uint32_t lh_product_hash(const C&, double inv_p, uint32_t ra, uint32_t rb, uint32_t lcH,
-                                                    uint32_t hcH) {
-    constexpr uint32_t F = (8u - C::kP % 8u) % 8u;
-    const uint64_t w = static_cast<uint64_t>(ra) * rb;  // the DQT word product, exact (< 2^48)
-    const double wd = __hiloint2double(0x43300000 | static_cast<int>(w >> 32), static_cast<int>(w)) - kTwo52;
-    const uint64_t ob = dbits(__dadd_rz(__dmul_ru(wd, inv_p), kTwo52));  // low 52 bits: floor(w/p)
-    const uint32_t lo = (static_cast<uint32_t>(w) & 0x07070707u) + (static_cast<uint32_t>(ob) & 0x07070707u) * F;
-    const uint32_t hi = static_cast<uint32_t>(w >> 32) + static_cast<uint32_t>(ob >> 32) * F;  // lane 0: digit 4
-    const uint32_t il = hash9(lo & 0x07070707u);
-    const uint32_t ih = hash9(__funnelshift_r(lo, hi, 16) & 0x07070707u);
-    return add_mod_bytes_fast(lds_u32(lcH + 4 * il), lds_u32(hcH + 4 * ih), C::kP);
+__device__ __forceinline__ uint32_t lh_product_lane(double inv_p, uint32_t ra, uint32_t rb, uint32_t tb,
+                                                    uint32_t hb) {
+    constexpr uint32_t P = C::kP;
+    constexpr uint32_t F = (8u - P % 8u) % 8u;
+    constexpr uint32_t kWeights = 1u | (P << 8) | (P * P << 16);
+    // the packed words as doubles (exact magic-add conversions) and their product
+    // (I2F.F64 conversions measured 34.6 vs 34.1 us per C3 launch)
+    const double wa = __hiloint2double(0x43300000, static_cast<int>(ra)) - kTwo52;
+    const double wb = __hiloint2double(0x43300000, static_cast<int>(rb)) - kTwo52;
+    const double r = wa * wb;
+    const uint64_t rw = dbits(r + kTwo52);                             // low 52 bits: r as an integer
+    const uint64_t ob = dbits(__dadd_rz(__dmul_ru(r, inv_p), kTwo52));  // low 52 bits: floor(r/p)
+    const uint32_t lo = (static_cast<uint32_t>(rw) & 0x07070707u) + (static_cast<uint32_t>(ob) & 0x07070707u) * F;
+    const uint32_t hi = static_cast<uint32_t>(rw >> 32) + static_cast<uint32_t>(ob >> 32) * F;  // lane 0: digit 4
+    const uint32_t il = __dp4a(lo & 0x07070707u, kWeights, 0u);
+    const uint32_t ih = __dp4a(__funnelshift_r(lo, hi, 16) & 0x07070707u, kWeights, 0u);
+    const uint32_t lv = lds_u16(tb + (il << 6) - (il & 1u) * 62u);
+    const uint32_t hv = lds_u32(hb + (ih << 7));
+    return lv + hv;  // coefficient lanes < 2p: the caller reduces them mod p (bytes_below_2p_mod)
+}
+
+// bytewise t mod p for byte lanes below 2p <= 128 (carry-free)
+__device__ __forceinline__ uint32_t bytes_below_2p_mod(uint32_t t, uint32_t p) {
+    return t - p * (((t + (128u - p) * 0x01010101u) >> 7) & 0x01010101u);
 }
 
 // dlog product on hash-indexed tables: logH holds 4*log (zero -> 4*(2g-1)),
@@ -374,27 +399,75 @@ __device__ __forceinline__ uint32_t dlog_product(const C&, uint32_t ia, uint32_t
 #ifndef QPK_GFE_S
 #define QPK_GFE_S 2
 #endif
-// MODE: 0 packed, 1 dlog as a compile-time choice (fast paths), -1 = P.mode
+// MODE: kGfqPacked / kGfqDlog / kGfqLinear as a compile-time choice (fast
+// paths), -1 = P.mode
+#ifndef QPK_GFE_PK_RR  // ... and of the hash-indexed REDQ/L-H path (lane-private tables, 66 KB:
+#define QPK_GFE_PK_RR 1   //     smaller tiles keep two CTAs per SM)
+#endif
+#ifndef QPK_GFE_PK_S
+#define QPK_GFE_PK_S 2
+#endif
+#ifndef QPK_GFE_PK_T
+#define QPK_GFE_PK_T 256
+#endif
 template <int K_, class K, int MODE = -1>
 struct GfqElemOp {
     static constexpr int ND = 2 * K_ - 1;
-    static constexpr int IN0 = K_, IN1 = K_, OUT = K_, R = QPK_GFE_R, RR = QPK_GFE_RR, S = QPK_GFE_S;
-    GfqElemParams P;
+    static constexpr int IN0 = K_, IN1 = K_, OUT = K_, R = QPK_GFE_R;
     // hash-indexed fast path (GF(p^3), p < 8, q = 2^8) when the host built its tables
     static constexpr bool kHashable = K_ == 3 && ct_small_p<K>() && R % 4 == 0;
+    static constexpr uint32_t kP3 = [] {
+        if constexpr (kHashable) return K::kP * K::kP * K::kP;
+        else return 0u;
+    }();
+    static constexpr bool kLinear = [] {
+        if constexpr (kHashable) return K::kP == 7;
+        else return false;
+    }();
+    // the REDQ/L-H path of the hash-indexed fields stages 66 KB of lane-private
+    // tables: one wide CTA per SM
+    static constexpr bool kLanePriv = kHashable && MODE == kGfqPacked;
+    static constexpr int RR = kLanePriv ? QPK_GFE_PK_RR : QPK_GFE_RR, S = kLanePriv ? QPK_GFE_PK_S : QPK_GFE_S;
+    static constexpr int THREADS = kLanePriv ? QPK_GFE_PK_T : kThreads;
+    // compact L|H block (kernels.hpp lh_off): L as p^3 u16 (padded to whole
+    // words), then H as p^3 u32
+    static constexpr uint32_t kLWords = (kP3 + 1) / 2, kLhWords = kLWords + kP3;
+    static constexpr bool kCustomStage = kHashable;
+    GfqElemParams P;
     __host__ __device__ bool hashed() const { return kHashable && P.bin_off != 0; }
-    __host__ __device__ __forceinline__ bool packed() const { return MODE < 0 ? P.mode == 0 : MODE == 0; }
-    // dlog products on the hash-indexed fields read the interleaved copies
-    __host__ __device__ bool dlog_copies() const { return hashed() && !packed() && P.dlog_off != 0; }
-    // staged tables: lc|hc|log|alog, the hash-indexed block, or (dlog) only
-    // the interleaved log/antilog copies
+    __host__ __device__ __forceinline__ int mode() const {
+        const int m = MODE < 0 ? P.mode : MODE;
+        return (m == kGfqLinear && !kLinear) ? kGfqPacked : m;  // linear: GF(7^3) only
+    }
+    __host__ __device__ __forceinline__ bool packed() const { return mode() != kGfqDlog; }
+    __host__ __device__ bool custom_stage() const { return hashed() && mode() == kGfqPacked; }
+    // staged tables: lc|hc|log|alog, or on the hash-indexed fields the block the
+    // path reads: 32 lane-private copies of the L|H block (packed), the
+    // interleaved dlog copies, nothing (linear)
     __host__ __device__ uint32_t tables_words() const {
-        if (dlog_copies()) return P.tables_words - P.dlog_off;
-        const uint32_t end = P.dlog_off ? P.dlog_off : P.tables_words;  // the copies are dlog-only
-        return hashed() ? end - P.bin_off : P.bin_off ? P.bin_off : P.tables_words;
+        if (hashed()) {
+            if (mode() == kGfqLinear) return 0u;
+            return mode() == kGfqDlog ? P.lh_off - P.dlog_off : 32u * kLhWords;
+        }
+        return P.bin_off ? P.bin_off : P.tables_words;
     }
     __host__ __device__ const uint32_t* tables_src() const {
-        return P.lc + (dlog_copies() ? P.dlog_off : hashed() ? P.bin_off : 0u);
+        return P.lc + (hashed() ? (mode() == kGfqDlog ? P.dlog_off : P.lh_off) : 0u);
+    }
+    // lane-private copies: warp w moves block words [32c, 32c + 32) for
+    // c = w, w + 8, ... (one coalesced load, then word j goes to 32 j + lane)
+    __device__ void stage_custom(uint32_t* dst) const {
+        const uint32_t* src = P.lc + P.lh_off;
+        const uint32_t lane = threadIdx.x & 31u, nw = blockDim.x >> 5;
+        for (uint32_t c = threadIdx.x >> 5; 32 * c < kLhWords; c += nw) {
+            const uint32_t j0 = 32 * c;
+            const uint32_t mine = j0 + lane < kLhWords ? __ldg(src + j0 + lane) : 0u;
+#pragma unroll 8
+            for (uint32_t j = 0; j < 32; ++j) {
+                const uint32_t v = __shfl_sync(0xffffffffu, mine, j);
+                if (j0 + j < kLhWords) dst[32 * (j0 + j) + lane] = v;
+            }
+        }
     }
 
     // groups of 4 records = 3 packed words
@@ -414,7 +487,7 @@ struct GfqElemOp {
             }
         }
         if constexpr (K::kP == 7) {
-            if (packed()) {
+            if (mode() == kGfqLinear) {
 #pragma unroll
                 for (int g = 0; g < R / 4; ++g) {
                     uint32_t t[4];
@@ -429,28 +502,34 @@ struct GfqElemOp {
                 return;
             }
         }
-        const bool copies = dlog_copies();
-        const uint32_t zero4 = 4 * (2 * P.group - 1) * (copies ? kDlogCopies : 1u);
-        // interleaved copies: this lane's copy offset; the log block is 512 entries
-        const uint32_t lane4 = copies ? 4 * (threadIdx.x % kDlogCopies) : 0u;
-        const uint32_t logb = copies ? tab + lane4 : tab + 4096;
-        const uint32_t alogb = copies ? tab + 4 * 512 * kDlogCopies + lane4 : tab + 6144;
-        const uint32_t stride = copies ? kDlogCopies : 1u;
+        const bool pk = packed();
+        // packed: this lane's private copies of the L and H tables
+        const uint32_t tb = tab + 4 * (threadIdx.x & 31u), hb = tb + 128 * kLWords;
+        // dlog: lane l reads interleaved copy l mod n (entry e of copy c at
+        // word n*e + c): logR (512 entries, pre-scaled by 4n) | alogR; zero
+        // sentinel at 2g-1
+        constexpr uint32_t nc = kDlogCopies;
+        const uint32_t t0 = tab + 4 * (threadIdx.x % nc), t1 = t0 + 4 * 512 * nc;
+        const uint32_t zero4 = 4 * (2 * P.group - 1) * nc;
 #pragma unroll
         for (int g = 0; g < R / 4; ++g) {
             uint32_t res[4];
 #pragma unroll
             for (int r = 0; r < 4; ++r) {
                 const uint32_t ya = record24(aw + 3 * g, r), yb = record24(bw + 3 * g, r);
-                if (packed()) {
-                    res[r] = lh_product_hash(c, P.rq.inv_p, ya & 0xffffffu, yb & 0xffffffu, tab, tab + 2048);
+                if (pk) {
+                    res[r] = lh_product_lane<K>(P.rq.inv_p, ya & 0xffffffu, yb & 0xffffffu, tb, hb);
                 } else {
-                    res[r] = dlog_product_hash(ya, yb, logb, alogb, zero4, stride);
+                    res[r] = dlog_product_hash(ya, yb, t0, t1, zero4, nc);
                 }
             }
             ow[3 * g] = res[0] | (res[1] << 24);
             ow[3 * g + 1] = (res[1] >> 8) | (res[2] << 16);
             ow[3 * g + 2] = (res[2] >> 16) | (res[3] << 8);
+            if (pk) {  // L + H lanes, four records at a time
+#pragma unroll
+                for (int i = 0; i < 3; ++i) ow[3 * g + i] = bytes_below_2p_mod(ow[3 * g + i], K::kP);
+            }
         }
     }
 
@@ -536,12 +615,17 @@ struct GfqElemOp {
 // (scripts/stream_variants.cu): for C2, 16 KB tiles x 3 stages at 2 CTAs/SM
 // reach 98% of cudaMemcpy device-to-device bandwidth; a warp-specialised
 // variant with per-warp output stores was slower.
-constexpr int kThreads = 256;
+// threads per CTA of the TMA pipeline: Op::THREADS when the op sets it
+template <class Op, class = void>
+struct op_threads : std::integral_constant<int, kThreads> {};
+template <class Op>
+struct op_threads<Op, std::void_t<decltype(Op::THREADS)>> : std::integral_constant<int, Op::THREADS> {};
 
 template <class Op>
 struct Geometry {
     static constexpr int R = Op::R, RR = Op::RR, S = Op::S;
-    static constexpr int TILE = kThreads * R * RR;  // records per tile
+    static constexpr int THREADS = op_threads<Op>::value;
+    static constexpr int TILE = THREADS * R * RR;  // records per tile
     static constexpr uint32_t B0 = Op::IN0 * TILE, B1 = Op::IN1 * TILE, BO = Op::OUT * TILE;
     static constexpr int W0 = R * Op::IN0 / 4, W1 = R * Op::IN1 / 4, WO = R * Op::OUT / 4;
     static_assert((R * Op::IN0) % 4 == 0 && (R * Op::IN1) % 4 == 0 && (R * Op::OUT) % 4 == 0, "u32 runs");
@@ -596,8 +680,26 @@ __device__ __forceinline__ void stage_tables(const Op& op, uint32_t* dst) {
     if (ASYNC && WAIT) asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
+template <class Op, class = void>
+struct has_custom_stage : std::false_type {};
 template <class Op>
-__global__ void __launch_bounds__(kThreads) stream_tma_kernel(const Op op, const uint8_t* __restrict__ in0,
+struct has_custom_stage<Op, std::enable_if_t<Op::kCustomStage>> : std::true_type {};
+
+// an op's tables: its own staging (lane-private copies built from a compact
+// table) or the plain copy
+template <class Op, bool ASYNC = true, bool WAIT = true>
+__device__ __forceinline__ void stage_op_tables(const Op& op, uint32_t* dst) {
+    if constexpr (has_custom_stage<Op>::value) {
+        if (op.custom_stage()) {
+            op.stage_custom(dst);
+            return;
+        }
+    }
+    stage_tables<Op, ASYNC, WAIT>(op, dst);
+}
+
+template <class Op>
+__global__ void __launch_bounds__(op_threads<Op>::value) stream_tma_kernel(const Op op, const uint8_t* __restrict__ in0,
                                                               const uint8_t* __restrict__ in1,
                                                               uint8_t* __restrict__ out, uint64_t n_tiles,
                                                               uint32_t* status) {
@@ -634,7 +736,7 @@ __global__ void __launch_bounds__(kThreads) stream_tma_kernel(const Op op, const
     // large tables only (C3 dlog copies, 38 KB: 32.7 -> 32.0 us); C2's
     // 2.5 KB table measured 0.4% slower staged early (0.1584 vs 0.1590 ms)
     const bool early = op.tables_words() >= QPK_EARLY_STAGE_WORDS;
-    if (early) stage_tables<Op, true, false>(op, s_tab);
+    if (early) stage_op_tables<Op, true, false>(op, s_tab);
     pdl_wait();
     if (tid == 0) {
         for (int s = 0; s < S; ++s) {
@@ -642,7 +744,7 @@ __global__ void __launch_bounds__(kThreads) stream_tma_kernel(const Op op, const
             if (t < n_tiles) issue(s, t);
         }
     }
-    if (!early) stage_tables<Op, true, false>(op, s_tab);
+    if (!early) stage_op_tables<Op, true, false>(op, s_tab);
     asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
 
@@ -659,7 +761,7 @@ __global__ void __launch_bounds__(kThreads) stream_tma_kernel(const Op op, const
         uint32_t* obuf = reinterpret_cast<uint32_t*>(s_out + size_t(os) * G::BO);
 #pragma unroll
         for (int rr = 0; rr < G::RR; ++rr) {
-            const int run = rr * kThreads + tid;  // R consecutive records
+            const int run = rr * G::THREADS + tid;  // R consecutive records
             uint32_t a[G::W0 > 0 ? G::W0 : 1], b[G::W1 > 0 ? G::W1 : 1];
             lds_run<G::W0>(src + run * (G::R * Op::IN0), a);
             lds_run<G::W1>(src + G::B0 + run * (G::R * Op::IN1), b);
@@ -739,7 +841,7 @@ __global__ void __launch_bounds__(kThreads) stream_direct_kernel(const Op op, co
         ldg_run<G::W0>(in0 + run * (G::R * Op::IN0), a);
         ldg_run<G::W1>(in1 + run * (G::R * Op::IN1), b);
     }
-    stage_tables<Op, false>(op, s_tab);
+    stage_op_tables<Op, false>(op, s_tab);
     __syncthreads();
     const uint32_t tab = smem_addr(s_tab);
     uint32_t err = 0;
@@ -765,7 +867,7 @@ __global__ void __launch_bounds__(kThreads) stream_tail_kernel(const Op op, cons
     using G = Geometry<Op>;
     extern __shared__ __align__(128) uint8_t smem[];
     uint32_t* s_tab = reinterpret_cast<uint32_t*>(smem);
-    stage_tables<Op, false>(op, s_tab);
+    stage_op_tables<Op, false>(op, s_tab);
     pdl_wait();
     __syncthreads();
     const uint32_t tab = smem_addr(s_tab);
@@ -853,13 +955,13 @@ cudaError_t run_stream(const Op& op, const uint8_t* in0, const uint8_t* in1, uin
         static thread_local int occ_per_sm = 0;
         if (occ_smem != smem) {
             int v = 0;
-            cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, stream_tma_kernel<Op>, kThreads, smem);
+            cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, stream_tma_kernel<Op>, G::THREADS, smem);
             if (e != cudaSuccess) return e;
             occ_smem = smem;
             occ_per_sm = std::max(v, 1);
         }
         const uint64_t grid = std::min<uint64_t>(n_tiles, uint64_t(sms) * occ_per_sm);
-        const cudaError_t e = launch_pdl(stream_tma_kernel<Op>, dim3(static_cast<unsigned>(grid)), dim3(kThreads),
+        const cudaError_t e = launch_pdl(stream_tma_kernel<Op>, dim3(static_cast<unsigned>(grid)), dim3(G::THREADS),
                                          smem, s, op, in0, in1, out, n_tiles, status);
         if (e != cudaSuccess) return e;
     }
@@ -926,9 +1028,12 @@ template <int K_>
 cudaError_t gfq_elem_dispatch(const GfqElemParams& P, const uint8_t* a, const uint8_t* b, uint64_t n,
                               uint8_t* out, cudaStream_t s) {
     if constexpr (K_ == 3) {
-        if (P.p == 7 && P.rq.qbits == 8 && plan_is_safe(P.rq))
-            return P.mode == 0 ? run_stream(GfqElemOp<3, CtConst<7, 8>, 0>{P}, a, b, out, n, nullptr, s)
-                               : run_stream(GfqElemOp<3, CtConst<7, 8>, 1>{P}, a, b, out, n, nullptr, s);
+        if (P.p == 7 && P.rq.qbits == 8 && plan_is_safe(P.rq)) switch (P.mode) {
+                case kGfqDlog: return run_stream(GfqElemOp<3, CtConst<7, 8>, kGfqDlog>{P}, a, b, out, n, nullptr, s);
+                case kGfqLinear:
+                    return run_stream(GfqElemOp<3, CtConst<7, 8>, kGfqLinear>{P}, a, b, out, n, nullptr, s);
+                default: return run_stream(GfqElemOp<3, CtConst<7, 8>, kGfqPacked>{P}, a, b, out, n, nullptr, s);
+            }
     }
     return P.rq.qbits ? run_stream(GfqElemOp<K_, RtConst<true>>{P}, a, b, out, n, nullptr, s)
                       : run_stream(GfqElemOp<K_, RtConst<false>>{P}, a, b, out, n, nullptr, s);
