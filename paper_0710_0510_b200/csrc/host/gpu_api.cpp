@@ -189,22 +189,22 @@ DeviceFieldCache& device_field(const GfqField& f) {
     u64 nlh = 1;
     for (u32 i = 0; i < k; ++i) nlh *= lh;
     const u64 order = f.order();
-    // small fields (p <= 8, k = 3) also get the L, H, log and antilog tables
-    // re-indexed by the 9-bit hash of the digit bytes (kernels.hpp kHash9)
-    const bool bin = p <= 8 && k == 3;
+    // the compile-time fast path (GF(7^3) at q = 2^8, stream_kernels.cuh
+    // GfqElemOp::fast) gets one more block, at the base-p index of three
+    // coefficients or digits: L as u16 | H | log (pre-scaled antilog byte
+    // offsets) | kDlogCopies interleaved copies of the doubled antilog table
+    const bool fast = qpk::gfq_fast_field(p, k, FieldAccess::q(f));
     const u64 base_words = 2 * nlh + 2 * order;
-    // the hash-indexed blocks start 16-byte aligned (cp.async staging)
-    const u64 bin_off = (base_words + 3) / 4 * 4;
     const u64 group = order - 1;
-    const u64 bin_words = (3 * 512 + 2 * group + 3) / 4 * 4;
     const u64 nc = qpk::kDlogCopies;
-    const u64 lh_off = bin_off + bin_words + nc * (512 + 2 * group);
     const u64 p3 = p * p * p;
-    const u64 lh_words = (p3 + 1) / 2 + p3;
-    const u64 words = bin ? lh_off + lh_words : base_words;
-    // a launch stages the block its path reads (hash-indexed fields: the L/H
-    // or the dlog copies; else every table)
-    const u64 staged = bin ? std::max(nc * (512 + 2 * group), 32 * lh_words) : base_words;
+    const u64 fast_off = (base_words + 3) / 4 * 4;  // 16-byte aligned
+    const u64 alog_off = ((p3 + 1) / 2 + 2 * p3 + 3) / 4 * 4;  // 16-byte aligned (vector staging)
+    const u64 fast_words = alog_off + 2 * group * nc;
+    const u64 words = fast ? fast_off + fast_words : base_words;
+    // a launch stages the tables its path reads (the fast path: 32
+    // lane-private copies of L|H, or of log plus the antilog copies)
+    const u64 staged = fast ? 32 * ((p3 + 1) / 2 + p3) : base_words;
     if (staged * 4 > 96 * 1024)
         throw std::invalid_argument("qpack-b200 GF(p^k): field tables exceed the shared-memory budget");
     // coefficient-form tables: rep -> packed coefficient bytes
@@ -223,46 +223,29 @@ DeviceFieldCache& device_field(const GfqField& f) {
         host[2 * nlh + i] = FieldAccess::log(f)[i];
         host[2 * nlh + order + i] = bytes_of(static_cast<u32>(i));
     }
-    if (bin) {
-        uint32_t* hl = host.data() + bin_off;
-        uint32_t* hh = hl + 512;
-        uint32_t* hg = hl + 1024;
-        uint32_t* al2 = hl + 1536;
-        std::vector<uint8_t> seen(512, 0);
-        for (u64 d2 = 0; d2 < 8; ++d2)
-            for (u64 d1 = 0; d1 < 8; ++d1)
-                for (u64 d0 = 0; d0 < 8; ++d0) {
-                    const uint32_t h = qpk::hash9_host(static_cast<uint32_t>(d0 | (d1 << 8) | (d2 << 16)));
-                    if (seen[h]++) throw std::logic_error("qpack-b200: kHash9 is not injective");
-                    if (d0 >= p || d1 >= p || d2 >= p) continue;
-                    const u64 lh_idx = d0 + lh * (d1 + lh * d2);
-                    hl[h] = host[lh_idx];
-                    hh[h] = host[nlh + lh_idx];
-                    const u64 lg = FieldAccess::log(f)[d0 + p * (d1 + p * d2)];
-                    hg[h] = static_cast<uint32_t>(4 * (lg == group ? 2 * group - 1 : lg));
-                }
-        for (u64 i = 0; i + 1 < 2 * group; ++i) al2[i] = bytes_of(static_cast<u32>(i % group));
-        al2[2 * group - 1] = 0;
-        uint32_t* lgR = hl + bin_words;
-        uint32_t* alR = lgR + nc * 512;
-        for (u64 c = 0; c < nc; ++c) {
-            for (u64 h = 0; h < 512; ++h) lgR[h * nc + c] = static_cast<uint32_t>(nc * hg[h]);
-            for (u64 i = 0; i < 2 * group; ++i) alR[i * nc + c] = al2[i];
-        }
-        // compact L|H block at the base-p index of three digits: L (degree < 2:
-        // coefficient bytes 0, 1) as u16, then H as u32 coefficient bytes (the
-        // kernel makes 32 lane-private copies)
-        auto* l16 = reinterpret_cast<uint16_t*>(host.data() + lh_off);
-        uint32_t* h32 = host.data() + lh_off + (p3 + 1) / 2;
+    if (fast) {
+        auto* l16 = reinterpret_cast<uint16_t*>(host.data() + fast_off);
+        uint32_t* h32 = host.data() + fast_off + (p3 + 1) / 2;
+        uint32_t* lg32 = h32 + p3;
+        uint32_t* alR = host.data() + fast_off + alog_off;
         for (u64 d2 = 0; d2 < p; ++d2)
             for (u64 d1 = 0; d1 < p; ++d1)
                 for (u64 d0 = 0; d0 < p; ++d0) {
                     const u64 lh_idx = d0 + lh * (d1 + lh * d2);
                     const u64 e = d0 + p * (d1 + p * d2);
+                    // the low half has degree < k-1 = 2: two coefficient bytes
                     if (host[lh_idx] >> 16) throw std::logic_error("qpack-b200: low-half table entry of degree >= 2");
                     l16[e] = static_cast<uint16_t>(host[lh_idx]);
                     h32[e] = host[nlh + lh_idx];
+                    const u64 lg = FieldAccess::log(f)[e];  // zero -> the sentinel g
+                    lg32[e] = static_cast<uint32_t>(4 * nc * (lg == group ? 2 * group - 1 : lg));
                 }
+        // rep i mod g for i < 2g-1, zero at 2g-1: a sum of two logs indexes it
+        // with no reduction mod g, and any sum involving zero clamps to 2g-1
+        for (u64 i = 0; i < 2 * group; ++i) {
+            const uint32_t v = i + 1 < 2 * group ? bytes_of(static_cast<u32>(i % group)) : 0u;
+            for (u64 cp = 0; cp < nc; ++cp) alR[i * nc + cp] = v;
+        }
     }
     c->tables.ensure(words * 4);
     check(cudaMemcpy(c->tables.ptr, host.data(), words * 4, cudaMemcpyHostToDevice), "field tables upload");
@@ -287,9 +270,7 @@ DeviceFieldCache& device_field(const GfqField& f) {
     E.log = tb + 2 * nlh;
     E.alog = tb + 2 * nlh + order;
     E.tables_words = static_cast<uint32_t>(words);
-    E.bin_off = bin ? static_cast<uint32_t>(bin_off) : 0u;
-    E.dlog_off = bin ? static_cast<uint32_t>(bin_off + bin_words) : 0u;
-    E.lh_off = bin ? static_cast<uint32_t>(lh_off) : 0u;
+    E.fast_off = fast ? static_cast<uint32_t>(fast_off) : 0u;
     if (k == 3) {
         const std::vector<u64> xv = {0, 1, 0};
         const GfqElt x = f.from_coeffs(xv);

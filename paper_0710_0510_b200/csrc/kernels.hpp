@@ -47,24 +47,17 @@ struct PolymulParams {
     uint32_t k;
 };
 
-// Small fields (p <= 8, k = 3) index their tables by a 9-bit multiplicative
-// hash of the three coefficient (or digit) bytes y = c0 | c1 << 8 | c2 << 16,
-// c_j < 8: h(y) = ((y * kHash9) mod 2^24) >> 15 is injective on all 512 such
-// keys (found by search; the host re-checks it when it builds the tables).
-// Bits 24..31 of y do not enter h, so a record can be hashed straight out of a
-// packed run without masking.
-constexpr uint32_t kHash9 = 13115393u;
-constexpr uint32_t hash9_host(uint32_t y) { return ((y * kHash9) & 0xffffffu) >> 15; }
-
-// The dlog path of those fields reads its log and antilog tables from
-// kDlogCopies interleaved copies (entry e, copy c at word e*kDlogCopies + c);
+// The compile-time fast path of the GF elementwise product: GF(7^3) at
+// q = 2^8 (BASELINE config 3).  Its dlog path reads the antilog table from
+// kDlogCopies interleaved copies (entry e, copy c at word e*kDlogCopies + c;
 // lane l reads copy l mod kDlogCopies, so only the 32/kDlogCopies lanes of
-// one copy share its 32/kDlogCopies banks (random lookups: ~2 wavefronts
-// per warp-wide load instead of ~3.5 over one copy).
+// one copy share its banks).
 #ifndef QPK_DLOG_COPIES
 #define QPK_DLOG_COPIES 8
 #endif
 constexpr uint32_t kDlogCopies = QPK_DLOG_COPIES;
+constexpr bool gfq_fast_field(uint64_t p, uint32_t k, uint64_t q) { return p == 7 && k == 3 && q == 256; }
+
 // GF elementwise product paths (qpk_gfq_mul_batch `path`)
 constexpr int kGfqPacked = 0;  // DQT pack, fp64 product, REDQ, L/H tables (gfq.cpp:353-384)
 constexpr int kGfqDlog = 1;    // dlog/Zech representation (gfq.cpp:260-264)
@@ -81,15 +74,12 @@ struct GfqElemParams {
     const uint32_t* log;    // p^k: coefficient index -> rep
     const uint32_t* alog;   // p^k: rep -> coefficient bytes (sentinel -> 0)
     uint32_t tables_words;  // all tables, contiguous from lc (for smem staging)
-    uint32_t bin_off;       // word offset of the hash-indexed tables (p <= 8, k = 3), else 0:
-                            //   lcH[512] | hcH[512] | logH[512] (4*log, zero -> 4*(2g-1)) | alog2[2g]
-                            //   alog2[i] = coefficients of rep i mod g (i < 2g-1), alog2[2g-1] = 0
-    uint32_t dlog_off;      // word offset of the interleaved dlog block (hash-indexed fields), else 0:
-                            //   logR[512 * kDlogCopies] (4*kDlogCopies*log, zero -> 4*kDlogCopies*(2g-1))
-                            //   | alogR[2g * kDlogCopies] (alog2 interleaved)
-    uint32_t lh_off;        // word offset of the compact L|H block (hash-indexed fields), else 0:
-                            //   at the base-p index of three digits, L as p^3 u16 (coefficient
-                            //   bytes 0, 1; padded to whole words), then H as p^3 u32
+    uint32_t fast_off;      // word offset of the fast-path block (gfq_fast_field), else 0; at the
+                            // base-p index e of three coefficients or digits:
+                            //   L16[p^3] (low half: coefficient bytes 0, 1; padded to whole words)
+                            //   | H[p^3] (coefficient bytes) | LOG[p^3] (4*kDlogCopies*log, zero ->
+                            //   4*kDlogCopies*(2g-1)) | (16-byte aligned) ALOG[2g * kDlogCopies] (rep i mod g as
+                            //   coefficient bytes, zero at 2g-1; copies interleaved)
     uint32_t col3, col4;    // k = 3: coefficient bytes of x^3 and x^4 mod the field polynomial
     int mode;               // kGfqPacked, kGfqDlog or kGfqLinear
 };

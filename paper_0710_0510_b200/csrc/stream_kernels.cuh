@@ -242,10 +242,6 @@ __device__ __forceinline__ uint32_t add_mod_bytes(uint32_t x, uint32_t y, uint32
 
 __device__ __forceinline__ uint32_t add_mod_bytes_fast(uint32_t x, uint32_t y, uint32_t p);
 
-// 9-bit table index of three byte lanes below 8 (kernels.hpp kHash9); byte
-// lane 3 of y is ignored: (y * (kHash9 << 8)) keeps only y mod 2^24
-__device__ __forceinline__ uint32_t hash9(uint32_t y) { return (y * (kHash9 << 8)) >> 23; }
-
 // bytewise t mod p of a packed word (bytes may be any value)
 __device__ __forceinline__ uint32_t bytes_mod_p(uint32_t w, uint32_t p, uint32_t magic) {
     uint32_t r = 0;
@@ -296,15 +292,17 @@ __device__ __forceinline__ uint32_t bytes_below_2p_mod(uint32_t t, uint32_t p) {
     return t - p * (((t + (128u - p) * 0x01010101u) >> 7) & 0x01010101u);
 }
 
-// dlog product on hash-indexed tables: logH holds 4*log (zero -> 4*(2g-1)),
-// so rep(a) + rep(b) indexes the doubled antilog table with no reduction
-// mod g, and any sum involving zero clamps to its zero entry (gfq.cpp:260-264)
-// (stride = kDlogCopies on the interleaved copies: logH and alog2 already
-// point at this lane's copy and the logs are pre-scaled by the stride)
-__device__ __forceinline__ uint32_t dlog_product_hash(uint32_t ya, uint32_t yb, uint32_t logH, uint32_t alog2,
-                                                      uint32_t zero4, uint32_t stride) {
-    const uint32_t s = lds_u32(logH + 4 * stride * hash9(ya)) + lds_u32(logH + 4 * stride * hash9(yb));
-    return lds_u32(alog2 + min(s, zero4));
+// dlog product on the fast-path tables (gfq.cpp:260-264): the logs of both
+// records (base-p index by one dp4a; byte lane 3 of y has weight 0) from
+// this lane's private log copy, pre-scaled to antilog byte offsets with zero
+// at 2g-1, so the sum indexes the doubled antilog table with no reduction
+// mod g and any sum involving zero clamps to its zero entry
+template <uint32_t P>
+__device__ __forceinline__ uint32_t dlog_product_lane(uint32_t ya, uint32_t yb, uint32_t lg, uint32_t al,
+                                                      uint32_t zero4) {
+    constexpr uint32_t kWeights = 1u | (P << 8) | (P * P << 16);
+    const uint32_t s = lds_u32(lg + 128u * __dp4a(ya, kWeights, 0u)) + lds_u32(lg + 128u * __dp4a(yb, kWeights, 0u));
+    return lds_u32(al + min(s, zero4));
 }
 
 // GF(7^3) product on the integer DQT word (q = 2^8).  With coefficients
@@ -340,9 +338,10 @@ __device__ __forceinline__ uint32_t record24(const uint32_t* w, int r) {
     return __funnelshift_r(w[i], w[i + 1], sh);
 }
 
+// the compile-time fast path (kernels.hpp gfq_fast_field): GF(7^3), q = 2^8
 template <class K>
-constexpr bool ct_small_p() {
-    if constexpr (K::kSafe) return K::kP < 8 && K::kQbitsCt == 8;
+constexpr bool ct_fast_field() {
+    if constexpr (K::kSafe) return K::kP == 7 && K::kQbitsCt == 8;
     else return false;
 }
 
@@ -401,8 +400,18 @@ __device__ __forceinline__ uint32_t dlog_product(const C&, uint32_t ia, uint32_t
 #endif
 // MODE: kGfqPacked / kGfqDlog / kGfqLinear as a compile-time choice (fast
 // paths), -1 = P.mode
-#ifndef QPK_GFE_PK_RR  // ... and of the hash-indexed REDQ/L-H path (lane-private tables, 66 KB:
-#define QPK_GFE_PK_RR 1   //     smaller tiles keep two CTAs per SM)
+// ... and of the fast field's REDQ/L-H (PK) and dlog (DL) paths: 66 KB of
+// lane-private tables, outputs stored straight from registers (kDirectStore),
+// 16-record runs x 2 stages keep two CTAs per SM.  Measured (C3, 2^24
+// products, scripts/c3_sweep.py): bulk-stored output tiles 34.2 / 29.4 us
+// (PK / DL, 8-record runs x 2 stages); direct stores 32.4 / 27.2 us, x 3
+// stages 32.4 / 25.1, 16-record runs x 2 stages 31.2 / 24.6 us; one CTA of
+// 512 or 1024 threads per SM and 4-record runs measured slower.
+#ifndef QPK_GFE_PK_RR
+#define QPK_GFE_PK_RR 1
+#endif
+#ifndef QPK_GFE_PK_R
+#define QPK_GFE_PK_R 16
 #endif
 #ifndef QPK_GFE_PK_S
 #define QPK_GFE_PK_S 2
@@ -410,68 +419,89 @@ __device__ __forceinline__ uint32_t dlog_product(const C&, uint32_t ia, uint32_t
 #ifndef QPK_GFE_PK_T
 #define QPK_GFE_PK_T 256
 #endif
+#ifndef QPK_GFE_DL_R
+#define QPK_GFE_DL_R 16
+#endif
+#ifndef QPK_GFE_DL_S
+#define QPK_GFE_DL_S 2
+#endif
+#ifndef QPK_GFE_DL_T
+#define QPK_GFE_DL_T 256
+#endif
 template <int K_, class K, int MODE = -1>
 struct GfqElemOp {
     static constexpr int ND = 2 * K_ - 1;
-    static constexpr int IN0 = K_, IN1 = K_, OUT = K_, R = QPK_GFE_R;
-    // hash-indexed fast path (GF(p^3), p < 8, q = 2^8) when the host built its tables
-    static constexpr bool kHashable = K_ == 3 && ct_small_p<K>() && R % 4 == 0;
-    static constexpr uint32_t kP3 = [] {
-        if constexpr (kHashable) return K::kP * K::kP * K::kP;
+    // fast path (GF(7^3), q = 2^8) when the host built its block
+    static constexpr bool kFast = K_ == 3 && ct_fast_field<K>();
+    static constexpr bool kFastDlog = kFast && MODE == kGfqDlog;
+    static constexpr int IN0 = K_, IN1 = K_, OUT = K_;
+    static constexpr int R = kFastDlog ? QPK_GFE_DL_R : (kFast && MODE == kGfqPacked) ? QPK_GFE_PK_R : QPK_GFE_R;
+    static_assert(!kFast || R % 4 == 0, "the fast path handles groups of 4 records");
+    static constexpr uint32_t kP = [] {
+        if constexpr (kFast) return K::kP;
         else return 0u;
     }();
-    static constexpr bool kLinear = [] {
-        if constexpr (kHashable) return K::kP == 7;
-        else return false;
-    }();
-    // the REDQ/L-H path of the hash-indexed fields stages 66 KB of lane-private
-    // tables: one wide CTA per SM
-    static constexpr bool kLanePriv = kHashable && MODE == kGfqPacked;
-    static constexpr int RR = kLanePriv ? QPK_GFE_PK_RR : QPK_GFE_RR, S = kLanePriv ? QPK_GFE_PK_S : QPK_GFE_S;
-    static constexpr int THREADS = kLanePriv ? QPK_GFE_PK_T : kThreads;
-    // compact L|H block (kernels.hpp lh_off): L as p^3 u16 (padded to whole
-    // words), then H as p^3 u32
-    static constexpr uint32_t kLWords = (kP3 + 1) / 2, kLhWords = kLWords + kP3;
-    static constexpr bool kCustomStage = kHashable;
+    static constexpr uint32_t kP3 = kP * kP * kP;
+    // its REDQ/L-H and dlog paths stage 66 KB of tables (32 lane-private
+    // copies, kernels.hpp fast_off): smaller tiles keep two CTAs per SM
+    static constexpr bool kLanePriv = kFast && (MODE == kGfqPacked || MODE == kGfqDlog);
+    static constexpr int RR = kLanePriv ? QPK_GFE_PK_RR : QPK_GFE_RR;
+    static constexpr int S = kFastDlog ? QPK_GFE_DL_S : kLanePriv ? QPK_GFE_PK_S : QPK_GFE_S;
+    static constexpr int THREADS = kFastDlog ? QPK_GFE_DL_T : kLanePriv ? QPK_GFE_PK_T : kThreads;
+    // block words: L16 | H | LOG | ALOG copies
+    static constexpr uint32_t kLWords = (kP3 + 1) / 2, kHOff = kLWords, kLogOff = kLWords + kP3,
+                              kAlogOff = (kLWords + 2 * kP3 + 3) / 4 * 4;  // 16-byte aligned
+    static constexpr bool kCustomStage = kFast;
+#ifndef QPK_GFE_DS
+#define QPK_GFE_DS 1
+#endif
+    static constexpr bool kDirectStore = kLanePriv && QPK_GFE_DS;
     GfqElemParams P;
-    __host__ __device__ bool hashed() const { return kHashable && P.bin_off != 0; }
+    __host__ __device__ bool fast() const { return kFast && P.fast_off != 0; }
     __host__ __device__ __forceinline__ int mode() const {
         const int m = MODE < 0 ? P.mode : MODE;
-        return (m == kGfqLinear && !kLinear) ? kGfqPacked : m;  // linear: GF(7^3) only
+        return (m == kGfqLinear && !kFast) ? kGfqPacked : m;  // linear: the fast field only
     }
     __host__ __device__ __forceinline__ bool packed() const { return mode() != kGfqDlog; }
-    __host__ __device__ bool custom_stage() const { return hashed() && mode() == kGfqPacked; }
-    // staged tables: lc|hc|log|alog, or on the hash-indexed fields the block the
-    // path reads: 32 lane-private copies of the L|H block (packed), the
-    // interleaved dlog copies, nothing (linear)
+    __host__ __device__ bool custom_stage() const { return fast() && mode() != kGfqLinear; }
+    __host__ __device__ uint32_t alog_words() const { return 2 * P.group * kDlogCopies; }
+    // staged tables: lc|hc|log|alog, or on the fast field what its path reads:
+    // lane-private L|H (packed), lane-private log + the antilog copies (dlog),
+    // nothing (linear)
     __host__ __device__ uint32_t tables_words() const {
-        if (hashed()) {
+        if (fast()) {
             if (mode() == kGfqLinear) return 0u;
-            return mode() == kGfqDlog ? P.lh_off - P.dlog_off : 32u * kLhWords;
+            return mode() == kGfqDlog ? 32u * kP3 + alog_words() : 32u * (kLWords + kP3);
         }
-        return P.bin_off ? P.bin_off : P.tables_words;
+        return P.fast_off ? P.fast_off : P.tables_words;
     }
-    __host__ __device__ const uint32_t* tables_src() const {
-        return P.lc + (hashed() ? (mode() == kGfqDlog ? P.dlog_off : P.lh_off) : 0u);
-    }
+    __host__ __device__ const uint32_t* tables_src() const { return P.lc + (fast() ? P.fast_off : 0u); }
     // lane-private copies: warp w moves block words [32c, 32c + 32) for
-    // c = w, w + 8, ... (one coalesced load, then word j goes to 32 j + lane)
+    // c = w, w + 8, ... (one coalesced load, then word j goes to 32 j + lane);
+    // the dlog path then copies the interleaved antilog block behind them
     __device__ void stage_custom(uint32_t* dst) const {
-        const uint32_t* src = P.lc + P.lh_off;
+        const bool dl = mode() == kGfqDlog;
+        const uint32_t* src = P.lc + P.fast_off + (dl ? kLogOff : 0u);
+        const uint32_t n = dl ? kP3 : kLWords + kP3;
         const uint32_t lane = threadIdx.x & 31u, nw = blockDim.x >> 5;
-        for (uint32_t c = threadIdx.x >> 5; 32 * c < kLhWords; c += nw) {
+        for (uint32_t c = threadIdx.x >> 5; 32 * c < n; c += nw) {
             const uint32_t j0 = 32 * c;
-            const uint32_t mine = j0 + lane < kLhWords ? __ldg(src + j0 + lane) : 0u;
+            const uint32_t mine = j0 + lane < n ? __ldg(src + j0 + lane) : 0u;
 #pragma unroll 8
             for (uint32_t j = 0; j < 32; ++j) {
                 const uint32_t v = __shfl_sync(0xffffffffu, mine, j);
-                if (j0 + j < kLhWords) dst[32 * (j0 + j) + lane] = v;
+                if (j0 + j < n) dst[32 * (j0 + j) + lane] = v;
             }
+        }
+        if (dl) {
+            const uint4* a = reinterpret_cast<const uint4*>(P.lc + P.fast_off + kAlogOff);  // 16-byte aligned
+            uint4* d = reinterpret_cast<uint4*>(dst + 32 * kP3);
+            for (uint32_t i = threadIdx.x; i < alog_words() / 4; i += blockDim.x) d[i] = __ldg(a + i);
         }
     }
 
     // groups of 4 records = 3 packed words
-    __device__ __forceinline__ void apply_hashed(const uint32_t* a, const uint32_t* b, uint32_t (&ow)[R * OUT / 4],
+    __device__ __forceinline__ void apply_fast(const uint32_t* a, const uint32_t* b, uint32_t (&ow)[R * OUT / 4],
                                                  uint32_t tab) const {
         const K c{P.rq};
         constexpr int NW = R * 3 / 4;
@@ -486,7 +516,7 @@ struct GfqElemOp {
                 bw[i] = bytes_mod_p(bw[i], c.p(), P.rq.mod_magic);
             }
         }
-        if constexpr (K::kP == 7) {
+        if constexpr (kFast) {
             if (mode() == kGfqLinear) {
 #pragma unroll
                 for (int g = 0; g < R / 4; ++g) {
@@ -503,13 +533,11 @@ struct GfqElemOp {
             }
         }
         const bool pk = packed();
-        // packed: this lane's private copies of the L and H tables
-        const uint32_t tb = tab + 4 * (threadIdx.x & 31u), hb = tb + 128 * kLWords;
-        // dlog: lane l reads interleaved copy l mod n (entry e of copy c at
-        // word n*e + c): logR (512 entries, pre-scaled by 4n) | alogR; zero
-        // sentinel at 2g-1
+        // this lane's private copies: packed L16 at tb, H at hb; dlog log at tb
+        const uint32_t tb = tab + 4 * (threadIdx.x & 31u), hb = tb + 128 * kHOff;
+        // dlog: lane l reads antilog copy l mod n
         constexpr uint32_t nc = kDlogCopies;
-        const uint32_t t0 = tab + 4 * (threadIdx.x % nc), t1 = t0 + 4 * 512 * nc;
+        const uint32_t al = tab + 128 * kP3 + 4 * (threadIdx.x % nc);
         const uint32_t zero4 = 4 * (2 * P.group - 1) * nc;
 #pragma unroll
         for (int g = 0; g < R / 4; ++g) {
@@ -520,7 +548,7 @@ struct GfqElemOp {
                 if (pk) {
                     res[r] = lh_product_lane<K>(P.rq.inv_p, ya & 0xffffffu, yb & 0xffffffu, tb, hb);
                 } else {
-                    res[r] = dlog_product_hash(ya, yb, t0, t1, zero4, nc);
+                    res[r] = dlog_product_lane<kP>(ya, yb, tb, al, zero4);
                 }
             }
             ow[3 * g] = res[0] | (res[1] << 24);
@@ -535,9 +563,9 @@ struct GfqElemOp {
 
     __device__ __forceinline__ void apply(const uint32_t* a, const uint32_t* b, uint32_t (&ow)[R * OUT / 4],
                                           uint32_t tab, uint32_t&) const {
-        if constexpr (kHashable) {
-            if (P.bin_off) {
-                apply_hashed(a, b, ow, tab);
+        if constexpr (kFast) {
+            if (P.fast_off) {
+                apply_fast(a, b, ow, tab);
                 return;
             }
         }
@@ -621,17 +649,27 @@ struct op_threads : std::integral_constant<int, kThreads> {};
 template <class Op>
 struct op_threads<Op, std::void_t<decltype(Op::THREADS)>> : std::integral_constant<int, Op::THREADS> {};
 
+// ops with kDirectStore store their output runs straight from registers
+// (vector st.global, a warp's runs are contiguous) instead of staging the
+// output tile for a bulk store: no output buffers in shared memory, so an op
+// with large tables keeps one more input stage in flight
+template <class Op, class = void>
+struct op_direct_store : std::false_type {};
+template <class Op>
+struct op_direct_store<Op, std::enable_if_t<Op::kDirectStore>> : std::true_type {};
+
 template <class Op>
 struct Geometry {
     static constexpr int R = Op::R, RR = Op::RR, S = Op::S;
     static constexpr int THREADS = op_threads<Op>::value;
+    static constexpr bool DS = op_direct_store<Op>::value;
     static constexpr int TILE = THREADS * R * RR;  // records per tile
     static constexpr uint32_t B0 = Op::IN0 * TILE, B1 = Op::IN1 * TILE, BO = Op::OUT * TILE;
     static constexpr int W0 = R * Op::IN0 / 4, W1 = R * Op::IN1 / 4, WO = R * Op::OUT / 4;
     static_assert((R * Op::IN0) % 4 == 0 && (R * Op::IN1) % 4 == 0 && (R * Op::OUT) % 4 == 0, "u32 runs");
     static_assert(B0 % 16 == 0 && B1 % 16 == 0 && BO % 16 == 0, "bulk copies move multiples of 16 bytes");
     // stage buffers | output double buffer | S mbarriers | (16-aligned) tables
-    static constexpr size_t tab_off = (size_t(S) * (B0 + B1) + 2 * size_t(BO) + S * 8 + 15) / 16 * 16;
+    static constexpr size_t tab_off = (size_t(S) * (B0 + B1) + (DS ? 0 : 2 * size_t(BO)) + S * 8 + 15) / 16 * 16;
     static constexpr size_t smem_pipe = tab_off;
 };
 
@@ -680,6 +718,21 @@ __device__ __forceinline__ void stage_tables(const Op& op, uint32_t* dst) {
     if (ASYNC && WAIT) asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
+template <int N>
+__device__ __forceinline__ void stg_run(uint8_t* base, const uint32_t (&w)[N]) {
+    if constexpr (N % 4 == 0) {
+#pragma unroll
+        for (int i = 0; i < N / 4; ++i)
+            reinterpret_cast<uint4*>(base)[i] = make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
+    } else if constexpr (N % 2 == 0) {
+#pragma unroll
+        for (int i = 0; i < N / 2; ++i) reinterpret_cast<uint2*>(base)[i] = make_uint2(w[2 * i], w[2 * i + 1]);
+    } else {
+#pragma unroll
+        for (int i = 0; i < N; ++i) reinterpret_cast<uint32_t*>(base)[i] = w[i];
+    }
+}
+
 template <class Op, class = void>
 struct has_custom_stage : std::false_type {};
 template <class Op>
@@ -708,7 +761,7 @@ __global__ void __launch_bounds__(op_threads<Op>::value) stream_tma_kernel(const
     extern __shared__ __align__(128) uint8_t smem[];
     uint8_t* s_in = smem;
     uint8_t* s_out = smem + size_t(S) * (G::B0 + G::B1);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(s_out + 2 * size_t(G::BO));
+    uint64_t* bars = reinterpret_cast<uint64_t*>(s_out + (G::DS ? 0 : 2 * size_t(G::BO)));
     uint32_t* s_tab = reinterpret_cast<uint32_t*>(smem + G::tab_off);  // 16-byte aligned
     const uint32_t tab = smem_addr(s_tab);
     const int tid = threadIdx.x;
@@ -752,12 +805,33 @@ __global__ void __launch_bounds__(op_threads<Op>::value) stream_tma_kernel(const
     uint32_t it = 0;
     for (uint64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++it) {
         const int s = it % S;
+        const uint8_t* src = s_in + size_t(s) * (G::B0 + G::B1);
+        if constexpr (G::DS) {
+            // every thread waits on the stage's mbarrier (the TMA writes are
+            // visible to it); one barrier per tile frees the stage
+            mbar_wait(&bars[s], (it / S) & 1);
+#pragma unroll
+            for (int rr = 0; rr < G::RR; ++rr) {
+                const int run = rr * G::THREADS + tid;
+                uint32_t a[G::W0 > 0 ? G::W0 : 1], b[G::W1 > 0 ? G::W1 : 1];
+                lds_run<G::W0>(src + run * (G::R * Op::IN0), a);
+                lds_run<G::W1>(src + G::B0 + run * (G::R * Op::IN1), b);
+                uint32_t ow[G::WO];
+                op.apply(a, b, ow, tab, err);
+                stg_run<G::WO>(out + tile * G::BO + size_t(run) * (G::R * Op::OUT), ow);
+            }
+            __syncthreads();
+            if (tid == 0) {
+                const uint64_t next = tile + uint64_t(S) * gridDim.x;
+                if (next < n_tiles) issue(s, next);
+            }
+            continue;
+        }
         const int os = it & 1;
         if (tid == 0) bulk_wait_read<1>();  // output buffer `os` (two tiles ago) drained
         mbar_wait(&bars[s], (it / S) & 1);
         __syncthreads();
 
-        const uint8_t* src = s_in + size_t(s) * (G::B0 + G::B1);
         uint32_t* obuf = reinterpret_cast<uint32_t*>(s_out + size_t(os) * G::BO);
 #pragma unroll
         for (int rr = 0; rr < G::RR; ++rr) {
@@ -807,21 +881,6 @@ __device__ __forceinline__ void ldg_run(const uint8_t* base, uint32_t (&w)[N > 0
     } else {
 #pragma unroll
         for (int i = 0; i < N; ++i) w[i] = __ldg(reinterpret_cast<const uint32_t*>(base) + i);
-    }
-}
-
-template <int N>
-__device__ __forceinline__ void stg_run(uint8_t* base, const uint32_t (&w)[N]) {
-    if constexpr (N % 4 == 0) {
-#pragma unroll
-        for (int i = 0; i < N / 4; ++i)
-            reinterpret_cast<uint4*>(base)[i] = make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
-    } else if constexpr (N % 2 == 0) {
-#pragma unroll
-        for (int i = 0; i < N / 2; ++i) reinterpret_cast<uint2*>(base)[i] = make_uint2(w[2 * i], w[2 * i + 1]);
-    } else {
-#pragma unroll
-        for (int i = 0; i < N; ++i) reinterpret_cast<uint32_t*>(base)[i] = w[i];
     }
 }
 
