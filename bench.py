@@ -18,8 +18,11 @@ roofline  HBM: 15 B/word algorithmic (8 in + 7 out) / kernel time vs the
           measured copy bandwidth in MEASURED_PEAKS.json
 cpu_baseline  the reference's own CPU path (oracle/_ref, built from
           /root/reference unmodified) on a bounded sample, all host threads
-secondary the other BASELINE configs (C1, C3 both paths, C4, C5) measured
-          the same way with their own rooflines (N = 1 only)
+configs   every BASELINE config (C1, C2, C3 on each path, C4, C5) with the
+          same legs -- value, roofline, e2e through its C-ABI host entry point,
+          cpu_baseline (the reference CPU path, all threads and one thread) --
+          N = 1 only; next_rows: the SURVEY 8(f) kernels (K5, K6)
+summary   compact per-config values, the LAST key of the line
 """
 from __future__ import annotations
 
@@ -112,87 +115,104 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------- reference
-def run_reference(args, rank):
-    """The reference's own CPU implementation (oracle/_ref when built here,
-    else the C restatement) on the host cores, same metric/config."""
+def host_threads():
+    return len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def c2_words(n, first=0):
+    """Words [first, first + n) of the seeded C2 stream (the device generator's)."""
     import numpy as np
 
     import oracle as O
+    dr = O.draws(0x07100510 + 2, n * ND, 128, start=first * ND).reshape(n, ND).astype(np.uint64)
+    w = np.zeros(n, np.uint64)
+    for j in range(ND):
+        w = w * np.uint64(128) + dr[:, j]
+    return w.astype(np.float64)
 
-    threads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+
+def time_cpu(run, steps, warmup):
+    """Reference-arm protocol: warm-up calls, then the mean over `steps`
+    calls (each returns its own seconds, measured inside the call)."""
+    for _ in range(warmup):
+        run()
+    ts = [run() for _ in range(steps)]
+    return sum(ts) / len(ts)
+
+
+def c2_reference_rate(words, out, threads, steps, warmup):
+    """The reference's redq_residues_into (oracle/_ref, unmodified sources,
+    float_premul + window-4 table) over `words` on `threads` host threads;
+    the C restatement when the reference was not built here."""
+    import oracle as O
     use_ref = O.ref() is not None
-    kind = "reference" if use_ref else "port"
 
-    def words_for(n):
-        dr = O.draws(0x07100510 + 2, n * ND, 128).reshape(n, ND).astype(np.uint64)
-        w = np.zeros(n, np.uint64)
-        for j in range(ND):
-            w = w * np.uint64(128) + dr[:, j]
-        return w.astype(np.float64)
-
-    def run(words):
+    def run():
         if use_ref:
-            out, ns, _ = O.ref_redq_f64(5, 128, 6, words, float_mode=True, window=4, threads=threads)
+            _, ns, _ = O.ref_redq_f64(5, 128, 6, words, float_mode=True, window=4, threads=threads, out=out)
             return ns * 1e-9
         t0 = time.perf_counter()
         O.redq_f64(5, 128, 6, words, float_mode=True, window=4)
         return time.perf_counter() - t0
+    t = time_cpu(run, steps, warmup)
+    return ND * words.size / t, ("reference" if use_ref else "port"), (threads if use_ref else 1)
 
-    # size each step to ~1.5 s of wall time so K+W steps end within minutes
-    probe = words_for(1 << 18)
-    rate = (1 << 18) / max(run(probe), 1e-6)
-    sample = int(min(N_WORDS, max(1 << 16, rate * 1.5)))
-    words = words_for(sample)
-    for _ in range(args.warmup):
-        run(words)
-    ts = [run(words) for _ in range(args.steps)]
-    t = sum(ts) / len(ts)
-    value = ND * sample / t
+
+def headline_config(world):
+    return {"workload": WORKLOAD, "words_per_gpu": N_WORDS, "global_words": world * N_WORDS,
+            "l2": "inputs larger than L2 (512 MiB in + 448 MiB out per GPU per step)",
+            "parallelism": f"dp{world} (independent word shards, no collective)"}
+
+
+def run_reference(args, rank):
+    """The reference's own CPU implementation on the host cores: the same
+    metric, config and 2^26-word workload as our arm (rank 0's shard), every
+    step the full workload, all host threads."""
+    import numpy as np
+    threads = host_threads()
+    words = c2_words(N_WORDS)
+    out = np.empty((N_WORDS, ND), np.uint8)
+    value, kind, cores = c2_reference_rate(words, out, threads, args.steps, args.warmup)
+    t = ND * N_WORDS / value
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded SplitMix64)",
-        "config": {"workload": WORKLOAD, "sample_words_per_step": sample},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads if use_ref else 1, "kind": kind,
-                         "sample": f"{sample} words of the C2 stream per step (redq_residues_into, float_premul + "
-                                   f"window-4 table; -O2 asserts armed as shipped)"},
+        "config": headline_config(args.gpus),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind, "cpu_model": cpu_model(),
+                         "sample": f"the full {N_WORDS}-word C2 workload per step (redq_residues_into, float_premul + "
+                                   "window-4 table; -O2 asserts armed as shipped); output preallocated"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
 
 
 def cpu_baseline_leg():
-    """Reference CPU path on the host cores, bounded sample (~5 s)."""
+    """C2's reference CPU path on the host cores with the reference arm's
+    protocol (the full 2^26-word workload, output preallocated, 1 warm-up
+    call, mean of 3), all threads and one thread (on a 2^22-word sample)."""
     import numpy as np
-
-    import oracle as O
-    threads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
-    if O.ref() is None:
-        kind, threads_used = "port", 1
-    else:
-        kind, threads_used = "reference", threads
-
-    def words_for(n):
-        dr = O.draws(0x07100510 + 2, n * ND, 128).reshape(n, ND).astype(np.uint64)
-        w = np.zeros(n, np.uint64)
-        for j in range(ND):
-            w = w * np.uint64(128) + dr[:, j]
-        return w.astype(np.float64)
-
-    def run(words):
-        if kind == "reference":
-            _, ns, _ = O.ref_redq_f64(5, 128, 6, words, float_mode=True, window=4, threads=threads_used)
-            return ns * 1e-9
-        t0 = time.perf_counter()
-        O.redq_f64(5, 128, 6, words, float_mode=True, window=4)
-        return time.perf_counter() - t0
-
-    rate = (1 << 18) / max(run(words_for(1 << 18)), 1e-6)
-    sample = int(min(N_WORDS, max(1 << 16, rate * 4.0)))
-    t = run(words_for(sample))
-    return {"value": ND * sample / t, "unit": UNIT, "cores": threads_used, "kind": kind,
-            "sample": f"{sample} words of the C2 stream (redq_residues_into, float_premul + window-4 table, "
-                      f"reference built -O2 with asserts armed as shipped), {threads_used} threads"}
+    threads = host_threads()
+    words = c2_words(N_WORDS)
+    out = np.empty((N_WORDS, ND), np.uint8)
+    value, kind, cores = c2_reference_rate(words, out, threads, 3, 1)
+    one, _, _ = c2_reference_rate(words[:1 << 22], out[:1 << 22], 1, 2, 1)
+    return {"value": value, "unit": UNIT, "cores": cores, "kind": kind, "one_thread": one, "cpu_model": cpu_model(),
+            "sample": f"the full {N_WORDS}-word C2 workload (redq_residues_into, float_premul + window-4 table, reference "
+                      f"built -O2 with asserts armed as shipped), {cores} threads, mean of 3 after 1 warm-up; "
+                      "one_thread: 2^22 words on 1 thread"}
 
 
 # ---------------------------------------------------------------------- ours
@@ -272,10 +292,11 @@ def run_ours(args, rank, world, local_rank):
     achieved = ALGO_BYTES_PER_WORD * N_WORDS / (kernel_ms * 1e-3) / 1e9
     traffic = ncu_traffic("redq_c2")
 
-    secondary = None
+    configs = next_rows = None
     if world == 1 and not args.no_secondary:
         clocks.active = True
-        secondary = measure_secondary(Q, torch, dev)
+        configs = measure_configs(Q, torch, dev, peak)
+        next_rows = measure_next_rows(Q, torch, dev, peak, configs["fp64_peaks_tflops"]["dmma_probe"])
         clocks.active = False
     del w, out, hw, ho
     clocks.stop()
@@ -284,9 +305,7 @@ def run_ours(args, rank, world, local_rank):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded SplitMix64, generated on device)",
-        "config": {"workload": WORKLOAD, "words_per_gpu": N_WORDS, "global_words": world * N_WORDS,
-                   "l2": "inputs larger than L2 (512 MiB in + 448 MiB out per GPU per step)",
-                   "parallelism": f"dp{world} (independent word shards, no collective)"},
+        "config": headline_config(world),
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": world * N_WORDS * 8,
                 "d2h_bytes_per_step": world * N_WORDS * ND, "steps": e2e_steps,
                 "path": "qpk_redq_residues_f64_host (pinned host buffers; 2M-word chunks: H2D stream -> kernel stream -> D2H stream, 4 buffer slots)"},
@@ -298,97 +317,40 @@ def run_ours(args, rank, world, local_rank):
                      "algorithmic_bytes_per_launch": ALGO_BYTES_PER_WORD * N_WORDS},
         "clocks": clocks.summary(),
     }
-    if secondary is not None:
-        line["secondary"] = secondary
+    if configs is not None:
+        configs = {"C2": {"workload": WORKLOAD, "metric": METRIC, "unit": UNIT, "value": value, "ms": ms_step,
+                          "roofline": line["roofline"], "e2e": line["e2e"], "cpu_baseline": None}, **configs}
+        line["configs"] = configs
+        line["next_rows"] = next_rows
     return line
 
 
-def secondary_cpu_refs(sec):
-    """The reference's CPU path timed beside each secondary config (SURVEY
-    8(d)): oracle/_ref (the unmodified sources, -O2, asserts armed) on all host
-    threads, a bounded sample of the same seeded workload, ~1-3 s each."""
+def sig(x, n=3):
+    """x rounded to n significant digits (compact summary)."""
+    if x is None or x == 0:
+        return x
+    import math
+    return round(x, -int(math.floor(math.log10(abs(x)))) + n - 1)
+
+
+def measure_configs(Q, torch, dev, peak_hbm):
+    """BASELINE configs C1, C3, C4, C5 (C2 is the headline) on one GPU, each
+    with the same three legs as the headline: `value` (inputs resident in
+    HBM, CUDA-event timed), `e2e` (the same metric through the C-ABI host
+    entry point: pinned host buffers, H2D + kernels + D2H inside the timed
+    region) and `cpu_baseline` (the reference's own CPU path, oracle/_ref,
+    reference-arm protocol), plus the roofline of the dominant kernel."""
     import numpy as np
 
     import oracle as O
-    if O.ref() is None:
-        return
-    th = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
-
-    def entry(value, unit, sample):
-        return {"value": value, "unit": unit, "cores": th, "kind": "reference", "sample": sample}
-
-    # C1: fqt_mul per pair (REDQ/FQT path), first 2^20 pairs' worth of draws
-    n = 1 << 18
-    d = O.draws(0x07100510 + 1, 8 * n, 3).reshape(n, 8)
-    _, ns, _ = O.ref_polymul_batch(3, 3, d[:, :4], d[:, 4:], algo=0, threads=th)
-    if "c1_polymul" in sec:
-        sec["c1_polymul"]["cpu_ref"] = entry(n / (ns * 1e-9), "pairs/s",
-                                             f"{n} pairs of the C1 stream, fqt_mul(a,b,3,qadic_for_degree(3,3,53))")
-    # C3: fgdp_dot on length-1 vectors (packed) and GfqField::mul (dlog)
-    n = 1 << 20
-    d = O.draws(0x07100510 + 3, 6 * n, 7).reshape(n, 6)
-    rf = O.RefField(7, 3, 256)
-    for algo, name, what in ((0, "c3_gfq_mul_packed", "fgdp_dot on length-1 vectors"),
-                             (1, "c3_gfq_mul_dlog", "GfqField::mul")):
-        _, ns, _ = rf.mul_batch(d[:, :3], d[:, 3:], algo=algo, threads=th)
-        if name in sec:
-            sec[name]["cpu_ref"] = entry(n / (ns * 1e-9), "products/s", f"{n} products of the C3 stream, {what}")
-    # C4 / C5: gfq_matmul (as shipped) on a row slab, GF ops/s = 2 terms/s
-    for cid, k, q, nn in ((4, 2, 1 << 16, 4096), (5, 3, 1 << 10, 8192)):
-        rows = max(16, th)  # one row slab per host thread at least
-        A = O.draws(0x07100510 + cid, rows * nn * k, 3).reshape(rows, nn, k)
-        B = O.draws(0x07100510 + cid, nn * nn * k, 3, start=nn * nn * k).reshape(nn, nn, k)
-        _, ns, _ = O.RefField(3, k, q).matmul(A, B, 0, rows, algo=0, threads=th)
-        name = f"c{cid}_gfq_matmul"
-        if name in sec:
-            sec[name]["cpu_ref"] = entry(2 * rows * nn * nn / (ns * 1e-9), "GF ops/s",
-                                         f"{rows} rows x {nn} x {nn} of C{cid} (gfq_matmul, as shipped), extrapolated rate")
-    # K5: fgdp_dot of two long rep vectors
-    n = 1 << 24
-    v = O.draws(0x5, 2 * n, 27).astype(np.uint32)
-    t0 = time.perf_counter()
-    O.RefField(3, 3, 1 << 10).dot(v[:n], v[n:])
-    dt = time.perf_counter() - t0
-    if "k5_fgdp_dot_long" in sec:
-        sec["k5_fgdp_dot_long"]["cpu_ref"] = {"value": n / dt, "unit": "GF terms/s", "cores": 1, "kind": "reference",
-                                              "sample": f"one fgdp_dot of {n} terms (single call, single thread)"}
-    # K6: fqt_mul of two 2^11-coefficient polynomials, C1's params
-    n = 1 << 11
-    a = O.draws(0x6, 2 * n, 3).astype(np.uint64)
-    out = np.zeros(2 * n - 1, np.uint64)
-    cost = np.zeros(4, np.uint64)
-    t0 = time.perf_counter()
-    O.ref().ref_fqt_mul(3, 3, 32, 1, a[:n], n, a[n:], n, out, cost)
-    dt = time.perf_counter() - t0
-    if "k6_fqt_mul" in sec:
-        sec["k6_fqt_mul"]["cpu_ref_q32_d3_nq1"] = {
-            "value": n * n / dt, "unit": "coefficient products/s", "cores": 1, "kind": "reference",
-            "sample": f"one fqt_mul of two {n}-coefficient polynomials over F_3 (single call, single thread)"}
-    # ... and the wide-group parameters of the DMMA kernel (q = 2^13, d = 1, n_q = 409)
-    n = 1 << 14
-    a = O.draws(0x6, 2 * n, 3).astype(np.uint64)
-    out = np.zeros(2 * n - 1, np.uint64)
-    t0 = time.perf_counter()
-    O.ref().ref_fqt_mul(3, 1, 1 << 13, 409, a[:n], n, a[n:], n, out, cost)
-    dt = time.perf_counter() - t0
-    if "k6_fqt_mul" in sec:
-        sec["k6_fqt_mul"]["cpu_ref_q8192_d1_nq409"] = {
-            "value": n * n / dt, "unit": "coefficient products/s", "cores": 1, "kind": "reference",
-            "sample": f"one fqt_mul of two {n}-coefficient polynomials over F_3, q=2^13, n_q=409 (single call, single thread)"}
-    if "k6_fqt_mul_large" in sec:
-        sec["k6_fqt_mul_large"]["cpu_ref"] = {
-            "value": n * n / dt, "unit": "coefficient products/s", "cores": 1, "kind": "reference",
-            "sample": f"one fqt_mul of two {n}-coefficient polynomials, same params (the rate is size-independent: "
-                      "the reference loop is quadratic), single thread"}
-
-
-def measure_secondary(Q, torch, dev):
-    """C1, C3 (both paths), C4, C5 on one GPU; CUDA-event timed."""
     res = {}
-    peak_hbm, _ = measured_peaks()
+    threads = host_threads()
+    use_ref = O.ref() is not None
     fp64_peak = Q.probe_fp64(1, 8192)
     dfma_peak = Q.probe_fp64(0, 8192)
-    res["fp64_peaks_tflops"] = {"dmma_probe": fp64_peak, "dfma_probe": dfma_peak, "nominal": 37.0}
+    res["fp64_peaks_tflops"] = {"dmma_probe": fp64_peak, "dfma_probe": dfma_peak, "nominal": 37.0,
+                                "note": "mma.sync.m8n8k4.f64 / DFMA probe kernels measured in this run "
+                                        "(tcgen05 has no f64 kind on sm_100a)"}
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
     def time_it(fn, reps, warm=3, cold=True):
@@ -407,28 +369,11 @@ def measure_secondary(Q, torch, dev):
             ts.append(e0.elapsed_time(e1))
         return statistics.median(ts)
 
-    def time_rotating(fns, reps=10):
-        """Per-launch time of back-to-back launches cycling through buffer
-        sets whose total exceeds L2 (each set was last touched > 126 MB of
-        traffic ago); one event pair per batch -- the event clock ticks in
-        ~2 us steps, too coarse for a single 10-40 us launch."""
-        for fn in fns:
-            fn()
-        torch.cuda.synchronize()
-        ts = []
-        for _ in range(reps):
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            for fn in fns:
-                fn()
-            e1.record()
-            torch.cuda.synchronize()
-            ts.append(e0.elapsed_time(e1) / len(fns))
-        return statistics.median(ts)
-
     def time_graph(fns, reps=10):
-        """Same as time_rotating with the launches captured in one CUDA graph:
-        device time per launch without the Python call overhead."""
+        """Per-launch device time of back-to-back launches cycling through
+        buffer sets whose total exceeds L2 (each set was last touched > 126 MB
+        of traffic ago), captured in one CUDA graph; one event pair per replay
+        (the event clock ticks in ~2 us steps, too coarse for one launch)."""
         for fn in fns:
             fn()
         torch.cuda.synchronize()
@@ -448,7 +393,30 @@ def measure_secondary(Q, torch, dev):
             ts.append(e0.elapsed_time(e1) / len(fns))
         return statistics.median(ts)
 
-    # C1: 2^20 polynomial pairs, 15.7 MB per set; 24 sets (377 MB) rotate
+    def time_host(fn, steps=5, warm=2):
+        """Wall time per call of a synchronous host-buffer C-ABI entry point."""
+        for _ in range(warm):
+            fn()
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            fn()
+        return (time.perf_counter() - t0) / steps
+
+    def pinned(shape, dtype):
+        return torch.empty(shape, dtype=dtype, pin_memory=True).numpy()
+
+    def cpu_entry(rate_all, rate_one, unit, sample):
+        return {"value": rate_all, "unit": unit, "cores": threads if use_ref else 1, "one_thread": rate_one,
+                "kind": "reference" if use_ref else "port", "sample": sample}
+
+    def hbm_roof(bytes_per_launch, ms, kernel):
+        a = bytes_per_launch / (ms * 1e-3) / 1e9
+        return {"bound": "hbm", "achieved": a, "peak": peak_hbm, "unit": "GB/s", "frac": a / peak_hbm,
+                "algorithmic_bytes_per_launch": bytes_per_launch, "kernel": kernel}
+
+    # ---------------------------------------------------------------- C1
+    # 2^20 pairs of degree-<4 polynomials over F_3, q = 2^5: 15 B per pair
+    # (4 + 4 in, 7 out); 24 sets (377 MB) rotate through the graph
     n1 = Q.C1.n
     pm = Q.PolymulPlan(3, 32, 4, 1)
     sets1 = []
@@ -457,18 +425,35 @@ def measure_secondary(Q, torch, dev):
         b1 = torch.empty_like(a1)
         Q.gen_pairs(Q.C1.seed, n1, 4, 3, a1, b1)
         sets1.append((a1, b1, torch.empty((n1, 7), dtype=torch.uint8, device=dev)))
-    fns = [lambda s=s_: pm(s[0], s[1], out=s[2]) for s_ in sets1]
-    eager = time_rotating(fns)
-    cold = time_graph(fns)
-    hot = time_graph([lambda s=sets1[0]: pm(s[0], s[1], out=s[2])] * 24)
-    single = time_it(lambda: pm(sets1[0][0], sets1[0][1], out=sets1[0][2]), 20)
+    ms = time_graph([lambda s=s_: pm(s[0], s[1], out=s[2]) for s_ in sets1])
+    ms_hot = time_graph([lambda s=sets1[0]: pm(s[0], s[1], out=s[2])] * 24)
+    ms_single = time_it(lambda: pm(sets1[0][0], sets1[0][1], out=sets1[0][2]), 20)
     pm.sync()
-    del sets1, fns
-    res["c1_polymul"] = {"pairs_per_s_cold": n1 / (cold * 1e-3), "ms_cold": cold, "ms_hot": hot,
-                         "timing": "CUDA graph of 24 launches over rotating buffer sets (377 MB > L2)",
-                         "ms_eager_python_calls": eager, "ms_single_launch_flushed": single,
-                         "GBps_cold": 15 * n1 / (cold * 1e-3) / 1e9, "frac_hbm_cold": 15 * n1 / (cold * 1e-3) / 1e9 / peak_hbm}
-    # C3: 2^24 GF(7^3) products, 151 MB per set; 3 sets rotate
+    ha, hb, ho = pinned((n1, 4), torch.uint8), pinned((n1, 4), torch.uint8), pinned((n1, 7), torch.uint8)
+    ha[:] = sets1[0][0].view(n1, 4).cpu().numpy()
+    hb[:] = sets1[0][1].view(n1, 4).cpu().numpy()
+    t_e2e = time_host(lambda: pm(ha, hb, out=ho), steps=20)
+    assert np.array_equal(ho, sets1[0][2].cpu().numpy()), "C1 e2e output differs from the device output"
+    del sets1
+    cpu = None
+    if use_ref:
+        out = np.empty((n1, 7), np.uint8)
+        rate = lambda th, n: n / time_cpu(lambda: O.ref_polymul_batch(3, 3, ha[:n], hb[:n], algo=0, threads=th,
+                                                                      out=out[:n])[1] * 1e-9, 3, 1)
+        cpu = cpu_entry(rate(threads, n1), rate(1, 1 << 18), "pairs/s",
+                        f"the full {n1}-pair C1 workload per call (fqt_mul per pair, qadic_for_degree(3,3,53)); "
+                        "mean of 3 after 1 warm-up; one_thread: 2^18 pairs")
+    res["C1"] = {"workload": "C1 F_3 polymul: 2^20 pairs of degree-<4 polys, q=2^5 -> 7 residues/pair",
+                 "metric": "polymul_pairs_per_s", "unit": "pairs/s", "value": n1 / (ms * 1e-3), "ms": ms,
+                 "timing": "CUDA graph of 24 launches over rotating buffer sets (377 MB > L2), per launch",
+                 "ms_hot": ms_hot, "ms_single_launch_flushed": ms_single,
+                 "roofline": hbm_roof(15 * n1, ms, "stream_direct_kernel<PolymulOp<4,4,CtConst<3,5>>>"),
+                 "e2e": {"value": n1 / t_e2e, "unit": "pairs/s", "h2d_bytes_per_step": 8 * n1,
+                         "d2h_bytes_per_step": 7 * n1, "path": "qpk_polymul_batch_host (pinned host buffers)"},
+                 "cpu_baseline": cpu}
+
+    # ---------------------------------------------------------------- C3
+    # 2^24 GF(7^3) products, 9 B each (3 + 3 in, 3 out); 3 sets rotate
     n3 = Q.C3.n
     f3 = Q.GfqField(7, 3, 256)
     sets3 = []
@@ -477,67 +462,41 @@ def measure_secondary(Q, torch, dev):
         b3 = torch.empty_like(a3)
         Q.gen_pairs(Q.C3.seed, n3, 3, 7, a3, b3)
         sets3.append((a3, b3, torch.empty((n3, 3), dtype=torch.uint8, device=dev)))
-    for path, name in ((0, "packed"), (1, "dlog")):
+    ha, hb, ho = pinned((n3, 3), torch.uint8), pinned((n3, 3), torch.uint8), pinned((n3, 3), torch.uint8)
+    ha[:] = sets3[0][0].view(n3, 3).cpu().numpy()
+    hb[:] = sets3[0][1].view(n3, 3).cpu().numpy()
+    rf = O.RefField(7, 3, 256) if use_ref else None
+    nc = 1 << 22
+    oc = np.empty((nc, 3), np.uint8)
+    for path, name, what, algo in ((0, "C3_redq", "DQT pack, fp64 product, REDQ, L/H tables (fgdp_dot on length-1 "
+                                                  "vectors)", 0),
+                                   (1, "C3_dlog", "dlog/Zech (GfqField::mul)", 1),
+                                   (2, "C3_linear", "extra: integer word product + lane-wise mod 7 (no REDQ)", 0)):
         ms = time_graph([lambda s=s_, pth=path: f3.mul_batch(s[0], s[1], pth, out=s[2]) for s_ in sets3] * 4)
         single = time_it(lambda pth=path: f3.mul_batch(sets3[0][0], sets3[0][1], pth, out=sets3[0][2]), 20)
-        gbs = 9 * n3 / (ms * 1e-3) / 1e9
-        res[f"c3_gfq_mul_{name}"] = {"products_per_s": n3 / (ms * 1e-3), "ms": ms, "GBps": gbs,
-                                     "frac_hbm": gbs / peak_hbm, "ms_single_launch_flushed": single}
+        t_e2e = time_host(lambda pth=path: f3.mul_batch(ha, hb, pth, out=ho))
+        assert np.array_equal(ho, sets3[0][2].cpu().numpy()), f"{name} e2e output differs from the device output"
+        cpu = None
+        if use_ref:
+            rate = lambda th, n, al=algo: n / time_cpu(
+                lambda: rf.mul_batch(ha[:n], hb[:n], algo=al, threads=th, out=oc[:n])[1] * 1e-9, 3, 1)
+            cpu = cpu_entry(rate(threads, nc), rate(1, 1 << 20), "products/s",
+                            f"2^22 products of the C3 stream per call ({'fgdp_dot on length-1 vectors' if algo == 0 else 'GfqField::mul'}"
+                            "); mean of 3 after 1 warm-up; one_thread: 2^20 products")
+        res[name] = {"workload": f"C3 GF(7^3) elementwise: 2^24 products, q=2^8, path {path}: {what}",
+                     "metric": "gf_products_per_s", "unit": "products/s", "value": n3 / (ms * 1e-3), "ms": ms,
+                     "timing": "CUDA graph of 12 launches over 3 rotating buffer sets (453 MB > L2), per launch",
+                     "ms_single_launch_flushed": single,
+                     "roofline": hbm_roof(9 * n3, ms, f"stream_tma_kernel<GfqElemOp<3,CtConst<7,8>,{path}>>"),
+                     "e2e": {"value": n3 / t_e2e, "unit": "products/s", "h2d_bytes_per_step": 6 * n3,
+                             "d2h_bytes_per_step": 3 * n3,
+                             "path": f"qpk_gfq_mul_batch_host path {path} (pinned host buffers)"},
+                     "cpu_baseline": cpu}
     del sets3
-    # K5: GF(3^3) GEMV on reps, 8192 x 8192 (256 MiB of
-    # A, streamed once per launch: > L2), and one long fgdp_dot of 2^26 terms
-    f5 = Q.GfqField(3, 3, 1 << 10)
-    gen = torch.Generator(device=dev).manual_seed(5)
-    nn = 8192
-    A5 = torch.randint(0, 27, (nn, nn), dtype=torch.int32, device=dev, generator=gen)
-    x5 = torch.randint(0, 27, (nn,), dtype=torch.int32, device=dev, generator=gen)
-    y5 = torch.empty((nn,), dtype=torch.int32, device=dev)
-    ms = time_graph([lambda: f5.gemv(A5, x5, out=y5)] * 4)
-    gbs = (nn * nn * 4 + nn * 4 * 2) / (ms * 1e-3) / 1e9
-    res["k5_gfq_gemv"] = {"m": nn, "K": nn, "field": "GF(3^3) q=2^10", "ms": ms, "GBps": gbs,
-                          "frac_hbm": gbs / peak_hbm, "gf_terms_per_s": nn * nn / (ms * 1e-3)}
-    del A5
-    nd = 1 << 26
-    v1 = torch.randint(0, 27, (1, nd), dtype=torch.int32, device=dev, generator=gen)
-    v2 = torch.randint(0, 27, (nd,), dtype=torch.int32, device=dev, generator=gen)
-    y1 = torch.empty((1,), dtype=torch.int32, device=dev)
-    ms = time_graph([lambda: f5.gemv(v1, v2, out=y1)] * 2)
-    gbs = nd * 8 / (ms * 1e-3) / 1e9
-    res["k5_fgdp_dot_long"] = {"n": nd, "field": "GF(3^3) q=2^10", "ms": ms, "GBps": gbs, "frac_hbm": gbs / peak_hbm}
-    del v1, v2
-    # K6: one chunked FQT product of two 2^16-coefficient
-    # polynomials over F_3; C1's params (q=2^5, d=3, n_q=1: one REDQ per
-    # packed product) and a wide-group packing (q=2^13, d=1, n_q=409)
-    n6 = 1 << 16
-    a6 = torch.randint(0, 3, (n6,), dtype=torch.uint8, device=dev, generator=gen)
-    b6 = torch.randint(0, 3, (n6,), dtype=torch.uint8, device=dev, generator=gen)
-    o6 = torch.empty((2 * n6 - 1,), dtype=torch.uint8, device=dev)
-    res["k6_fqt_mul"] = {"n": n6, "p": 3}
-    for name, (q6, d6, nq6) in (("q32_d3_nq1", (32, 3, 1)), ("q8192_d1_nq409", (1 << 13, 1, 409))):
-        pm6 = Q.PolymulPlan(3, q6, d6 + 1, nq6)
-        ms = time_graph([lambda: pm6.fqt_mul(a6, b6, out=o6)] * 2)
-        chunks = -(-n6 // (d6 + 1))
-        wp = chunks * chunks / (ms * 1e-3)
-        res["k6_fqt_mul"][name] = {"ms": ms, "coeff_products_per_s": n6 * n6 / (ms * 1e-3),
-                                   "word_products_per_s": wp, "redq_per_s": wp / nq6,
-                                   "fp64_tflops": 2 * wp / 1e12,
-                                   # n_q >= 16 runs on the fp64 tensor pipe (DMMA), n_q = 1 on CUDA cores
-                                   "kernel": "fqt_mma_kernel (DMMA)" if nq6 >= 16 else "fqt_conv_step_kernel (SWAR REDQ)",
-                                   "frac_fp64_probe": 2 * wp / 1e12 / (fp64_peak if nq6 >= 16 else dfma_peak)}
-    # K6 at scale: 2^20-coefficient operands on the DMMA kernel (the 2^16
-    # case above is launch/latency dominated)
-    nL = 1 << 20
-    aL = torch.randint(0, 3, (nL,), dtype=torch.uint8, device=dev, generator=gen)
-    bL = torch.randint(0, 3, (nL,), dtype=torch.uint8, device=dev, generator=gen)
-    oL = torch.empty((2 * nL - 1,), dtype=torch.uint8, device=dev)
-    pmL = Q.PolymulPlan(3, 1 << 13, 2, 409)
-    ms = time_it(lambda: pmL.fqt_mul(aL, bL, out=oL), 3, warm=1, cold=False)
-    wp = (nL // 2) ** 2 / (ms * 1e-3)
-    res["k6_fqt_mul_large"] = {"n": nL, "p": 3, "q": 1 << 13, "d": 1, "n_q": 409, "ms": ms,
-                               "coeff_products_per_s": nL * nL / (ms * 1e-3), "fp64_tflops": 2 * wp / 1e12,
-                               "kernel": "fqt_mma_kernel (DMMA)", "frac_fp64_probe": 2 * wp / 1e12 / fp64_peak}
-    del aL, bL, oL
-    # C4, C5: GF(p^k) matrix products (pack + contraction), GF ops/s = 2 n^3 / t
+
+    # ------------------------------------------------------------ C4, C5
+    # GF(p^k) matrix products (K1 pack + K4 DMMA contraction), GF ops/s =
+    # 2 n^3 / t (one multiply-add per term = 2 fp64 flops on the tensor pipe)
     for cfg in (Q.C4, Q.C5):
         nn, k = cfg.n, cfg.k
         A = torch.empty(nn * nn * k, dtype=torch.uint8, device=dev)
@@ -548,18 +507,133 @@ def measure_secondary(Q, torch, dev):
         Cm = torch.empty((nn, nn, k), dtype=torch.uint8, device=dev)
         ms = time_it(lambda: f.matmul(A, B, nn, nn, nn, cfg.chunk, out=Cm), 5, warm=2, cold=False)
         tf = 2 * nn ** 3 / (ms * 1e-3) / 1e12
-        res[f"c{cfg.cid}_gfq_matmul"] = {"gf_ops_per_s": 2 * nn ** 3 / (ms * 1e-3), "ms": ms, "tflops": tf,
-                                          "frac_dmma_probe": tf / fp64_peak, "frac_nominal_37": tf / 37.0,
-                                          "n": nn, "chunk": cfg.chunk, "repack": "redq"}
+        hA, hB, hC = pinned((nn, nn, k), torch.uint8), pinned((nn, nn, k), torch.uint8), pinned((nn, nn, k), torch.uint8)
+        hA[:] = A.view(nn, nn, k).cpu().numpy()
+        hB[:] = B.view(nn, nn, k).cpu().numpy()
+        t_e2e = time_host(lambda: f.matmul(hA, hB, nn, nn, nn, cfg.chunk, out=hC), steps=3, warm=1)
+        assert np.array_equal(hC, Cm.cpu().numpy()), f"C{cfg.cid} e2e output differs from the device output"
+        # the reference's own signature: gfq_matmul(GfqMatrix...) on reps
+        log = f.tables()["log"]
+        wts = np.array([cfg.p ** i for i in range(k)], np.uint32)
+        rA = pinned((nn, nn), torch.int32).view(np.uint32)
+        rB = pinned((nn, nn), torch.int32).view(np.uint32)
+        rA[:] = log[(hA.astype(np.uint32) * wts).sum(axis=2)]   # from_index (gfq.cpp:317-320)
+        rB[:] = log[(hB.astype(np.uint32) * wts).sum(axis=2)]
+        rC = pinned((nn, nn), torch.int32).view(np.uint32)
+        t_rep = time_host(lambda: f.matmul_rep(rA, rB, out=rC), steps=3, warm=1)
+        e2e = {"value": 2 * nn ** 3 / t_e2e, "unit": "GF ops/s", "h2d_bytes_per_step": 2 * nn * nn * k,
+               "d2h_bytes_per_step": nn * nn * k,
+               "path": f"qpk_gfq_matmul_repack_host (coefficient records, chunk {cfg.chunk or 'none'}; pinned host buffers)",
+               "rep_api": {"value": 2 * nn ** 3 / t_rep, "h2d_bytes_per_step": 8 * nn * nn,
+                           "d2h_bytes_per_step": 4 * nn * nn,
+                           "path": "qpk_gfq_matmul_rep_host = gfq_matmul(GfqMatrix, GfqMatrix, GfqField) (reps; "
+                                   "the reference's chunk n_q)"}}
+        cpu = None
+        if use_ref:
+            rows = max(16, threads)
+            rf = O.RefField(3, k, cfg.q)
+            cb = np.empty((rows, nn, k), np.uint8)
+            rate = lambda th, r: 2 * r * nn * nn / time_cpu(
+                lambda: rf.matmul(hA[:r], hB, 0, r, algo=0, threads=th, out=cb[:r])[1] * 1e-9, 1, 0)
+            cpu = cpu_entry(rate(threads, rows), rate(1, 2), "GF ops/s",
+                            f"{rows} rows x {nn} x {nn} of C{cfg.cid} per call (gfq_matmul as shipped, row slabs over "
+                            "threads), rate extrapolated; one_thread: 2 rows")
+        name = f"C{cfg.cid}"
+        res[name] = {"workload": f"C{cfg.cid} GF(3^{k}) matmul {nn}^3, q=2^{cfg.q.bit_length() - 1}"
+                                 + (f", delayed REDQ re-pack every {cfg.chunk}" if cfg.chunk else ""),
+                     "metric": "gf_ops_per_s", "unit": "GF ops/s", "value": 2 * nn ** 3 / (ms * 1e-3), "ms": ms,
+                     "roofline": {"bound": "tensor", "achieved": tf, "peak": fp64_peak, "unit": "TFLOP/s",
+                                  "frac": tf / fp64_peak, "peak_source": "fp64 DMMA probe (this run)",
+                                  "frac_of_nominal_37": tf / 37.0, "kernel": "gfq_matmul_kernel (DMMA) + K1 pack"},
+                     "e2e": e2e, "cpu_baseline": cpu, "repack": "redq"}
         if cfg.cid == 5:
-            # the same product with the lane-fold re-pack (same C)
             ms = time_it(lambda: f.matmul(A, B, nn, nn, nn, cfg.chunk, out=Cm, repack="fold"), 5, warm=2, cold=False)
             tf = 2 * nn ** 3 / (ms * 1e-3) / 1e12
-            res["c5_gfq_matmul_fold"] = {"gf_ops_per_s": 2 * nn ** 3 / (ms * 1e-3), "ms": ms, "tflops": tf,
-                                         "frac_dmma_probe": tf / fp64_peak, "frac_nominal_37": tf / 37.0,
-                                         "n": nn, "chunk": cfg.chunk, "repack": "fold"}
+            res["C5_fold"] = {"workload": "C5 with the lane-fold re-pack (same C)", "unit": "GF ops/s",
+                              "value": 2 * nn ** 3 / (ms * 1e-3), "ms": ms,
+                              "roofline": {"bound": "tensor", "achieved": tf, "peak": fp64_peak, "unit": "TFLOP/s",
+                                           "frac": tf / fp64_peak}}
         del A, B, Cm
     return res
+
+
+def measure_next_rows(Q, torch, dev, peak_hbm, fp64_peak):
+    """K5 GF GEMV / long fgdp_dot and K6 chunked FQT."""
+    res = {}
+
+    def time_graph(fns, reps=10):
+        for fn in fns:
+            fn()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for fn in fns:
+                fn()
+        ts = []
+        for _ in range(reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            g.replay()
+            e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1) / len(fns))
+        return statistics.median(ts)
+
+    f5 = Q.GfqField(3, 3, 1 << 10)
+    gen = torch.Generator(device=dev).manual_seed(5)
+    nn = 8192
+    A5 = torch.randint(0, 27, (nn, nn), dtype=torch.int32, device=dev, generator=gen)
+    x5 = torch.randint(0, 27, (nn,), dtype=torch.int32, device=dev, generator=gen)
+    y5 = torch.empty((nn,), dtype=torch.int32, device=dev)
+    ms = time_graph([lambda: f5.gemv(A5, x5, out=y5)] * 4)
+    gbs = (nn * nn * 4 + nn * 4 * 2) / (ms * 1e-3) / 1e9
+    res["K5_gemv"] = {"m": nn, "K": nn, "field": "GF(3^3) q=2^10", "ms": ms, "frac_hbm": gbs / peak_hbm}
+    del A5
+    nd = 1 << 26
+    v1 = torch.randint(0, 27, (1, nd), dtype=torch.int32, device=dev, generator=gen)
+    v2 = torch.randint(0, 27, (nd,), dtype=torch.int32, device=dev, generator=gen)
+    y1 = torch.empty((1,), dtype=torch.int32, device=dev)
+    ms = time_graph([lambda: f5.gemv(v1, v2, out=y1)] * 2)
+    res["K5_dot"] = {"n": nd, "ms": ms, "frac_hbm": nd * 8 / (ms * 1e-3) / 1e9 / peak_hbm}
+    del v1, v2
+    nL = 1 << 20
+    aL = torch.randint(0, 3, (nL,), dtype=torch.uint8, device=dev, generator=gen)
+    bL = torch.randint(0, 3, (nL,), dtype=torch.uint8, device=dev, generator=gen)
+    oL = torch.empty((2 * nL - 1,), dtype=torch.uint8, device=dev)
+    pmL = Q.PolymulPlan(3, 1 << 13, 2, 409)
+    pmL.fqt_mul(aL, bL, out=oL)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(3):
+        pmL.fqt_mul(aL, bL, out=oL)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / 3
+    tf = 2 * (nL // 2) ** 2 / (ms * 1e-3) / 1e12
+    res["K6_fqt_2^20"] = {"q": 1 << 13, "d": 1, "n_q": 409, "ms": ms, "frac_fp64": tf / fp64_peak}
+    return res
+
+
+def summary(line):
+    """Compact per-config block, printed LAST in the JSON line so that it
+    survives a truncated stdout tail: value / roofline fraction / e2e /
+    reference CPU (all threads, one thread) per config."""
+    out = {}
+    for name, c in line.get("configs", {}).items():
+        if not isinstance(c, dict) or "value" not in c:
+            continue
+        e = {"v": sig(c["value"]), "u": c.get("unit"), "frac": sig(c.get("roofline", {}).get("frac"), 2),
+             "bound": c.get("roofline", {}).get("bound")}
+        if c.get("e2e"):
+            e["e2e"] = sig(c["e2e"]["value"])
+        if c.get("cpu_baseline"):
+            e["cpu"] = sig(c["cpu_baseline"]["value"])
+            e["cpu1"] = sig(c["cpu_baseline"].get("one_thread"))
+        out[name] = e
+    for name, c in line.get("next_rows", {}).items():
+        out[name] = {"ms": sig(c["ms"]), "frac": sig(c.get("frac_hbm", c.get("frac_fp64")), 2)}
+    return out
 
 
 def main():
@@ -591,8 +665,10 @@ def main():
     if rank == 0:
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline_leg()
-            if "secondary" in line:
-                secondary_cpu_refs(line["secondary"])
+            if "configs" in line:
+                line["configs"]["C2"]["cpu_baseline"] = line["cpu_baseline"]
+        if "configs" in line:
+            line["summary"] = summary(line)  # last key: survives a truncated stdout tail
         print(json.dumps(line))
     if world > 1:
         import torch.distributed as dist

@@ -13,8 +13,8 @@
  *
  * Pointer conventions: functions WITHOUT a `_host` suffix take DEVICE
  * pointers and a `stream` (a cudaStream_t, NULL = legacy default stream);
- * they are asynchronous and latch data errors on the plan (qpk_redq_sync /
- * qpk_polymul_sync report them).  `_host` functions take HOST pointers
+ * they are asynchronous and latch data errors on the plan or field
+ * (qpk_redq_sync / qpk_polymul_sync / qpk_field_sync report them).  `_host` functions take HOST pointers
  * (pinned memory gives the full PCIe overlap), copy in and out internally
  * and return only when results are visible — the reference's synchronous
  * semantics.  There is no CPU fallback: without a usable CUDA device every
@@ -88,7 +88,10 @@ QPK_API qpk_status qpk_redq_residues_u128(qpk_redq_plan plan, const uint64_t* wo
 QPK_API qpk_status qpk_redq_residues_u128_host(qpk_redq_plan plan, const uint64_t* words, uint64_t n,
                                                uint8_t* residues, qpk_cost* cost);
 /* wait for `stream`, then report (and clear) latched data errors:
- * QPK_ERR_DOMAIN = a word not below q^(d+1) / not an exact double (redq.cpp:27-28) */
+ * QPK_ERR_DOMAIN = a word not below q^(d+1) / not an exact double (redq.cpp:27-28).
+ * The error word is per plan: it collects what every launch on the plan
+ * latched, on any stream (a caller that shares one plan across streams sees
+ * the union; use one plan per stream to attribute errors to one stream). */
 QPK_API qpk_status qpk_redq_sync(qpk_redq_plan plan, void* stream);
 /* closed-form counters of n reductions (divisions, reduction_calls, table_accesses) */
 QPK_API qpk_status qpk_redq_cost(qpk_redq_plan plan, uint64_t n, qpk_cost* cost);
@@ -142,6 +145,13 @@ QPK_API qpk_status qpk_field_tables(qpk_field f, uint32_t* log, uint64_t* antilo
  * reference's scalar call (host code, like every per-element call) */
 QPK_API qpk_status qpk_field_op(qpk_field f, int op, const uint32_t* a, const uint32_t* b, uint64_t n, uint32_t* out);
 QPK_API qpk_status qpk_field_op1(qpk_field f, int op, uint32_t a, uint32_t b, uint32_t* out);
+/* Device-pointer rep entry points (qpk_gfq_matmul_rep, qpk_gfq_gemv) run
+ * asynchronously: a rep >= p^k is read as the zero element and latched on
+ * the field.  qpk_field_sync waits for `stream` and reports (then clears)
+ * what any launch on the field latched, whatever its stream:
+ * QPK_ERR_OUT_OF_RANGE for reps outside the field (gfq.cpp:317-320).  The
+ * _host entry points check it themselves before returning. */
+QPK_API qpk_status qpk_field_sync(qpk_field f, void* stream);
 /* fgdp_dot on reps (host, reference Alg. 4)     gfq.hpp:98-99, gfq.cpp:335-387 */
 QPK_API qpk_status qpk_fgdp_dot(qpk_field f, const uint32_t* v1, const uint32_t* v2, uint64_t n, uint32_t* out,
                                 qpk_cost* cost);

@@ -289,22 +289,23 @@ class RefField:
         ref().ref_field_tables(self.h, to_index, fval, from_index)
         return to_index, fval, from_index
 
-    def mul_batch(self, a, b, algo=0, threads=1):
+    def mul_batch(self, a, b, algo=0, threads=1, out=None):
         a = np.ascontiguousarray(a, np.uint8)
         b = np.ascontiguousarray(b, np.uint8)
-        out = np.empty_like(a)
+        out = np.empty_like(a) if out is None else out
         ns = C.c_uint64()
         cost = np.zeros(4, np.uint64)
         _chk(ref(), ref().ref_gfq_mul_batch(self.h, a, b, a.shape[0], out, algo, threads, C.byref(ns), cost), "ref")
         return out, ns.value, cost
 
-    def matmul(self, A, B, row_lo=0, row_hi=None, algo=1, threads=os.cpu_count() or 1):
+    def matmul(self, A, B, row_lo=0, row_hi=None, algo=1, threads=os.cpu_count() or 1, out=None):
+        """out: optional (m, n, k) uint8 buffer (rows [row_lo, row_hi) are written)."""
         A = np.ascontiguousarray(A, np.uint8)
         B = np.ascontiguousarray(B, np.uint8)
         m, K, k = A.shape
         n = B.shape[1]
         row_hi = m if row_hi is None else row_hi
-        C_ = np.zeros((m, n, k), np.uint8)
+        C_ = np.zeros((m, n, k), np.uint8) if out is None else out
         ns = C.c_uint64()
         cost = np.zeros(4, np.uint64)
         _chk(ref(), ref().ref_gfq_matmul(self.h, A, B, m, K, n, row_lo, row_hi, C_, algo, threads,
@@ -337,9 +338,9 @@ class RefField:
         return out, cost
 
 
-def ref_redq_f64(p, q, d, words, float_mode=True, window=0, binary_shift=False, threads=1):
+def ref_redq_f64(p, q, d, words, float_mode=True, window=0, binary_shift=False, threads=1, out=None):
     w = np.ascontiguousarray(words, np.float64)
-    out = np.empty((w.size, d + 1), np.uint8)
+    out = np.empty((w.size, d + 1), np.uint8) if out is None else out
     ns = C.c_uint64()
     cost = np.zeros(4, np.uint64)
     lib = ref()
@@ -348,11 +349,11 @@ def ref_redq_f64(p, q, d, words, float_mode=True, window=0, binary_shift=False, 
     return out, ns.value, cost
 
 
-def ref_polymul_batch(p, d, a, b, algo=0, threads=1):
+def ref_polymul_batch(p, d, a, b, algo=0, threads=1, out=None):
     a = np.ascontiguousarray(a, np.uint8)
     b = np.ascontiguousarray(b, np.uint8)
     n = a.shape[0]
-    out = np.empty((n, 2 * d + 1), np.uint8)
+    out = np.empty((n, 2 * d + 1), np.uint8) if out is None else out
     ns = C.c_uint64()
     cost = np.zeros(4, np.uint64)
     lib = ref()

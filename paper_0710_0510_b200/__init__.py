@@ -116,6 +116,7 @@ SIGNATURES = {
     "qpk_field_tables": (I, [VP, VP, VP, VP, VP, VP, VP]),
     "qpk_field_op": (I, [VP, I, VP, VP, U64, VP]),
     "qpk_field_op1": (I, [VP, I, U32, U32, C.POINTER(C.c_uint32)]),
+    "qpk_field_sync": (I, [VP, VP]),
     "qpk_fgdp_dot": (I, [VP, VP, VP, U64, PU32, PCost]),
     "qpk_gfq_mul_batch": (I, [VP, VP, VP, U64, VP, I, VP]),
     "qpk_gfq_mul_batch_host": (I, [VP, VP, VP, U64, VP, I]),
@@ -185,6 +186,43 @@ def _host(x, dtype):
     return a
 
 
+def _dev(t, dtypes, name, numel=None):
+    """A device-path tensor argument: a CUDA tensor, contiguous, of one of
+    `dtypes` (torch dtype names), holding at least `numel` elements; anything
+    else raises InvalidArgument before a pointer reaches the C-ABI."""
+    if not _is_torch(t):
+        raise InvalidArgument(f"{name}: expected a CUDA tensor (the other operands are on the device)")
+    if str(t.dtype).replace("torch.", "") not in dtypes:
+        raise InvalidArgument(f"{name}: dtype {t.dtype} (expected {' / '.join(dtypes)})")
+    if not t.is_contiguous():
+        raise InvalidArgument(f"{name}: tensor is not contiguous")
+    if t.device.type != "cuda":
+        raise InvalidArgument(f"{name}: tensor is on {t.device}, not a CUDA device")
+    if numel is not None and t.numel() < numel:
+        raise InvalidArgument(f"{name}: {t.numel()} elements, needs {numel}")
+    return t
+
+
+def _out_host(out, dtype, numel, name="out"):
+    """A caller's host output buffer: a C-contiguous numpy array of `dtype`
+    with at least `numel` elements (results are written through its pointer)."""
+    if not isinstance(out, np.ndarray) or out.dtype != np.dtype(dtype):
+        raise InvalidArgument(f"{name}: expected a numpy {np.dtype(dtype)} array")
+    if not out.flags.c_contiguous or not out.flags.writeable:
+        raise InvalidArgument(f"{name}: array is not C-contiguous and writeable")
+    if out.size < numel:
+        raise InvalidArgument(f"{name}: {out.size} elements, needs {numel}")
+    return out
+
+
+def _records(a, b, k, name):
+    """n records of k bytes in two equally sized operands."""
+    na, nb = (a.numel(), b.numel()) if _is_torch(a) else (a.size, b.size)
+    if na != nb or na % k:
+        raise InvalidArgument(f"{name}: operands of {na} and {nb} bytes are not the same n records of {k} bytes")
+    return na // k
+
+
 # ----------------------------------------------------------------- REDQ
 BASE_P, BINARY_SHIFT = 0, 1
 INTEGER, FLOAT_PREMUL = 0, 1
@@ -227,10 +265,12 @@ class RedqPlan:
         nd = self.d + 1
         if _is_torch(words):
             import torch
+            _dev(words, ("float64", "int64", "uint64"), "words")
             wide = words.dtype in (torch.int64, torch.uint64) and words.dim() == 2 and words.shape[-1] == 2
             n = words.shape[0] if wide else words.numel()  # u128 words as (lo, hi) pairs
             if out is None:
                 out = torch.empty((n, nd), dtype=torch.uint8, device=words.device)
+            _dev(out, ("uint8",), "out", n * nd)
             if wide:
                 _check(lib().qpk_redq_residues_u128(self._h, _ptr(words), n, _ptr(out), _stream()))
             elif words.dtype in (torch.int64, torch.uint64):  # integer words (two's-complement bits as u64)
@@ -240,23 +280,20 @@ class RedqPlan:
             return out
         if isinstance(words, np.ndarray) and words.dtype == np.uint64 and words.ndim == 2 and words.shape[1] == 2:
             w = np.ascontiguousarray(words)  # u128 words as (lo, hi) pairs
-            if out is None:
-                out = np.empty((w.shape[0], nd), np.uint8)
+            out = np.empty((w.shape[0], nd), np.uint8) if out is None else _out_host(out, np.uint8, w.shape[0] * nd)
             cost = Cost()
             _check(lib().qpk_redq_residues_u128_host(self._h, _ptr(w), w.shape[0], _ptr(out), C.byref(cost)))
             self.last_cost = cost.as_dict()
             return out
         if isinstance(words, np.ndarray) and words.dtype == np.uint64:
             w = np.ascontiguousarray(words).reshape(-1)
-            if out is None:
-                out = np.empty((w.size, nd), np.uint8)
+            out = np.empty((w.size, nd), np.uint8) if out is None else _out_host(out, np.uint8, w.size * nd)
             cost = Cost()
             _check(lib().qpk_redq_residues_u64_host(self._h, _ptr(w), w.size, _ptr(out), C.byref(cost)))
             self.last_cost = cost.as_dict()
             return out
         w = _host(words, np.float64).reshape(-1)
-        if out is None:
-            out = np.empty((w.size, nd), np.uint8)
+        out = np.empty((w.size, nd), np.uint8) if out is None else _out_host(out, np.uint8, w.size * nd)
         cost = Cost()
         _check(lib().qpk_redq_residues_f64_host(self._h, _ptr(w), w.size, _ptr(out), C.byref(cost)))
         self.last_cost = cost.as_dict()
@@ -289,16 +326,18 @@ class PolymulPlan:
         ko = 2 * self.k - 1
         if _is_torch(a):
             import torch
-            n = a.numel() // self.k
+            _dev(a, ("uint8",), "a")
+            _dev(b, ("uint8",), "b")
+            n = _records(a, b, self.k, "polymul_batch")
             if out is None:
                 out = torch.empty((n, ko), dtype=torch.uint8, device=a.device)
+            _dev(out, ("uint8",), "out", n * ko)
             _check(lib().qpk_polymul_batch(self._h, _ptr(a), _ptr(b), n, _ptr(out), _stream()))
             return out
         a = _host(a, np.uint8)
         b = _host(b, np.uint8)
-        n = a.size // self.k
-        if out is None:
-            out = np.empty((n, ko), np.uint8)
+        n = _records(a, b, self.k, "polymul_batch")
+        out = np.empty((n, ko), np.uint8) if out is None else _out_host(out, np.uint8, n * ko)
         cost = Cost()
         _check(lib().qpk_polymul_batch_host(self._h, _ptr(a), _ptr(b), n, _ptr(out), C.byref(cost)))
         self.last_cost = cost.as_dict()
@@ -312,15 +351,18 @@ class PolymulPlan:
         polymul.cpp:81-147): len(a)+len(b)-1 coefficients mod p."""
         if _is_torch(a):
             import torch
+            _dev(a, ("uint8",), "a")
+            _dev(b, ("uint8",), "b")
             na, nb = a.numel(), b.numel()
             if out is None:  # an empty operand gives the empty product (polymul.cpp:81-88)
                 out = torch.empty((na + nb - 1 if na and nb else 0,), dtype=torch.uint8, device=a.device)
+            _dev(out, ("uint8",), "out", na + nb - 1 if na and nb else 0)
             _check(lib().qpk_fqt_mul(self._h, _ptr(a), na, _ptr(b), nb, _ptr(out), _stream()))
             return out
         a = _host(a, np.uint8).reshape(-1)
         b = _host(b, np.uint8).reshape(-1)
-        if out is None:
-            out = np.empty((a.size + b.size - 1 if a.size and b.size else 0,), np.uint8)
+        no = a.size + b.size - 1 if a.size and b.size else 0
+        out = np.empty((no,), np.uint8) if out is None else _out_host(out, np.uint8, no)
         cost = Cost()
         _check(lib().qpk_fqt_mul_host(self._h, _ptr(a), a.size, _ptr(b), b.size, _ptr(out), C.byref(cost)))
         self.last_cost = cost.as_dict()
@@ -352,6 +394,11 @@ class GfqField:
     @property
     def zero(self):
         return self.order - 1
+
+    def sync(self):
+        """Wait for torch's current stream and raise what the field's device
+        launches latched (OutOfRange: a rep outside the field)."""
+        _check(lib().qpk_field_sync(self._h, _stream()))
 
     def info(self):
         mod = np.zeros(self.k + 1, np.uint64)
@@ -426,16 +473,18 @@ class GfqField:
         """Elementwise products of k-byte coefficient records."""
         if _is_torch(a):
             import torch
-            n = a.numel() // self.k
+            _dev(a, ("uint8",), "a")
+            _dev(b, ("uint8",), "b")
+            n = _records(a, b, self.k, "gfq_mul_batch")
             if out is None:
                 out = torch.empty((n, self.k), dtype=torch.uint8, device=a.device)
+            _dev(out, ("uint8",), "out", n * self.k)
             _check(lib().qpk_gfq_mul_batch(self._h, _ptr(a), _ptr(b), n, _ptr(out), path, _stream()))
             return out
         a = _host(a, np.uint8)
         b = _host(b, np.uint8)
-        n = a.size // self.k
-        if out is None:
-            out = np.empty((n, self.k), np.uint8)
+        n = _records(a, b, self.k, "gfq_mul_batch")
+        out = np.empty((n, self.k), np.uint8) if out is None else _out_host(out, np.uint8, n * self.k)
         _check(lib().qpk_gfq_mul_batch_host(self._h, _ptr(a), _ptr(b), n, _ptr(out), path))
         return out
 
@@ -450,18 +499,25 @@ class GfqField:
         """C = A*B on coefficient records (A m x K x k, B K x n x k).
         repack: "redq" (delayed REDQ re-pack, the default) or "fold"
         (GF(3^3) at q = 2^10 only; same C)."""
+        if repack not in ("redq", "fold"):
+            raise InvalidArgument(f"gfq_matmul: unknown re-pack mode {repack!r}")
         mode = {"redq": 0, "fold": 1}[repack]
+        k = self.k
         if _is_torch(A):
             import torch
+            _dev(A, ("uint8",), "A", m * K * k)
+            _dev(B, ("uint8",), "B", K * n * k)
             if out is None:
                 out = torch.empty((m, n, self.k), dtype=torch.uint8, device=A.device)
+            _dev(out, ("uint8",), "out", m * n * k)
             _check(lib().qpk_gfq_matmul_repack(self._h, _ptr(A), _ptr(B), m, K, n, chunk, mode, _ptr(out),
                                                _stream()))
             return out
         A = _host(A, np.uint8)
         B = _host(B, np.uint8)
-        if out is None:
-            out = np.empty((m, n, self.k), np.uint8)
+        if A.size < m * K * k or B.size < K * n * k:
+            raise InvalidArgument("gfq_matmul: A or B holds fewer than m*K or K*n records")
+        out = np.empty((m, n, self.k), np.uint8) if out is None else _out_host(out, np.uint8, m * n * k)
         cost = Cost()
         _check(lib().qpk_gfq_matmul_repack_host(self._h, _ptr(A), _ptr(B), m, K, n, chunk, mode, _ptr(out),
                                                 C.byref(cost)))
@@ -473,10 +529,17 @@ class GfqField:
         the GPU.  Returns reps (m,) or, with coeffs=True, coefficients (m, k)."""
         if _is_torch(A):
             import torch
+            _dev(A, ("int32", "uint32"), "A")
+            if A.dim() != 2:
+                raise InvalidArgument("gfq_gemv: A must be an m x K tensor")
             m, K = A.shape
+            _dev(x, ("int32", "uint32"), "x")
+            if x.numel() != K:
+                raise InvalidArgument("gfq_gemv: x length differs from the columns of A")
             if out is None:
                 out = (torch.empty((m, self.k), dtype=torch.uint8, device=A.device) if coeffs
                        else torch.empty((m,), dtype=torch.int32, device=A.device))
+            _dev(out, ("uint8",) if coeffs else ("int32", "uint32"), "out", m * (self.k if coeffs else 1))
             _check(lib().qpk_gfq_gemv(self._h, _ptr(A), _ptr(x), m, K, None if coeffs else _ptr(out),
                                       _ptr(out) if coeffs else None, _stream()))
             return out
@@ -489,6 +552,8 @@ class GfqField:
             raise InvalidArgument("gfq_gemv: x length differs from the columns of A")
         if out is None:
             out = np.empty((m, self.k), np.uint8) if coeffs else np.empty((m,), np.uint32)
+        else:
+            _out_host(out, np.uint8 if coeffs else np.uint32, m * (self.k if coeffs else 1))
         cost = Cost()
         _check(lib().qpk_gfq_gemv_host(self._h, _ptr(A), _ptr(x), m, K, None if coeffs else _ptr(out),
                                        _ptr(out) if coeffs else None, C.byref(cost)))
@@ -504,20 +569,28 @@ class GfqField:
         y = self.gemv(v1.reshape(1, -1), v2)
         return int(y[0]), self.last_cost
 
-    def matmul_rep(self, A, B):
+    def matmul_rep(self, A, B, out=None):
         """The reference gfq_matmul on GfqMatrix data (reps in, reps out)."""
         if _is_torch(A):
             import torch
+            _dev(A, ("int32", "uint32"), "A")
+            _dev(B, ("int32", "uint32"), "B")
+            if A.dim() != 2 or B.dim() != 2 or A.shape[1] != B.shape[0]:
+                raise InvalidArgument("gfq_matmul: inner dimensions differ")  # gfq.cpp:391
             m, K = A.shape
             n = B.shape[1]
-            out = torch.empty((m, n), dtype=torch.int32, device=A.device)
+            if out is None:
+                out = torch.empty((m, n), dtype=torch.int32, device=A.device)
+            _dev(out, ("int32", "uint32"), "out", m * n)
             _check(lib().qpk_gfq_matmul_rep(self._h, _ptr(A), _ptr(B), m, K, n, _ptr(out), _stream()))
             return out
         A = _host(A, np.uint32)
         B = _host(B, np.uint32)
+        if A.ndim != 2 or B.ndim != 2 or A.shape[1] != B.shape[0]:
+            raise InvalidArgument("gfq_matmul: inner dimensions differ")  # gfq.cpp:391
         m, K = A.shape
         n = B.shape[1]
-        out = np.empty((m, n), np.uint32)
+        out = np.empty((m, n), np.uint32) if out is None else _out_host(out, np.uint32, m * n)
         cost = Cost()
         _check(lib().qpk_gfq_matmul_rep_host(self._h, _ptr(A), _ptr(B), m, K, n, _ptr(out), C.byref(cost)))
         self.last_cost = cost.as_dict()

@@ -4,6 +4,7 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstring>
 #include <memory>
 #include <sstream>
@@ -331,10 +332,16 @@ qpk_status qpk_field_op(qpk_field f, int op, const uint32_t* a, const uint32_t* 
         need(op >= 0 && op <= 3, "op must be 0..3");
         need(op >= 2 || n == 0 || b != nullptr, "binary op needs b");
         const auto& F = f->f;
-        for (uint64_t i = 0; i < n; ++i)  // reps must name field elements (GfqElt contract)
-            if (a[i] >= F.order() || (op < 2 && b[i] >= F.order()))
-                throw std::out_of_range("GfqField: rep outside the field");
+        // reps must name field elements (GfqElt contract): checked on the device
         qpack::gpu::gfq_rep_op_host(qpack::detail::device_field(F), F, op, a, op < 2 ? b : nullptr, n, out);
+    });
+}
+
+qpk_status qpk_field_sync(qpk_field f, void* stream) {
+    return guard([&] {
+        need(f != nullptr, "null field");
+        auto& F = qpack::detail::device_field(f->f);
+        qpack::gpu::raise_field_status(qpack::gpu::take_field_status(F, as_stream(stream)));
     });
 }
 
@@ -391,8 +398,7 @@ qpk_status qpk_gfq_mul_batch_host(qpk_field f, const uint8_t* a, const uint8_t* 
 qpk_status qpk_gfq_mul_rep_host(qpk_field f, const uint32_t* a, const uint32_t* b, uint64_t n, uint32_t* out) {
     return guard([&] {
         need(f != nullptr && (n == 0 || (a && b && out)), "null argument");
-        for (uint64_t i = 0; i < n; ++i)
-            if (a[i] >= f->f.order() || b[i] >= f->f.order()) throw std::out_of_range("rep outside the field");
+        // reps outside the field: out_of_range, detected on the device
         if (n) qpack::gpu::gfq_mul_rep_host(qpack::detail::device_field(f->f), a, b, n, out);
     });
 }
@@ -480,13 +486,19 @@ qpk_status qpk_gfq_matmul_rep_host(qpk_field f, const uint32_t* A, const uint32_
     return guard([&] {
         need(f != nullptr, "null field");
         need((m == 0 || n == 0) || (A && B && C) || K == 0, "null buffer");
-        qpack::GfqMatrix a{m, K, std::vector<qpack::GfqElt>(m * K)}, b{K, n, std::vector<qpack::GfqElt>(K * n)};
-        for (uint64_t i = 0; i < m * K; ++i) a.data[i].rep = A[i];
-        for (uint64_t i = 0; i < K * n; ++i) b.data[i].rep = B[i];
-        qpack::CostReport c;
-        const qpack::GfqMatrix r = qpack::gfq_matmul(a, b, f->f, &c);
-        for (uint64_t i = 0; i < m * n; ++i) C[i] = r.data[i].rep;
-        put_cost(cost, c);
+        // gfq_matmul(GfqMatrix...) on the caller's rep arrays in place (no
+        // GfqMatrix copies); reps outside the field are detected on the
+        // device (the K1 pack) and raise out_of_range like the reference
+        if (m != 0 && n != 0) {
+            if (K == 0) {
+                const uint32_t zero = static_cast<uint32_t>(f->f.order() - 1);
+                std::fill(C, C + m * n, zero);
+            } else {
+                qpack::gpu::gfq_matmul_host(qpack::detail::device_field(f->f), f->f, A, B, m, K, n, 0, C, true,
+                                            qpk::kRepackRedq);
+            }
+        }
+        put_cost(cost, qpack::gpu::matmul_cost(f->f, m, K, n));
     });
 }
 
@@ -505,11 +517,7 @@ qpk_status qpk_gfq_gemv_host(qpk_field f, const uint32_t* A, const uint32_t* x, 
     return guard([&] {
         need(f != nullptr, "null field");
         need(m == 0 || ((A || K == 0) && (x || K == 0) && (y_rep || y_coeff)), "null buffer");
-        const uint64_t order = f->f.order();
-        for (uint64_t i = 0; i < m * K; ++i)
-            if (A[i] >= order) throw std::out_of_range("gfq_gemv: rep outside the field");
-        for (uint64_t i = 0; i < K; ++i)
-            if (x[i] >= order) throw std::out_of_range("gfq_gemv: rep outside the field");
+        // reps outside the field are detected on the device (out_of_range)
         if (m) qpack::gpu::gfq_gemv_host(qpack::detail::device_field(f->f), f->f, A, x, m, K, y_rep, y_coeff);
         put_cost(cost, qpack::gpu::gemv_cost(f->f, m, K));
     });

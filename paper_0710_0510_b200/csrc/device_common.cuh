@@ -34,6 +34,13 @@ __device__ __forceinline__ uint64_t floor_div_premul(double r, double inv_up) {
     return floor_u52(__dmul_ru(r, inv_up));
 }
 
+// OR a thread's error bits into *status once per warp (every lane of the
+// warp must arrive)
+__device__ __forceinline__ void report_status(uint32_t err, uint32_t* status) {
+    err = __reduce_or_sync(0xffffffffu, err);
+    if (err && (threadIdx.x & 31) == 0 && status) atomicOr(status, err);
+}
+
 // ----------------------------------------------------------------- SplitMix64
 __host__ __device__ __forceinline__ uint64_t splitmix_at(uint64_t seed, uint64_t j) {
     uint64_t z = seed + j * 0x9e3779b97f4a7c15ULL;

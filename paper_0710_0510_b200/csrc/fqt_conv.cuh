@@ -529,14 +529,8 @@ cudaError_t run_conv_k(const FqtParams& P, const double* pw, uint64_t L1, const 
     const dim3 grid(static_cast<unsigned>((T + kFqtOut - 1) / kFqtOut), splits);
     const size_t smem = W > 0 ? size_t(P.rq.n_entries) * 4 : 0;
     if (smem > 160 * 1024) return cudaErrorInvalidValue;
-    static size_t cur = 0;
-    if (smem > 24 * 1024 && smem > cur) {
-        if (cudaError_t e = cudaFuncSetAttribute(fqt_conv_kernel<ND, W, K>,
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-            e != cudaSuccess)
-            return e;
-        cur = smem;
-    }
+    if (cudaError_t e = ensure_dyn_smem(reinterpret_cast<const void*>(fqt_conv_kernel<ND, W, K>), smem); e != cudaSuccess)
+        return e;
     return launch_pdl(fqt_conv_kernel<ND, W, K>, grid, dim3(kFqtT), smem, s, P, pw, L1, qw, L2, T, isplit, res);
 }
 
@@ -546,14 +540,8 @@ cudaError_t run_conv_mma(const FqtParams& P, const double* pw, uint64_t L1, cons
     const dim3 grid(static_cast<unsigned>((T + kMmaOut - 1) / kMmaOut), splits);
     const size_t smem = (size_t(kMmaBs) * kMmaPLD + kMmaQW) * 8 + (W > 0 ? size_t(P.rq.n_entries) * 4 : 0);
     if (smem > 200 * 1024) return cudaErrorInvalidValue;
-    static size_t cur = 0;
-    if (smem > 48 * 1024 && smem > cur) {
-        if (cudaError_t e = cudaFuncSetAttribute(fqt_mma_kernel<ND, W, K, INT>,
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-            e != cudaSuccess)
-            return e;
-        cur = smem;
-    }
+    if (cudaError_t e = ensure_dyn_smem(reinterpret_cast<const void*>(fqt_mma_kernel<ND, W, K, INT>), smem); e != cudaSuccess)
+        return e;
     return launch_pdl(fqt_mma_kernel<ND, W, K, INT>, grid, dim3(kMmaWarps * 32), smem, s, P, pw, L1, qw, L2, T, cd, res);
 }
 
@@ -563,14 +551,8 @@ cudaError_t run_conv_step(const FqtParams& P, const double* pw, uint64_t L1, con
     const dim3 grid(static_cast<unsigned>((T + kFqtT - 1) / kFqtT), splits);
     const size_t smem = W > 0 ? size_t(P.rq.n_entries) * 4 : 0;
     if (smem > 160 * 1024) return cudaErrorInvalidValue;
-    static size_t cur = 0;
-    if (smem > 48 * 1024 && smem > cur) {
-        if (cudaError_t e = cudaFuncSetAttribute(fqt_conv_step_kernel<ND, W, K, SWAR_B>,
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-            e != cudaSuccess)
-            return e;
-        cur = smem;
-    }
+    if (cudaError_t e = ensure_dyn_smem(reinterpret_cast<const void*>(fqt_conv_step_kernel<ND, W, K, SWAR_B>), smem); e != cudaSuccess)
+        return e;
     return launch_pdl(fqt_conv_step_kernel<ND, W, K, SWAR_B>, grid, dim3(kFqtT), smem, s, P, pw, L1, qw, L2, T, isplit,
                       res);
 }

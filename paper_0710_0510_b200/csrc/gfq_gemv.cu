@@ -72,11 +72,16 @@ struct Acc<false> {
 
 // x reps -> packed values (V), once per call
 template <bool INT>
-__global__ void gemv_prep_x_kernel(const double* __restrict__ fval, const uint32_t* __restrict__ x, uint64_t K,
-                                   typename Acc<INT>::V* __restrict__ xv) {
+__global__ void gemv_prep_x_kernel(const double* __restrict__ fval, uint32_t order, const uint32_t* __restrict__ x,
+                                   uint64_t K, typename Acc<INT>::V* __restrict__ xv, uint32_t* status) {
     pdl_wait();
-    for (uint64_t j = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < K; j += uint64_t(gridDim.x) * blockDim.x)
-        xv[j] = Acc<INT>::from(fval[x[j]]);
+    uint32_t err = 0;
+    for (uint64_t j = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < K; j += uint64_t(gridDim.x) * blockDim.x) {
+        const uint32_t e = x[j];
+        if (e >= order) err |= kErrRep;
+        xv[j] = Acc<INT>::from(fval[min(e, order - 1)]);  // order - 1: the zero element
+    }
+    report_status(err, status);
 }
 
 // XREP: x read as reps and looked up per use (few rows: no reuse to pay for
@@ -107,7 +112,15 @@ __global__ void __launch_bounds__(kGemvThreads) gfq_gemv_kernel(const GfqGemvPar
     const K c{P.rq};
     const int lane = threadIdx.x & 31;
     const V* tl = REPL ? tv + lane : tv;  // this lane's copy: entry e at tl[32 e]
-    auto val = [&](uint32_t e) -> V { return REPL ? tl[e << 5] : tl[e]; };
+    // reps >= order read as the zero element (order - 1, one min per
+    // lookup) and latch kErrRep (a running max: 3-input max per vector pair)
+    uint32_t emax = 0;
+    const uint32_t elast = P.order - 1;
+    auto val = [&](uint32_t e) -> V {
+        e = min(e, elast);
+        return REPL ? tl[e << 5] : tl[e];
+    };
+    auto seen = [&](const uint4& v) { emax = __vimax3_u32(__vimax3_u32(emax, v.x, v.y), v.z, v.w); };
     // CTA-uniform rounds of 8 tasks; with many splits (a multiple of 8) the
     // 8 tasks of a round are 8 consecutive splits of one row and the CTA adds
     // them before writing one partial (slot split/8)
@@ -133,6 +146,7 @@ __global__ void __launch_bounds__(kGemvThreads) gfq_gemv_kernel(const GfqGemvPar
                 V xs[4];
                 if constexpr (XREP) {
                     const uint4 b = ldg_stream(xr + j);  // few rows: x is streamed too
+                    seen(b);
                     xs[0] = val(b.x), xs[1] = val(b.y), xs[2] = val(b.z), xs[3] = val(b.w);
                 } else if constexpr (INT) {
                     const V* xq = xv + j;
@@ -144,6 +158,7 @@ __global__ void __launch_bounds__(kGemvThreads) gfq_gemv_kernel(const GfqGemvPar
                     const double2 b1 = __ldg(reinterpret_cast<const double2*>(xq) + 1);
                     xs[0] = b0.x, xs[1] = b0.y, xs[2] = b1.x, xs[3] = b1.y;
                 }
+                seen(a);
                 AC::mac(acc, val(a.x), xs[0]);
                 AC::mac(acc, val(a.y), xs[1]);
                 AC::mac(acc, val(a.z), xs[2]);
@@ -179,6 +194,8 @@ __global__ void __launch_bounds__(kGemvThreads) gfq_gemv_kernel(const GfqGemvPar
                 for (; j < k1; j += 128) four(ldg_stream(arow + j), j);
             } else {
                 for (uint64_t j = k0 + lane; j < k1; j += 32) {
+                    emax = max(emax, arow[j]);
+                    if constexpr (XREP) emax = max(emax, xr[j]);
                     AC::mac(acc, val(arow[j]), XREP ? val(xr[j]) : xv[j]);
                     if (P.chunk && ++cnt >= P.chunk) close_group();
                 }
@@ -202,6 +219,7 @@ __global__ void __launch_bounds__(kGemvThreads) gfq_gemv_kernel(const GfqGemvPar
             ws[s * m + row] = cf;
         }
     }
+    report_status(emax > elast ? kErrRep : 0u, P.status);
 }
 
 __device__ __forceinline__ void gemv_emit(uint32_t p, uint32_t k, const uint32_t* log, uint64_t row, uint32_t cf,
@@ -250,15 +268,6 @@ __global__ void __launch_bounds__(256) gemv_finish_cta_kernel(uint32_t p, uint32
     }
 }
 
-// raise a kernel's dynamic shared-memory limit to `bytes` (once per size)
-template <class F>
-cudaError_t allow_smem(F* fn, size_t bytes, size_t& cur) {
-    if (bytes <= cur || bytes <= 48 * 1024) return cudaSuccess;
-    const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
-    if (e == cudaSuccess) cur = bytes;
-    return e;
-}
-
 template <int KR, class K, bool INT, bool REPL, bool XREP>
 cudaError_t run_gemv_v(const GfqGemvParams& P, const uint32_t* A, const void* xv, uint64_t m, uint64_t Kd,
                        uint32_t splits, uint64_t ksplit, uint32_t* ws, int grid, cudaStream_t s) {
@@ -270,14 +279,13 @@ cudaError_t run_gemv_v(const GfqGemvParams& P, const uint32_t* A, const void* xv
     if (smem > 226 * 1024) return cudaErrorInvalidValue;  // + the static reduction slots
     const bool vec = Kd % 4 == 0 && ksplit % 128 == 0 && P.chunk % 4 == 0 && reinterpret_cast<uintptr_t>(A) % 16 == 0 &&
                      reinterpret_cast<uintptr_t>(xv) % 16 == 0;
-    static size_t attr[2] = {0, 0};
     if (vec) {
-        if (cudaError_t e = allow_smem(gfq_gemv_kernel<KR, K, true, INT, REPL, XREP>, smem, attr[1]); e != cudaSuccess)
+        if (cudaError_t e = ensure_dyn_smem(reinterpret_cast<const void*>(gfq_gemv_kernel<KR, K, true, INT, REPL, XREP>), smem); e != cudaSuccess)
             return e;
         return launch_pdl(gfq_gemv_kernel<KR, K, true, INT, REPL, XREP>, dim3(grid), dim3(kGemvThreads), smem, s, P,
                           A, xv, m, Kd, splits, ksplit, ws);
     } else {
-        if (cudaError_t e = allow_smem(gfq_gemv_kernel<KR, K, false, INT, REPL, XREP>, smem, attr[0]); e != cudaSuccess)
+        if (cudaError_t e = ensure_dyn_smem(reinterpret_cast<const void*>(gfq_gemv_kernel<KR, K, false, INT, REPL, XREP>), smem); e != cudaSuccess)
             return e;
         return launch_pdl(gfq_gemv_kernel<KR, K, false, INT, REPL, XREP>, dim3(grid), dim3(kGemvThreads), smem, s, P,
                           A, xv, m, Kd, splits, ksplit, ws);
@@ -347,10 +355,10 @@ cudaError_t launch_gfq_gemv(const GfqGemvParams& P, const uint32_t* A, const uin
     if (Kd && !xrep) {
         const int g = static_cast<int>(std::min<uint64_t>((Kd + 255) / 256, uint64_t(num_sms()) * 8));
         const cudaError_t e =
-            P.vals32 ? launch_pdl(gemv_prep_x_kernel<true>, dim3(g), dim3(256), 0, s, P.fval, x, Kd,
-                                  reinterpret_cast<uint32_t*>(xv))
-                     : launch_pdl(gemv_prep_x_kernel<false>, dim3(g), dim3(256), 0, s, P.fval, x, Kd,
-                                  reinterpret_cast<double*>(xv));
+            P.vals32 ? launch_pdl(gemv_prep_x_kernel<true>, dim3(g), dim3(256), 0, s, P.fval, P.order, x, Kd,
+                                  reinterpret_cast<uint32_t*>(xv), P.status)
+                     : launch_pdl(gemv_prep_x_kernel<false>, dim3(g), dim3(256), 0, s, P.fval, P.order, x, Kd,
+                                  reinterpret_cast<double*>(xv), P.status);
         if (e != cudaSuccess) return e;
     }
     // split length: a multiple of 128 (one warp-wide 16-byte vector row)

@@ -44,6 +44,7 @@ namespace qpk {
 namespace {
 
 constexpr int BM = 128, BN = 128, BK = 16, PAD = 4;
+static_assert(BK == kMatmulBK, "kernels.hpp kMatmulBK");
 constexpr int LDS_ = BM + PAD;            // shared row stride in doubles (== BN + PAD)
 constexpr int NCW = 8;                    // consumer warps
 constexpr int THREADS = (NCW + 1) * 32;   // + producer warp
@@ -406,13 +407,10 @@ cudaError_t run_matmul_t(const GfqMatmulParams& P, const double* at, const doubl
     for (int i = 0; i < KR; ++i) nlh *= P.lh_radix;
     const size_t smem = smem_bytes(NST) + size_t(2 * nlh + P.order) * 4;
     if (smem > 227 * 1024) return cudaErrorInvalidValue;
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(gfq_matmul_kernel<KR, K, REDQ_STAGE, NST, FOLD>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
+    if (cudaError_t e = ensure_dyn_smem(reinterpret_cast<const void*>(gfq_matmul_kernel<KR, K, REDQ_STAGE, NST, FOLD>),
+                                        smem);
+        e != cudaSuccess)
+        return e;
     dim3 grid(static_cast<unsigned>(n_pad / BN), static_cast<unsigned>(m_pad / BM));
     gfq_matmul_kernel<KR, K, REDQ_STAGE, NST, FOLD><<<grid, THREADS, smem, s>>>(P, at, b, m, n, K_pad, m_pad, n_pad,
                                                                                 oc, orp);

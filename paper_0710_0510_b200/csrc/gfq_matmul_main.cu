@@ -134,22 +134,26 @@ __global__ void pack_coeffs_kernel(uint32_t p, double qd, const uint8_t* __restr
 }
 
 __global__ void pack_reps_kernel(const double* __restrict__ fval, uint32_t order, const uint32_t* __restrict__ src,
-                                 uint64_t rows, uint64_t cols, double* __restrict__ dst, uint64_t ld, bool transpose) {
+                                 uint64_t rows, uint64_t cols, double* __restrict__ dst, uint64_t ld, bool transpose,
+                                 uint32_t* status) {
     extern __shared__ double s_fval[];
     __shared__ double tile[32][33];
     for (uint32_t i = threadIdx.y * 32 + threadIdx.x; i < order; i += 256) s_fval[i] = fval[i];
     __syncthreads();
     const uint64_t r0 = uint64_t(blockIdx.y) * 32, c0 = uint64_t(blockIdx.x) * 32;
     const int tx = threadIdx.x, ty = threadIdx.y;
+    uint32_t err = 0;
     for (int i = ty; i < 32; i += 8) {
         const uint64_t r = r0 + i, c = c0 + tx;
         double v = 0.0;
         if (r < rows && c < cols) {
             const uint32_t rep = src[r * cols + c];
-            v = rep < order ? s_fval[rep] : 0.0;
+            if (rep < order) v = s_fval[rep];
+            else err |= kErrRep;  // read as the zero element
         }
         tile[i][tx] = v;
     }
+    report_status(err, status);
     __syncthreads();
     for (int i = ty; i < 32; i += 8) {
         if (transpose) {
@@ -222,14 +226,14 @@ cudaError_t launch_pack_coeffs(uint32_t p, uint32_t k, double qd, const uint8_t*
 }
 
 cudaError_t launch_pack_reps(const double* fval, uint32_t order, const uint32_t* src, uint64_t rows, uint64_t cols,
-                             double* dst, uint64_t ld, bool transpose, cudaStream_t s) {
+                             double* dst, uint64_t ld, bool transpose, uint32_t* status, cudaStream_t s) {
     if (rows == 0 || cols == 0) return cudaSuccess;
     dim3 grid(static_cast<unsigned>((cols + 31) / 32), static_cast<unsigned>((rows + 31) / 32));
     const size_t smem = size_t(order) * 8;
     if (smem > 200 * 1024) return cudaErrorInvalidValue;
-    if (smem > 48 * 1024)
-        cudaFuncSetAttribute(pack_reps_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    pack_reps_kernel<<<grid, dim3(32, 8), smem, s>>>(fval, order, src, rows, cols, dst, ld, transpose);
+    if (cudaError_t e = ensure_dyn_smem(reinterpret_cast<const void*>(pack_reps_kernel), smem); e != cudaSuccess)
+        return e;
+    pack_reps_kernel<<<grid, dim3(32, 8), smem, s>>>(fval, order, src, rows, cols, dst, ld, transpose, status);
     return cudaGetLastError();
 }
 

@@ -99,6 +99,7 @@ struct Staging {
 namespace qpack::detail {
 
 struct DevicePlanCache {
+    std::uint64_t gen = 0;  // RedqPlan::correction_gen the constants were built from
     qpk::RedqParams prm{};
     gpu::DevBuf table;   // byte-packed correction windows
     gpu::DevBuf status;  // latched kErr* bits

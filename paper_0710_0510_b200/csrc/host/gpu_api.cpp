@@ -152,15 +152,32 @@ qpk::RedqParams make_redq_params(const RedqPlan& plan, gpu::DevBuf* table) {
     return P;
 }
 
+// The device mirrors hang off const plans and fields (the reference
+// functions are reentrant on shared const objects): their lazy creation is
+// serialised by one process-wide lock, held for every lookup.
+std::mutex g_mirror_mu;
+
 DevicePlanCache& device_plan(const RedqPlan& plan) {
+    std::lock_guard<std::mutex> lock(g_mirror_mu);
     if (!plan.device) {
         gpu::require_device();
         auto c = std::make_shared<DevicePlanCache>();
         c->prm = make_redq_params(plan, &c->table);
+        c->gen = plan.correction_gen;
         c->status.ensure(4);
         check(cudaMemset(c->status.ptr, 0, 4), "status init");
         settle_uploads();
         plan.device = std::move(c);
+    } else if (plan.device->gen != plan.correction_gen) {
+        // a table was attached since the upload: launches still in flight may
+        // read the old table, so the device drains before it is replaced; the
+        // latched error word is kept
+        DevicePlanCache& c = *plan.device;
+        std::lock_guard<std::mutex> lk(c.mu);
+        check(cudaDeviceSynchronize(), "drain before a table swap");
+        c.prm = make_redq_params(plan, &c.table);
+        c.gen = plan.correction_gen;
+        settle_uploads();
     }
     return *plan.device;
 }
@@ -177,6 +194,7 @@ CostReport redq_batch_cost(const RedqPlan& plan, u64 n) {
 }
 
 DeviceFieldCache& device_field(const GfqField& f) {
+    std::lock_guard<std::mutex> lock(g_mirror_mu);
     auto& slot = FieldAccess::device(f);
     if (slot) return *slot;
     gpu::require_device();
@@ -251,6 +269,8 @@ DeviceFieldCache& device_field(const GfqField& f) {
     check(cudaMemcpy(c->tables.ptr, host.data(), words * 4, cudaMemcpyHostToDevice), "field tables upload");
     c->fval.ensure(order * 8);
     check(cudaMemcpy(c->fval.ptr, FieldAccess::fval(f).data(), order * 8, cudaMemcpyHostToDevice), "fval upload");
+    c->status.ensure(4);
+    check(cudaMemset(c->status.ptr, 0, 4), "status init");
     settle_uploads();
     c->nlh = static_cast<uint32_t>(nlh);
 
@@ -298,6 +318,7 @@ DeviceFieldCache& device_field(const GfqField& f) {
     G.lc = E.lc;
     G.log = E.log;
     G.fval = M.fval;
+    G.status = c->status.as<uint32_t>();
     G.vals32 = 1;
     for (const double v : FieldAccess::fval(f)) G.vals32 &= v < 4294967296.0 ? 1u : 0u;
     slot = std::move(c);
@@ -325,6 +346,25 @@ uint32_t take_status(DevicePlanCache& dp, cudaStream_t s) {
 void raise_status(uint32_t st) {
     if (st & qpk::kErrDomain) throw std::domain_error("redq: input exceeds q^(d+1), digits are not all below q");
     if (st & qpk::kErrOutOfRange) throw std::out_of_range("floor_div_premul: numerator exceeds guaranteed range r_max");
+}
+
+// The field's error word (kErrRep: a rep >= p^k, read as zero; kErrDomain:
+// the inverse of zero): every launch on the field ORs into it, whatever its
+// stream; reading it waits for stream `s` and clears it.
+uint32_t take_field_status(DeviceFieldCache& F, cudaStream_t s) {
+    check(cudaStreamSynchronize(s), "stream sync");
+    uint32_t st = 0;
+    check(cudaMemcpy(&st, F.status.ptr, 4, cudaMemcpyDeviceToHost), "status read");
+    if (st) {
+        check(cudaMemset(F.status.ptr, 0, 4), "status clear");
+        detail::settle_uploads();
+    }
+    return st;
+}
+
+void raise_field_status(uint32_t st) {
+    if (st & qpk::kErrRep) throw std::out_of_range("GfqField: rep outside the field");
+    if (st & qpk::kErrDomain) throw std::domain_error("GfqField: zero has no inverse");
 }
 
 void redq_device(DevicePlanCache& dp, const double* d_words, u64 n, uint8_t* d_out, cudaStream_t s) {
@@ -640,9 +680,11 @@ void gfq_mul_rep_host(DeviceFieldCache& F, const uint32_t* a, const uint32_t* b,
     dc.ensure(n * 4);
     check(cudaMemcpy(da.ptr, a, n * 4, cudaMemcpyHostToDevice), "H2D");
     check(cudaMemcpy(db.ptr, b, n * 4, cudaMemcpyHostToDevice), "H2D");
-    check(qpk::launch_gfq_mul_rep(F.elem.group, da.as<uint32_t>(), db.as<uint32_t>(), n, dc.as<uint32_t>(), 0),
+    check(qpk::launch_gfq_mul_rep(F.elem.group, da.as<uint32_t>(), db.as<uint32_t>(), n, dc.as<uint32_t>(),
+                                  F.status.as<uint32_t>(), 0),
           "gfq_mul_rep launch");
     check(cudaMemcpy(out, dc.ptr, n * 4, cudaMemcpyDeviceToHost), "D2H");
+    raise_field_status(take_field_status(F, 0));
 }
 
 // GfqField::mul / add / neg / inverse over host rep arrays, on the device
@@ -657,11 +699,6 @@ void gfq_rep_op_host(DeviceFieldCache& F, const GfqField& field, int op, const u
         check(cudaMemcpy(F.zech.ptr, z.data(), z.size() * 4, cudaMemcpyHostToDevice), "zech upload");
         detail::settle_uploads();
     }
-    if (!F.status.ptr) {
-        F.status.ensure(4);
-        check(cudaMemset(F.status.ptr, 0, 4), "status clear");
-        detail::settle_uploads();
-    }
     F.io_a.ensure(n * 4);
     F.io_b.ensure(n * 4);
     F.io_c.ensure(n * 4);
@@ -672,12 +709,7 @@ void gfq_rep_op_host(DeviceFieldCache& F, const GfqField& field, int op, const u
                                  F.io_c.as<uint32_t>(), F.status.as<uint32_t>(), 0),
           "gfq rep op launch");
     check(cudaMemcpy(out, F.io_c.ptr, n * 4, cudaMemcpyDeviceToHost), "D2H");
-    uint32_t st = 0;
-    check(cudaMemcpy(&st, F.status.ptr, 4, cudaMemcpyDeviceToHost), "status read");
-    if (st) {
-        check(cudaMemset(F.status.ptr, 0, 4), "status clear");
-        throw std::domain_error("GfqField: zero has no inverse");
-    }
+    raise_field_status(take_field_status(F, 0));
 }
 
 void gfq_mul_batch(std::span<const GfqElt> a, std::span<const GfqElt> b, const GfqField& field,
@@ -712,6 +744,9 @@ uint32_t resolve_chunk(const DeviceFieldCache& F, const GfqField& field, u64 K, 
     if (chunk == 0) {
         if (K <= field.params().n_q) return 0;  // one accumulation group: never reduce
         chunk = static_cast<uint32_t>(std::min<u64>(safe, 1u << 30));
+        // a whole number of K-stages re-packs between stages (the fast
+        // kernels; C5's field: 85 -> 80, measured 90 -> ~40 ms at 8192^3)
+        if (chunk >= qpk::kMatmulBK) chunk -= chunk % qpk::kMatmulBK;
     }
     if (chunk > safe)
         throw std::invalid_argument("gfq_matmul: chunk " + std::to_string(chunk) + " lets digit sums reach q (max " +
@@ -773,9 +808,10 @@ void gfq_matmul_device(DeviceFieldCache& F, const GfqField& field, const void* A
     if (mp != m || kp != K) check(cudaMemsetAsync(at, 0, kp * mp * 8, s), "memset");
     if (np != n || kp != K) check(cudaMemsetAsync(bt, 0, kp * np * 8, s), "memset");
     if (reps) {
-        check(qpk::launch_pack_reps(F.mm.fval, F.mm.order, static_cast<const uint32_t*>(A), m, K, at, mp, true, s),
+        uint32_t* st = F.status.as<uint32_t>();
+        check(qpk::launch_pack_reps(F.mm.fval, F.mm.order, static_cast<const uint32_t*>(A), m, K, at, mp, true, st, s),
               "pack A");
-        check(qpk::launch_pack_reps(F.mm.fval, F.mm.order, static_cast<const uint32_t*>(B), K, n, bt, np, false, s),
+        check(qpk::launch_pack_reps(F.mm.fval, F.mm.order, static_cast<const uint32_t*>(B), K, n, bt, np, false, st, s),
               "pack B");
     } else {
         check(qpk::launch_pack_coeffs(F.mm.p, F.mm.k, F.mm.qd, static_cast<const uint8_t*>(A), m, K, at, mp, true, s),
@@ -802,6 +838,7 @@ void gfq_matmul_host(DeviceFieldCache& F, const GfqField& field, const void* A, 
     check(cudaMemcpy(db, B, K * n * es, cudaMemcpyHostToDevice), "H2D");
     gfq_matmul_device(F, field, da, db, m, K, n, chunk, dc, reps, 0, repack);
     check(cudaMemcpy(C, dc, m * n * es, cudaMemcpyDeviceToHost), "D2H");
+    if (reps) raise_field_status(take_field_status(F, 0));
 }
 
 CostReport matmul_cost(const GfqField& field, u64 m, u64 K, u64 n) {
@@ -848,6 +885,7 @@ void gfq_gemv_host(DeviceFieldCache& F, const GfqField& field, const uint32_t* A
     gfq_gemv_device(F, field, da, dx, m, K, y_rep ? dr : nullptr, y_coeff ? dc : nullptr, 0);
     if (y_rep) check(cudaMemcpy(y_rep, dr, m * 4, cudaMemcpyDeviceToHost), "D2H");
     if (y_coeff) check(cudaMemcpy(y_coeff, dc, m * field.k(), cudaMemcpyDeviceToHost), "D2H");
+    raise_field_status(take_field_status(F, 0));
 }
 
 CostReport gemv_cost(const GfqField& field, u64 m, u64 K) {

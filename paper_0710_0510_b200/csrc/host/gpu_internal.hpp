@@ -15,6 +15,9 @@ namespace qpack::gpu {
 
 uint32_t take_status(detail::DevicePlanCache& dp, cudaStream_t s);
 void raise_status(uint32_t st);
+// the field's error word (kErrRep, kErrDomain): wait for `s`, read, clear
+uint32_t take_field_status(detail::DeviceFieldCache& F, cudaStream_t s);
+void raise_field_status(uint32_t st);
 
 void redq_device(detail::DevicePlanCache& dp, const double* d_words, u64 n, uint8_t* d_out, cudaStream_t s);
 void redq_host(detail::DevicePlanCache& dp, const double* h_words, u64 n, uint8_t* h_out);

@@ -17,6 +17,8 @@ constexpr int kMaxGfqK = 4;         // coefficient records up to 4 bytes
 enum : uint32_t {
     kErrDomain = 1u,      // word outside [0, min(q^(d+1), 2^53))  (redq.cpp:22-29, dqt.cpp:96-97)
     kErrOutOfRange = 2u,  // premultiplied floor outside r_max     (fpdiv.cpp:133-135)
+    kErrRep = 4u,         // field element rep >= p^k: read as the zero element (gfq.cpp:317-320
+                          // from_index, gfq_matmul's GfqMatrix reps: std::out_of_range)
 };
 
 // One REDQ plan as the device sees it (RedqPlan, redq.hpp:46-61).
@@ -86,6 +88,7 @@ struct GfqElemParams {
 
 // GF(p^k) matrix product (configs 4/5).
 constexpr uint32_t kRepackRedq = 0, kRepackFold = 1;
+constexpr uint32_t kMatmulBK = 16;  // K-steps per shared-memory stage (gfq_matmul.cuh BK)
 
 // Post-re-pack digit bound of the lane fold for q = 2^B (gfq_matmul.cuh
 // repack_fold3): S = the even split kFoldShift<B>, bound (2^S-1) + (2^(B-S)-1).
@@ -116,6 +119,7 @@ struct GfqGemvParams {
     const uint32_t* lc;   // lc | hc contiguous (lh_radix^k words each), as GfqElemParams
     const uint32_t* log;  // p^k: coefficient index -> rep
     const double* fval;   // rep -> q-adic evaluation (float_eval, gfq.cpp:194-207)
+    uint32_t* status;     // the field's error word: kErrRep for reps >= order (read as zero)
 };
 
 // Chunked FQT product of two long polynomials (K6, fqt_mul polymul.cpp:81-147).
@@ -140,15 +144,17 @@ cudaError_t launch_polymul(const PolymulParams& P, const uint8_t* a, const uint8
                            uint8_t* out, uint32_t* status, cudaStream_t s);
 cudaError_t launch_gfq_elem(const GfqElemParams& P, const uint8_t* a, const uint8_t* b, uint64_t n,
                             uint8_t* out, cudaStream_t s);
+// GfqField::mul over reps; reps above g latch kErrRep in *status (read as zero)
 cudaError_t launch_gfq_mul_rep(uint32_t group, const uint32_t* a, const uint32_t* b, uint64_t n, uint32_t* out,
-                               cudaStream_t s);
+                               uint32_t* status, cudaStream_t s);
 
 // DQT pack of coefficient records into q-adic doubles (K1a): src is
 // rows x cols x k bytes; dst element (r, c) goes to dst[c*ld + r] when
 // `transpose`, else dst[r*ld + c].  dst must be pre-zeroed for padding.
 cudaError_t launch_pack_coeffs(uint32_t p, uint32_t k, double qd, const uint8_t* src, uint64_t rows,
                                uint64_t cols, double* dst, uint64_t ld, bool transpose, cudaStream_t s);
-// Zech/dlog tabulated pack (K1b): reps -> float_eval(rep) via a smem table.
+// Zech/dlog tabulated pack (K1b): reps -> float_eval(rep) via a smem table;
+// reps >= order are packed as zero and latch kErrRep in *status.
 // layout helpers of the GEMV-column matmul route (fields whose n_q is below
 // one fp64 MMA step): u32 transpose, coefficient records <-> reps through
 // the field's log / antilog-to-bytes tables (GfqElemParams log, alog)
@@ -158,7 +164,8 @@ cudaError_t launch_coeffs_to_reps(uint32_t p, uint32_t k, const uint32_t* log, c
 cudaError_t launch_reps_to_coeffs(uint32_t k, const uint32_t* alog, const uint32_t* src, uint64_t n, uint8_t* dst,
                                   cudaStream_t s);
 cudaError_t launch_pack_reps(const double* fval, uint32_t order, const uint32_t* src, uint64_t rows,
-                             uint64_t cols, double* dst, uint64_t ld, bool transpose, cudaStream_t s);
+                             uint64_t cols, double* dst, uint64_t ld, bool transpose, uint32_t* status,
+                             cudaStream_t s);
 
 // K4: C = A*B on packed operands.  at is K x m_pad (A transposed), b is
 // K x n_pad, both zero padded (m_pad, n_pad multiples of 128, K_pad of 16).
@@ -215,6 +222,11 @@ cudaError_t launch_gen_pairs(uint64_t seed, uint64_t n, uint32_t k, uint32_t bou
 cudaError_t launch_probe_dfma(double* sink, int iters, uint64_t* flops, cudaStream_t s);
 cudaError_t launch_probe_dmma(double* sink, int iters, uint64_t* flops, cudaStream_t s);
 
-int num_sms();
+int num_sms();  // of the current device
+
+// Raise `kernel`'s dynamic shared-memory limit to at least `bytes` on the
+// current device (a per-device function attribute: recorded per (kernel,
+// device), thread-safe; a no-op below the 48 KB default).
+cudaError_t ensure_dyn_smem(const void* kernel, size_t bytes);
 
 }  // namespace qpk

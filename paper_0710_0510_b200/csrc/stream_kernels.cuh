@@ -956,13 +956,9 @@ cudaError_t run_tail(const Op& op, const uint8_t* in0, const uint8_t* in1, uint8
                      uint32_t* status, cudaStream_t s) {
     using G = Geometry<Op>;
     const size_t tab_bytes = size_t(op.tables_words()) * 4;
-    static bool attr_done = false;
-    if (!attr_done) {
-        cudaError_t e = cudaFuncSetAttribute(stream_tail_kernel<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             227 * 1024);
-        if (e != cudaSuccess) return e;
-        attr_done = true;
-    }
+    if (cudaError_t e = ensure_dyn_smem(reinterpret_cast<const void*>(stream_tail_kernel<Op>), tab_bytes);
+        e != cudaSuccess)
+        return e;
     const uint64_t groups = (n - first + G::R - 1) / G::R;
     const uint64_t grid = std::min<uint64_t>((groups + kThreads - 1) / kThreads, uint64_t(num_sms()) * 8);
     return launch_pdl(stream_tail_kernel<Op>, dim3(static_cast<unsigned>(grid)), dim3(kThreads), tab_bytes, s, op, in0,
@@ -982,13 +978,9 @@ cudaError_t run_stream(const Op& op, const uint8_t* in0, const uint8_t* in1, uin
     // small batches: the direct kernel over whole runs, then the tail
     if (aligned && n < kDirectMax && n >= uint64_t(G::R)) {
         const uint64_t n_runs = n / G::R;
-        static bool attr_direct = false;
-        if (!attr_direct && tab_bytes > 48 * 1024) {
-            cudaError_t e = cudaFuncSetAttribute(stream_direct_kernel<Op>,
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-            if (e != cudaSuccess) return e;
-            attr_direct = true;
-        }
+        if (cudaError_t e = ensure_dyn_smem(reinterpret_cast<const void*>(stream_direct_kernel<Op>), tab_bytes);
+            e != cudaSuccess)
+            return e;
         const uint64_t grid = std::min<uint64_t>((n_runs + kThreads - 1) / kThreads, uint64_t(sms) * 16);
         if (cudaError_t e = launch_pdl(stream_direct_kernel<Op>, dim3(static_cast<unsigned>(grid)), dim3(kThreads),
                                        tab_bytes, s, op, in0, in1, out, n_runs, status);
@@ -1001,22 +993,22 @@ cudaError_t run_stream(const Op& op, const uint8_t* in0, const uint8_t* in1, uin
     const uint64_t n_tiles = aligned ? n / G::TILE : 0;
     if (n_tiles > 0) {
         const size_t smem = G::smem_pipe + tab_bytes;
-        static bool attr_done = false;  // per instantiation
-        if (!attr_done) {
-            cudaError_t e = cudaFuncSetAttribute(stream_tma_kernel<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 227 * 1024);
-            if (e != cudaSuccess) return e;
-            attr_done = true;
-        }
-        // occupancy per instantiation and table size (a per-call query costs
-        // microseconds of host time, comparable to a small launch)
+        if (cudaError_t e = ensure_dyn_smem(reinterpret_cast<const void*>(stream_tma_kernel<Op>), smem);
+            e != cudaSuccess)
+            return e;
+        // occupancy per instantiation, device and table size (a per-call
+        // query costs microseconds of host time, comparable to a small launch)
         static thread_local size_t occ_smem = 0;
+        static thread_local int occ_dev = -1;
         static thread_local int occ_per_sm = 0;
-        if (occ_smem != smem) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (occ_smem != smem || occ_dev != dev) {
             int v = 0;
             cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, stream_tma_kernel<Op>, G::THREADS, smem);
             if (e != cudaSuccess) return e;
             occ_smem = smem;
+            occ_dev = dev;
             occ_per_sm = std::max(v, 1);
         }
         const uint64_t grid = std::min<uint64_t>(n_tiles, uint64_t(sms) * occ_per_sm);

@@ -4,6 +4,11 @@
 // stream_inst.cu.
 #include <cuda_runtime.h>
 
+#include <atomic>
+#include <map>
+#include <mutex>
+#include <utility>
+
 #include <algorithm>
 #include <cstdint>
 
@@ -15,16 +20,12 @@ namespace qpk {
 
 namespace {
 
-int g_num_sms = 0;
 
 __device__ __forceinline__ uint32_t mod_small_g(uint32_t t, uint32_t p, uint32_t magic) {
     return t - p * __umulhi(t, magic);
 }
 
-__device__ __forceinline__ void report_g(uint32_t err, uint32_t* status) {
-    err = __reduce_or_sync(0xffffffffu, err);
-    if (err && (threadIdx.x & 31) == 0 && status) atomicOr(status, err);
-}
+__device__ __forceinline__ void report_g(uint32_t err, uint32_t* status) { report_status(err, status); }
 
 // Generic REDQ for d+1 > kMaxFastDigits: one word per thread, runtime loops.
 __global__ void redq_generic_kernel(const RedqParams P, const double* __restrict__ words, uint64_t n,
@@ -139,20 +140,24 @@ __global__ void redq_u128_kernel(const RedqParams P, const unsigned __int128* __
     report_g(err, status);
 }
 
-// field ops over reps (gfq.cpp:260-294); the zero element is rep g
+// field ops over reps (gfq.cpp:260-294); the zero element is rep g; reps
+// above g latch kErrRep and are read as zero
 __global__ void gfq_rep_op_kernel(int op, uint32_t p, uint32_t group, const uint32_t* __restrict__ zech,
                                   const uint32_t* __restrict__ a, const uint32_t* __restrict__ b, uint64_t n,
                                   uint32_t* __restrict__ out, uint32_t* status) {
     pdl_wait();
     uint32_t err = 0;
     for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
-        const uint32_t x = a[i];
+        uint32_t x = a[i];
+        if (x > group) err |= kErrRep, x = group;
         uint32_t r;
         if (op == 0) {  // mul: (a + b) mod g, zero absorbs
-            const uint32_t y = b[i];
+            uint32_t y = b[i];
+            if (y > group) err |= kErrRep, y = group;
             r = (x == group || y == group) ? group : (x + y >= group ? x + y - group : x + y);
         } else if (op == 1) {  // add through the Zech table: a + plus1[(b - a) mod g]
-            const uint32_t y = b[i];
+            uint32_t y = b[i];
+            if (y > group) err |= kErrRep, y = group;
             if (x == group) {
                 r = y;
             } else if (y == group) {
@@ -173,13 +178,16 @@ __global__ void gfq_rep_op_kernel(int op, uint32_t p, uint32_t group, const uint
 }
 
 __global__ void gfq_mul_rep_kernel(uint32_t group, const uint32_t* __restrict__ a, const uint32_t* __restrict__ b,
-                                   uint64_t n, uint32_t* __restrict__ out) {
+                                   uint64_t n, uint32_t* __restrict__ out, uint32_t* status) {
+    uint32_t err = 0;
     for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
-        const uint32_t x = a[i], y = b[i];
+        uint32_t x = a[i], y = b[i];
+        if (x > group || y > group) err |= kErrRep, x = min(x, group), y = min(y, group);
         uint32_t r = x + y;
         if (r >= group) r -= group;
         out[i] = (x == group || y == group) ? group : r;
     }
+    report_g(err, status);
 }
 
 // ------------------------------------------------------------- generators
@@ -213,13 +221,32 @@ unsigned grid_for(uint64_t n) {
 }  // namespace
 
 int num_sms() {
-    if (!g_num_sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-        if (g_num_sms <= 0) g_num_sms = 148;
+    // per device ordinal (a process may drive several GPUs)
+    static std::atomic<int> cache[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) dev = 0;
+    int v = cache[dev].load(std::memory_order_relaxed);
+    if (v <= 0) {
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        if (v <= 0) v = 148;
+        cache[dev].store(v, std::memory_order_relaxed);
     }
-    return g_num_sms;
+    return v;
+}
+
+cudaError_t ensure_dyn_smem(const void* kernel, size_t bytes) {
+    if (bytes <= 48 * 1024) return cudaSuccess;
+    static std::mutex mu;
+    static std::map<std::pair<const void*, int>, size_t> done;
+    int dev = 0;
+    if (cudaError_t e = cudaGetDevice(&dev); e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lock(mu);
+    size_t& cur = done[{kernel, dev}];
+    if (bytes <= cur) return cudaSuccess;
+    const cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
+    if (e == cudaSuccess) cur = bytes;
+    return e;
 }
 
 cudaError_t launch_redq_f64(const RedqParams& P, const double* words, uint64_t n, uint8_t* out, uint32_t* status,
@@ -292,9 +319,9 @@ cudaError_t launch_gfq_elem(const GfqElemParams& P, const uint8_t* a, const uint
 }
 
 cudaError_t launch_gfq_mul_rep(uint32_t group, const uint32_t* a, const uint32_t* b, uint64_t n, uint32_t* out,
-                               cudaStream_t s) {
+                               uint32_t* status, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
-    gfq_mul_rep_kernel<<<grid_for(n), 256, 0, s>>>(group, a, b, n, out);
+    gfq_mul_rep_kernel<<<grid_for(n), 256, 0, s>>>(group, a, b, n, out, status);
     return cudaGetLastError();
 }
 
