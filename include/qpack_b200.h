@@ -124,6 +124,13 @@ QPK_API qpk_status qpk_fqt_mul(qpk_polymul_plan plan, const uint8_t* a, uint64_t
                                uint8_t* out, void* stream);
 QPK_API qpk_status qpk_fqt_mul_host(qpk_polymul_plan plan, const uint8_t* a, uint64_t na, const uint8_t* b,
                                     uint64_t nb, uint8_t* out, qpk_cost* cost);
+/* the same product with u64 coefficients (reduced mod p on input), for any p
+ * the plan accepts -- the uint8 entry points above need p <= 256
+ * (DensePoly's u64 coefficients, poly.hpp; polymul.cpp:81-147) */
+QPK_API qpk_status qpk_fqt_mul_u64(qpk_polymul_plan plan, const uint64_t* a, uint64_t na, const uint64_t* b,
+                                   uint64_t nb, uint64_t* out, void* stream);
+QPK_API qpk_status qpk_fqt_mul_u64_host(qpk_polymul_plan plan, const uint64_t* a, uint64_t na, const uint64_t* b,
+                                        uint64_t nb, uint64_t* out, qpk_cost* cost);
 
 /* --------------------------------------------------------------- GF(p^k) */
 typedef struct qpk_field_s* qpk_field;

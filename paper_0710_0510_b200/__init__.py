@@ -130,6 +130,8 @@ SIGNATURES = {
     "qpk_gfq_gemv": (I, [VP, VP, VP, U64, U64, VP, VP, VP]),
     "qpk_fqt_mul": (I, [VP, VP, U64, VP, U64, VP, VP]),
     "qpk_fqt_mul_host": (I, [VP, VP, U64, VP, U64, VP, PCost]),
+    "qpk_fqt_mul_u64": (I, [VP, VP, U64, VP, U64, VP, VP]),
+    "qpk_fqt_mul_u64_host": (I, [VP, VP, U64, VP, U64, VP, PCost]),
     "qpk_gfq_gemv_host": (I, [VP, VP, VP, U64, U64, VP, VP, PCost]),
     "qpk_gen_draws": (I, [U64, U64, U64, U32, VP, VP]),
     "qpk_gen_words": (I, [U64, U64, U64, U64, U32, VP, VP]),
@@ -346,9 +348,35 @@ class PolymulPlan:
     def sync(self):
         _check(lib().qpk_polymul_sync(self._h, _stream()))
 
+    def _fqt_mul_u64(self, a, b, out=None):
+        if _is_torch(a):
+            import torch
+            _dev(a, ("int64", "uint64"), "a")
+            _dev(b, ("int64", "uint64"), "b")
+            na, nb = a.numel(), b.numel()
+            no = na + nb - 1 if na and nb else 0
+            if out is None:
+                out = torch.empty((no,), dtype=torch.int64, device=a.device)
+            _dev(out, ("int64", "uint64"), "out", no)
+            _check(lib().qpk_fqt_mul_u64(self._h, _ptr(a), na, _ptr(b), nb, _ptr(out), _stream()))
+            return out
+        a = _host(a, np.uint64).reshape(-1)
+        b = _host(b, np.uint64).reshape(-1)
+        no = a.size + b.size - 1 if a.size and b.size else 0
+        out = np.empty((no,), np.uint64) if out is None else _out_host(out, np.uint64, no)
+        cost = Cost()
+        _check(lib().qpk_fqt_mul_u64_host(self._h, _ptr(a), a.size, _ptr(b), b.size, _ptr(out), C.byref(cost)))
+        self.last_cost = cost.as_dict()
+        return out
+
     def fqt_mul(self, a, b, out=None):
         """One product of two long polynomials (chunked FQT, fqt_mul
-        polymul.cpp:81-147): len(a)+len(b)-1 coefficients mod p."""
+        polymul.cpp:81-147): len(a)+len(b)-1 coefficients mod p.  uint8
+        coefficients for p <= 256; uint64 operands (numpy or CUDA tensors)
+        take the u64 entry points (any p)."""
+        if (_is_torch(a) and str(a.dtype) in ("torch.int64", "torch.uint64")) or \
+                (isinstance(a, np.ndarray) and a.dtype in (np.uint64, np.int64)) or self.p > 256:
+            return self._fqt_mul_u64(a, b, out)
         if _is_torch(a):
             import torch
             _dev(a, ("uint8",), "a")

@@ -243,6 +243,25 @@ qpk_status qpk_fqt_mul_host(qpk_polymul_plan plan, const uint8_t* a, uint64_t na
     });
 }
 
+qpk_status qpk_fqt_mul_u64(qpk_polymul_plan plan, const uint64_t* a, uint64_t na, const uint64_t* b, uint64_t nb,
+                           uint64_t* out, void* stream) {
+    return guard([&] {
+        need(plan != nullptr, "null plan");
+        need(na == 0 || nb == 0 || (a && b && out), "null buffer");
+        qpack::gpu::fqt_mul_device_u64(plan->pl->redq, plan->pl->params, a, na, b, nb, out, as_stream(stream));
+    });
+}
+
+qpk_status qpk_fqt_mul_u64_host(qpk_polymul_plan plan, const uint64_t* a, uint64_t na, const uint64_t* b,
+                                uint64_t nb, uint64_t* out, qpk_cost* cost) {
+    return guard([&] {
+        need(plan != nullptr, "null plan");
+        need(na == 0 || nb == 0 || (a && b && out), "null buffer");
+        qpack::gpu::fqt_mul_host_u64(plan->pl->redq, plan->pl->params, a, na, b, nb, out);
+        put_cost(cost, qpack::gpu::fqt_cost(plan->pl->redq, plan->pl->params, na, nb));
+    });
+}
+
 qpk_status qpk_polymul_batch(qpk_polymul_plan plan, const uint8_t* a, const uint8_t* b, uint64_t n, uint8_t* out,
                              void* stream) {
     return guard([&] {

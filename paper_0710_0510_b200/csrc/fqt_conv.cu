@@ -187,6 +187,91 @@ __global__ void __launch_bounds__(256) fqt_wide_conv_kernel(const FqtWideParams 
     }
 }
 
+// ---- large p (p > 256, u64 coefficients): u128 words and group sums, one
+// thread per output chunk; residues kept per coefficient as u64 ----
+struct FqtWidePParams {
+    uint64_t p, neg_q, q;
+    uint32_t k, nq, nd, qbits;  // qbits: log2 q when q is a power of two, else 0
+    u128d qpow[15];             // q^i, i < nd
+};
+
+__global__ void fqt_widep_pack_kernel(uint64_t p, uint32_t k, uint64_t q, const uint64_t* __restrict__ a,
+                                      uint64_t na, uint64_t L1, u128d* __restrict__ wa,
+                                      const uint64_t* __restrict__ b, uint64_t nb, uint64_t L2,
+                                      u128d* __restrict__ wb) {
+    pdl_wait();
+    for (uint64_t x = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; x < L1 + L2;
+         x += uint64_t(gridDim.x) * blockDim.x) {
+        const bool first = x < L1;
+        const uint64_t c = first ? x : x - L1, n = first ? na : nb;
+        const uint64_t* src = first ? a : b;
+        u128d v = 0;  // Horner (pack, dqt.cpp:23-37), coefficients reduced mod p (DensePoly)
+        for (int j = static_cast<int>(k) - 1; j >= 0; --j) {
+            const uint64_t i = c * k + j;
+            v = v * q + (i < n ? src[i] % p : 0u);
+        }
+        (first ? wa : wb)[c] = v;
+    }
+}
+
+// integer-mode REDQ of one group sum (redq.cpp:44-65) added mod p into the
+// chunk's residues
+__device__ __forceinline__ void fqt_widep_close(const FqtWidePParams& P, u128d r, uint64_t (&racc)[15]) {
+    const u128d rop = r / P.p;
+    uint64_t u[15];
+    for (uint32_t i = 0; i < P.nd; ++i) {
+        const u128d x = P.qbits ? r >> (P.qbits * i) : r / P.qpow[i];
+        const u128d y = P.qbits ? rop >> (P.qbits * i) : rop / P.qpow[i];
+        u[i] = static_cast<uint64_t>(x - static_cast<u128d>(P.p) * y);  // in [0, p)
+    }
+    for (uint32_t i = 0; i < P.nd; ++i) {
+        const uint64_t mu =
+            i + 1 < P.nd ? static_cast<uint64_t>((u[i] + static_cast<u128d>(P.neg_q) * u[i + 1]) % P.p) : u[i];
+        const uint64_t s = racc[i] + mu;  // both < p < 2^63: no wrap
+        racc[i] = s >= P.p ? s - P.p : s;
+    }
+}
+
+__global__ void __launch_bounds__(256) fqt_widep_conv_kernel(const FqtWidePParams P, const u128d* __restrict__ pw,
+                                                             uint64_t L1, const u128d* __restrict__ qw, uint64_t L2,
+                                                             uint64_t T, uint64_t* __restrict__ res) {
+    pdl_wait();
+    for (uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < T; t += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t lo = t + 1 > L2 ? t + 1 - L2 : 0, hi = t < L1 - 1 ? t : L1 - 1;
+        uint64_t racc[15] = {};
+        u128d acc = 0;
+        uint32_t cnt = 0;
+        for (uint64_t i = lo; i <= hi; ++i) {
+            acc += pw[i] * qw[t - i];  // exact: a group sum stays below q^(2k-1) <= 2^m <= 2^128
+            if (++cnt == P.nq) {
+                fqt_widep_close(P, acc, racc);
+                acc = 0;
+                cnt = 0;
+            }
+        }
+        if (cnt) fqt_widep_close(P, acc, racc);
+        for (uint32_t i = 0; i < P.nd; ++i) res[t * P.nd + i] = racc[i];
+    }
+}
+
+// out coefficient c of chunk u = c / k, j = c % k: residue j of chunk u plus
+// residue j + k of chunk u - 1 (fqt_decode's overlap, polymul.cpp:52-79)
+__global__ void fqt_widep_overlap_kernel(uint64_t p, uint32_t k, uint32_t nd, const uint64_t* __restrict__ res,
+                                         uint64_t T, uint64_t* __restrict__ out, uint64_t nout) {
+    pdl_wait();
+    for (uint64_t c = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; c < nout;
+         c += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t u = c / k;
+        const uint32_t j = static_cast<uint32_t>(c % k);
+        uint64_t v = u < T ? res[u * nd + j] : 0;
+        if (u >= 1 && j + k < nd) {
+            const uint64_t w = res[(u - 1) * nd + j + k];
+            v = v + w >= p ? v + w - p : v + w;
+        }
+        out[c] = v;
+    }
+}
+
 }  // namespace
 
 
@@ -312,6 +397,48 @@ cudaError_t launch_fqt_mul_wide(uint32_t p, uint64_t q, uint32_t k, uint32_t nq,
     return launch_pdl(fqt_overlap_kernel, dim3(static_cast<unsigned>(std::min<uint64_t>((nchunks + 255) / 256, sms * 8))),
                       dim3(kOvThreads), 0, s, p, k, 2 * k - 1, static_cast<const uint32_t*>(res), 1u, T, out, nout,
                       uint64_t(0), L1, L2);
+}
+
+uint64_t fqt_widep_workspace_bytes(uint32_t k, uint64_t na, uint64_t nb) {
+    const uint64_t L1 = fqt_chunks(na, k), L2 = fqt_chunks(nb, k), T = L1 + L2 - 1;
+    return align16(L1 * 16) + align16(L2 * 16) + T * (2 * k - 1) * 8 + 16;
+}
+
+cudaError_t launch_fqt_mul_widep(uint64_t p, uint64_t q, uint32_t k, uint32_t nq, const uint64_t* a, uint64_t na,
+                                 const uint64_t* b, uint64_t nb, uint64_t* out, void* ws, cudaStream_t s) {
+    if (na == 0 || nb == 0) return cudaSuccess;
+    if (k < 1 || k > 8 || p < 2 || p >= (uint64_t(1) << 63) || nq == 0) return cudaErrorInvalidValue;
+    FqtWidePParams P{};
+    P.p = p;
+    P.k = k;
+    P.nq = nq;
+    P.nd = 2 * k - 1;
+    P.q = q;
+    P.neg_q = (p - q % p) % p;
+    P.qbits = (q & (q - 1)) == 0 ? static_cast<uint32_t>(__builtin_ctzll(q)) : 0u;
+    u128d qp = 1;
+    for (uint32_t i = 0; i < P.nd; ++i, qp *= q) P.qpow[i] = qp;
+    const uint64_t L1 = fqt_chunks(na, k), L2 = fqt_chunks(nb, k), T = L1 + L2 - 1;
+    auto* base = static_cast<uint8_t*>(ws);
+    auto* pw = reinterpret_cast<u128d*>(base);
+    auto* qw = reinterpret_cast<u128d*>(base + align16(L1 * 16));
+    auto* res = reinterpret_cast<uint64_t*>(base + align16(L1 * 16) + align16(L2 * 16));
+    const int sms = num_sms();
+    if (cudaError_t e = launch_pdl(fqt_widep_pack_kernel,
+                                   dim3(static_cast<unsigned>(std::min<uint64_t>((L1 + L2 + 255) / 256, sms * 8))),
+                                   dim3(256), 0, s, p, k, q, a, na, L1, pw, b, nb, L2, qw);
+        e != cudaSuccess)
+        return e;
+    if (cudaError_t e = launch_pdl(fqt_widep_conv_kernel,
+                                   dim3(static_cast<unsigned>(std::min<uint64_t>((T + 255) / 256, sms * 16))),
+                                   dim3(256), 0, s, P, static_cast<const u128d*>(pw), L1, static_cast<const u128d*>(qw),
+                                   L2, T, res);
+        e != cudaSuccess)
+        return e;
+    const uint64_t nout = na + nb - 1;
+    return launch_pdl(fqt_widep_overlap_kernel,
+                      dim3(static_cast<unsigned>(std::min<uint64_t>((nout + 255) / 256, sms * 8))), dim3(256), 0, s,
+                      p, k, 2 * k - 1, static_cast<const uint64_t*>(res), T, out, nout);
 }
 
 cudaError_t launch_fqt_mul(const FqtParams& P, const uint8_t* a, uint64_t na, const uint8_t* b, uint64_t nb,

@@ -495,14 +495,17 @@ PolymulPlan::PolymulPlan(const QadicParams& pr) : params(pr) {
     const ValidationResult vr = validate(pr);
     if (!vr.ok()) throw std::invalid_argument("dqt_mul_poly: " + vr.detail);
     if (pr.k > 8) throw std::invalid_argument("qpack-b200 polymul: device path packs at most k = 8 coefficients");
-    if (pr.p > 256) throw std::invalid_argument("qpack-b200 polymul: residues are uint8, p must be <= 256");
     redq = fqt_reduction_plan(pr, pr.k - 1);
+    P.k = pr.k;
+    // p > 256: only the u64-coefficient FQT entry points (no uint8 residues,
+    // no device REDQ mirror)
+    if (pr.p > 256) return;
     DevicePlanCache& dp = detail::device_plan(redq);
     P.rq = dp.prm;
-    P.k = pr.k;
 }
 
 void polymul_device(PolymulPlan& pl, const uint8_t* a, const uint8_t* b, u64 n, uint8_t* out, cudaStream_t s) {
+    if (pl.params.p > 256) throw std::invalid_argument("qpack-b200 polymul: residues are uint8, p must be <= 256");
     if (pl.params.k > static_cast<u32>(qpk::kMaxGfqK))
         throw std::invalid_argument("qpack-b200 polymul: the batched path packs at most k = 4 coefficients");
     // the batched kernel multiplies packed words in fp64: exact while the
@@ -515,6 +518,7 @@ void polymul_device(PolymulPlan& pl, const uint8_t* a, const uint8_t* b, u64 n, 
 }
 
 void polymul_host(PolymulPlan& pl, const uint8_t* a, const uint8_t* b, u64 n, uint8_t* out) {
+    if (pl.params.p > 256) throw std::invalid_argument("qpack-b200 polymul: residues are uint8, p must be <= 256");
     DevicePlanCache& dp = detail::device_plan(pl.redq);
     std::lock_guard<std::mutex> lock(dp.mu);
     if (!dp.staging) dp.staging = std::make_unique<Staging>();
@@ -541,8 +545,9 @@ void polymul_host(PolymulPlan& pl, const uint8_t* a, const uint8_t* b, u64 n, ui
 }
 
 // ---- chunked FQT product (K6) ----
-void fqt_check(const RedqPlan& plan, const QadicParams& params) {
-    if (params.p > 256) throw std::invalid_argument("qpack-b200 fqt_mul: coefficients are uint8, p must be <= 256");
+void fqt_check(const RedqPlan& plan, const QadicParams& params, bool wide_p = false) {
+    if (!wide_p && params.p > 256)
+        throw std::invalid_argument("qpack-b200 fqt_mul: uint8 coefficients need p <= 256 (u64 entry points: any p)");
     if (params.k < 1 || params.k > 8)
         throw std::invalid_argument("qpack-b200 fqt_mul: the device path packs 1..8 coefficients per chunk");
     if (plan.p != params.p || plan.q != params.q || plan.d != 2 * (params.k - 1))
@@ -588,6 +593,33 @@ void fqt_mul_host(const RedqPlan& plan, const QadicParams& params, const uint8_t
     check(cudaMemcpy(db, b, nb, cudaMemcpyHostToDevice), "H2D");
     fqt_mul_device(plan, params, da, na, db, nb, dc, 0);
     check(cudaMemcpy(out, dc, na + nb - 1, cudaMemcpyDeviceToHost), "D2H");
+}
+
+// p > 256 (or any p): u64 coefficients, u128 words (launch_fqt_mul_widep)
+void fqt_mul_device_u64(const RedqPlan& plan, const QadicParams& params, const uint64_t* a, u64 na, const uint64_t* b,
+                        u64 nb, uint64_t* out, cudaStream_t s) {
+    fqt_check(plan, params, true);
+    if (na == 0 || nb == 0) return;
+    gpu::require_device();
+    StreamBuf ws(qpk::fqt_widep_workspace_bytes(params.k, na, nb), s);
+    check(qpk::launch_fqt_mul_widep(params.p, params.q, params.k, static_cast<uint32_t>(std::max<u64>(params.n_q, 1)),
+                                    a, na, b, nb, out, ws.ptr, s),
+          "fqt_mul (u64 coefficients) launch");
+}
+
+void fqt_mul_host_u64(const RedqPlan& plan, const QadicParams& params, const uint64_t* a, u64 na, const uint64_t* b,
+                      u64 nb, uint64_t* out) {
+    fqt_check(plan, params, true);
+    if (na == 0 || nb == 0) return;
+    gpu::require_device();
+    DevBuf da, db, dc;  // per call: no device plan mirror for p > 256
+    da.ensure(na * 8);
+    db.ensure(nb * 8);
+    dc.ensure((na + nb - 1) * 8);
+    check(cudaMemcpy(da.ptr, a, na * 8, cudaMemcpyHostToDevice), "H2D");
+    check(cudaMemcpy(db.ptr, b, nb * 8, cudaMemcpyHostToDevice), "H2D");
+    fqt_mul_device_u64(plan, params, da.as<uint64_t>(), na, db.as<uint64_t>(), nb, dc.as<uint64_t>(), 0);
+    check(cudaMemcpy(out, dc.ptr, (na + nb - 1) * 8, cudaMemcpyDeviceToHost), "D2H");
 }
 
 CostReport fqt_cost(const RedqPlan& plan, const QadicParams& params, u64 na, u64 nb) {

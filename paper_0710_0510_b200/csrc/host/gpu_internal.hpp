@@ -42,6 +42,11 @@ void fqt_mul_device(const RedqPlan& plan, const QadicParams& params, const uint8
                     u64 nb, uint8_t* out, cudaStream_t s);
 void fqt_mul_host(const RedqPlan& plan, const QadicParams& params, const uint8_t* a, u64 na, const uint8_t* b, u64 nb,
                   uint8_t* out);
+// any p (u64 coefficients, reduced mod p; the reference's DensePoly range)
+void fqt_mul_device_u64(const RedqPlan& plan, const QadicParams& params, const uint64_t* a, u64 na, const uint64_t* b,
+                        u64 nb, uint64_t* out, cudaStream_t s);
+void fqt_mul_host_u64(const RedqPlan& plan, const QadicParams& params, const uint64_t* a, u64 na, const uint64_t* b,
+                      u64 nb, uint64_t* out);
 CostReport fqt_cost(const RedqPlan& plan, const QadicParams& params, u64 na, u64 nb);
 
 void gfq_mul_device(detail::DeviceFieldCache& F, const uint8_t* a, const uint8_t* b, u64 n, uint8_t* out, int path,

@@ -203,6 +203,14 @@ uint64_t fqt_wide_workspace_bytes(uint32_t k, uint64_t na, uint64_t nb);
 cudaError_t launch_fqt_mul_wide(uint32_t p, uint64_t q, uint32_t k, uint32_t nq, const uint8_t* a, uint64_t na,
                                 const uint8_t* b, uint64_t nb, uint8_t* out, void* ws, cudaStream_t s);
 
+// FQT product for p > 256 (any p < 2^63; the uint8 kernels above cover
+// p <= 256): u64 coefficients in and out (reduced mod p), u128 words and
+// group sums, integer-mode REDQ per group with the direct correction, one
+// thread per output chunk.  ws: fqt_widep_workspace_bytes.
+uint64_t fqt_widep_workspace_bytes(uint32_t k, uint64_t na, uint64_t nb);
+cudaError_t launch_fqt_mul_widep(uint64_t p, uint64_t q, uint32_t k, uint32_t nq, const uint64_t* a, uint64_t na,
+                                 const uint64_t* b, uint64_t nb, uint64_t* out, void* ws, cudaStream_t s);
+
 // ws: fqt_workspace_bytes (packed chunks and per-chunk residue partials).
 uint64_t fqt_workspace_bytes(uint32_t k, uint32_t nq, uint64_t na, uint64_t nb);
 cudaError_t launch_fqt_mul(const FqtParams& P, const uint8_t* a, uint64_t na, const uint8_t* b, uint64_t nb,
