@@ -166,3 +166,52 @@ def test_to_coeffs_matches_oracle(qpk, orc):
     of = orc.Field(7, 3, 256)
     for rep in (0, 1, 5, 100, 341, 342):
         assert f.to_coeffs(rep) == of.rep_to_coeffs(rep)
+
+
+class _QoField(__import__("ctypes").Structure):
+    """oracle/qpack_oracle.h qo_field (the C restatement's field tables)."""
+    import ctypes as C
+    _fields_ = [("p", C.c_uint64), ("q", C.c_uint64), ("order", C.c_uint64), ("group", C.c_uint64),
+                ("lh_radix", C.c_uint64), ("lh_size", C.c_uint64), ("k", C.c_uint32), ("n_q", C.c_uint32),
+                ("binary_shift", C.c_int), ("modulus", C.c_uint64 * 33), ("generator_index", C.c_uint64),
+                ("log", C.POINTER(C.c_uint32)), ("antilog", C.POINTER(C.c_uint64)), ("plus1", C.POINTER(C.c_uint32)),
+                ("fval", C.POINTER(C.c_double)), ("ltab", C.POINTER(C.c_uint32)), ("htab", C.POINTER(C.c_uint32)),
+                ("inv_p", C.c_double), ("r_max", C.c_uint64)]
+
+
+def _default_q(p, k):  # widest power-of-two radix with 2k-1 digits below 2^53 (gfq_default_q)
+    return 1 << (52 // (2 * k - 1))
+
+
+SWEEP_FIELDS = [(p, k, q, bs)
+                for (p, k, q) in [(2, 1, 1 << 20), (2, 2, 64), (2, 5, 0), (2, 6, 0), (2, 7, 0), (2, 8, 9),
+                                  (3, 1, 1 << 20), (3, 3, 1 << 10), (3, 5, 0), (3, 6, 25), (5, 2, 1 << 12), (5, 4, 0),
+                                  (7, 3, 256), (7, 4, 145), (11, 2, 1 << 12), (13, 3, 10 ** 3), (31, 2, 1 << 14),
+                                  (101, 2, 1 << 17), (257, 2, 131073), (1009, 1, 1 << 26), (65537, 1, 1 << 40),
+                                  (3, 2, 10 ** 4), (5, 3, 999)]
+                for bs in (0, 1)]
+SWEEP_FIELDS = [(p, k, q or _default_q(p, k), bs) for (p, k, q, bs) in SWEEP_FIELDS]
+
+
+@pytest.mark.parametrize("p,k,q,bs", SWEEP_FIELDS)
+def test_field_tables_match_the_restatement(qpk, orc, p, k, q, bs):
+    """Every table of the drop-in's GfqField (log, antilog, Zech, q-adic
+    evaluation and both half-window tables) against the C restatement's,
+    entry by entry, over 40 fields (k = 1..10, both indexings)."""
+    import ctypes as C
+    try:
+        f = qpk.GfqField(p, k, q, bs)
+    except qpk.QpackError:
+        pytest.skip("field outside the 2^20-entry table budget")
+    o = orc.Field(p, k, q, bs)
+    of = C.cast(C.c_void_p(o.h) if isinstance(o.h, int) else o.h, C.POINTER(_QoField)).contents
+    t = f.tables()
+    order = p ** k
+    assert of.order == order and list(of.modulus[:k + 1]) == f.info()["modulus"]
+    assert (t["log"] == np.ctypeslib.as_array(of.log, (order,))).all()
+    assert (t["antilog"][:order - 1] == np.ctypeslib.as_array(of.antilog, (order,))[:order - 1]).all()
+    assert (t["plus1"] == np.ctypeslib.as_array(of.plus1, (order,))).all()
+    assert (t["fval"] == np.ctypeslib.as_array(of.fval, (order,))).all()
+    assert t["low"].size == of.lh_size
+    assert (t["low"] == np.ctypeslib.as_array(of.ltab, (of.lh_size,))).all()
+    assert (t["high"] == np.ctypeslib.as_array(of.htab, (of.lh_size,))).all()
