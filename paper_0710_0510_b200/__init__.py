@@ -523,10 +523,12 @@ class GfqField:
         _check(lib().qpk_gfq_mul_rep_host(self._h, _ptr(a), _ptr(b), a.size, _ptr(out)))
         return out
 
-    def matmul(self, A, B, m, K, n, chunk=0, out=None, repack="redq"):
+    def matmul(self, A, B, m, K, n, chunk=0, out=None, repack="redq", counters=False):
         """C = A*B on coefficient records (A m x K x k, B K x n x k).
         repack: "redq" (delayed REDQ re-pack, the default) or "fold"
-        (GF(3^3) at q = 2^10 only; same C)."""
+        (GF(3^3) at q = 2^10 only; same C).  counters=True (host buffers):
+        self.last_cost gets the reference's gfq_matmul counters, the
+        data-dependent Zech reads included (an extra device pass, K7)."""
         if repack not in ("redq", "fold"):
             raise InvalidArgument(f"gfq_matmul: unknown re-pack mode {repack!r}")
         mode = {"redq": 0, "fold": 1}[repack]
@@ -548,11 +550,11 @@ class GfqField:
         out = np.empty((m, n, self.k), np.uint8) if out is None else _out_host(out, np.uint8, m * n * k)
         cost = Cost()
         _check(lib().qpk_gfq_matmul_repack_host(self._h, _ptr(A), _ptr(B), m, K, n, chunk, mode, _ptr(out),
-                                                C.byref(cost)))
-        self.last_cost = cost.as_dict()
+                                                C.byref(cost) if counters else None))
+        self.last_cost = cost.as_dict() if counters else None
         return out
 
-    def gemv(self, A, x, coeffs=False, out=None):
+    def gemv(self, A, x, coeffs=False, out=None, counters=True):
         """y = A x on reps (A m x K, x K): each y_i = fgdp_dot(A[i,:], x) on
         the GPU.  Returns reps (m,) or, with coeffs=True, coefficients (m, k)."""
         if _is_torch(A):
@@ -584,8 +586,8 @@ class GfqField:
             _out_host(out, np.uint8 if coeffs else np.uint32, m * (self.k if coeffs else 1))
         cost = Cost()
         _check(lib().qpk_gfq_gemv_host(self._h, _ptr(A), _ptr(x), m, K, None if coeffs else _ptr(out),
-                                       _ptr(out) if coeffs else None, C.byref(cost)))
-        self.last_cost = cost.as_dict()
+                                       _ptr(out) if coeffs else None, C.byref(cost) if counters else None))
+        self.last_cost = cost.as_dict() if counters else None
         return out
 
     def fgdp_dot_gpu(self, v1, v2):
@@ -597,8 +599,10 @@ class GfqField:
         y = self.gemv(v1.reshape(1, -1), v2)
         return int(y[0]), self.last_cost
 
-    def matmul_rep(self, A, B, out=None):
-        """The reference gfq_matmul on GfqMatrix data (reps in, reps out)."""
+    def matmul_rep(self, A, B, out=None, counters=False):
+        """The reference gfq_matmul on GfqMatrix data (reps in, reps out);
+        counters=True (host buffers): self.last_cost = the reference's
+        CostReport, data-dependent Zech reads included (K7)."""
         if _is_torch(A):
             import torch
             _dev(A, ("int32", "uint32"), "A")
@@ -620,8 +624,9 @@ class GfqField:
         n = B.shape[1]
         out = np.empty((m, n), np.uint32) if out is None else _out_host(out, np.uint32, m * n)
         cost = Cost()
-        _check(lib().qpk_gfq_matmul_rep_host(self._h, _ptr(A), _ptr(B), m, K, n, _ptr(out), C.byref(cost)))
-        self.last_cost = cost.as_dict()
+        _check(lib().qpk_gfq_matmul_rep_host(self._h, _ptr(A), _ptr(B), m, K, n, _ptr(out),
+                                             C.byref(cost) if counters else None))
+        self.last_cost = cost.as_dict() if counters else None
         return out
 
 

@@ -436,19 +436,18 @@ qpk_status qpk_gfq_matmul(qpk_field f, const uint8_t* A, const uint8_t* B, uint6
     });
 }
 
+// counters of C = A*B: the reference's closed-form part plus, when the
+// caller asked for them, the data-dependent Zech reads (K7)
+static void put_matmul_cost(qpk_cost* cost, const qpack::GfqField& f, uint64_t m, uint64_t K, uint64_t n, uint64_t zech) {
+    if (!cost) return;
+    qpack::CostReport c = qpack::gpu::matmul_cost(f, m, K, n);
+    c.table_accesses += zech;
+    put_cost(cost, c);
+}
+
 qpk_status qpk_gfq_matmul_host(qpk_field f, const uint8_t* A, const uint8_t* B, uint64_t m, uint64_t K, uint64_t n,
                                uint32_t chunk, uint8_t* C, qpk_cost* cost) {
-    return guard([&] {
-        need(f != nullptr, "null field");
-        need((m == 0 || n == 0) || (A && B && C) || K == 0, "null buffer");
-        if (m && n) {
-            if (K == 0)
-                std::memset(C, 0, m * n * f->f.k());
-            else
-                qpack::gpu::gfq_matmul_host(qpack::detail::device_field(f->f), f->f, A, B, m, K, n, chunk, C, false);
-        }
-        put_cost(cost, qpack::gpu::matmul_cost(f->f, m, K, n));
-    });
+    return qpk_gfq_matmul_repack_host(f, A, B, m, K, n, chunk, qpk::kRepackRedq, C, cost);
 }
 
 qpk_status qpk_gfq_matmul_repack(qpk_field f, const uint8_t* A, const uint8_t* B, uint64_t m, uint64_t K,
@@ -470,14 +469,15 @@ qpk_status qpk_gfq_matmul_repack_host(qpk_field f, const uint8_t* A, const uint8
     return guard([&] {
         need(f != nullptr, "null field");
         need((m == 0 || n == 0) || (A && B && C) || K == 0, "null buffer");
+        uint64_t zech = 0;
         if (m && n) {
             if (K == 0)
                 std::memset(C, 0, m * n * f->f.k());
             else
                 qpack::gpu::gfq_matmul_host(qpack::detail::device_field(f->f), f->f, A, B, m, K, n, chunk, C, false,
-                                            repack);
+                                            repack, cost ? &zech : nullptr);
         }
-        put_cost(cost, qpack::gpu::matmul_cost(f->f, m, K, n));
+        put_matmul_cost(cost, f->f, m, K, n, zech);
     });
 }
 
@@ -508,16 +508,17 @@ qpk_status qpk_gfq_matmul_rep_host(qpk_field f, const uint32_t* A, const uint32_
         // gfq_matmul(GfqMatrix...) on the caller's rep arrays in place (no
         // GfqMatrix copies); reps outside the field are detected on the
         // device (the K1 pack) and raise out_of_range like the reference
+        uint64_t zech = 0;
         if (m != 0 && n != 0) {
             if (K == 0) {
                 const uint32_t zero = static_cast<uint32_t>(f->f.order() - 1);
                 std::fill(C, C + m * n, zero);
             } else {
                 qpack::gpu::gfq_matmul_host(qpack::detail::device_field(f->f), f->f, A, B, m, K, n, 0, C, true,
-                                            qpk::kRepackRedq);
+                                            qpk::kRepackRedq, cost ? &zech : nullptr);
             }
         }
-        put_cost(cost, qpack::gpu::matmul_cost(f->f, m, K, n));
+        put_matmul_cost(cost, f->f, m, K, n, zech);
     });
 }
 
@@ -537,8 +538,10 @@ qpk_status qpk_gfq_gemv_host(qpk_field f, const uint32_t* A, const uint32_t* x, 
         need(f != nullptr, "null field");
         need(m == 0 || ((A || K == 0) && (x || K == 0) && (y_rep || y_coeff)), "null buffer");
         // reps outside the field are detected on the device (out_of_range)
-        if (m) qpack::gpu::gfq_gemv_host(qpack::detail::device_field(f->f), f->f, A, x, m, K, y_rep, y_coeff);
-        put_cost(cost, qpack::gpu::gemv_cost(f->f, m, K));
+        uint64_t zech = 0;
+        if (m) qpack::gpu::gfq_gemv_host(qpack::detail::device_field(f->f), f->f, A, x, m, K, y_rep, y_coeff,
+                                         cost ? &zech : nullptr);
+        put_matmul_cost(cost, f->f, m, K, 1, zech);
     });
 }
 

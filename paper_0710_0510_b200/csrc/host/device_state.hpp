@@ -113,6 +113,8 @@ struct DeviceFieldCache {
     gpu::DevBuf fval;    // rep -> q-adic double
     gpu::DevBuf zech;    // plus-one table (GfqField::add), uploaded on first use
     gpu::DevBuf status;  // data-error flag of the rep ops (inverse of zero)
+    gpu::DevBuf lh_reps; // low | high as reps, for the K7 counter (uploaded on first use)
+    gpu::DevBuf counter; // K7 total
     qpk::GfqElemParams elem{};
     qpk::GfqMatmulParams mm{};
     qpk::GfqGemvParams gemv{};

@@ -860,7 +860,7 @@ void gfq_matmul_device(DeviceFieldCache& F, const GfqField& field, const void* A
 }
 
 void gfq_matmul_host(DeviceFieldCache& F, const GfqField& field, const void* A, const void* B, u64 m, u64 K, u64 n,
-                     uint32_t chunk, void* C, bool reps, uint32_t repack) {
+                     uint32_t chunk, void* C, bool reps, uint32_t repack, u64* zech_reads) {
     std::lock_guard<std::mutex> lock(F.mu);
     const u64 es = reps ? 4 : field.k();
     auto* da = F.io_a.ensure(m * K * es);
@@ -871,12 +871,68 @@ void gfq_matmul_host(DeviceFieldCache& F, const GfqField& field, const void* A, 
     gfq_matmul_device(F, field, da, db, m, K, n, chunk, dc, reps, 0, repack);
     check(cudaMemcpy(C, dc, m * n * es, cudaMemcpyDeviceToHost), "D2H");
     if (reps) raise_field_status(take_field_status(F, 0));
+    if (zech_reads && m && n && K) {
+        // the reference's data-dependent counter part (K7), on rep operands
+        const uint32_t* ra = static_cast<const uint32_t*>(da);
+        const uint32_t* rb = static_cast<const uint32_t*>(db);
+        StreamBuf wa(reps ? 0 : m * K * 4, 0), wb(reps ? 0 : K * n * 4, 0);
+        if (!reps) {
+            const qpk::GfqElemParams& E = F.elem;
+            check(qpk::launch_coeffs_to_reps(E.p, E.k, E.log, static_cast<const uint8_t*>(da), m * K, wa.as<uint32_t>(), 0),
+                  "coeffs -> reps");
+            check(qpk::launch_coeffs_to_reps(E.p, E.k, E.log, static_cast<const uint8_t*>(db), K * n, wb.as<uint32_t>(), 0),
+                  "coeffs -> reps");
+            ra = wa.as<uint32_t>();
+            rb = wb.as<uint32_t>();
+        }
+        *zech_reads = zech_reads_device(F, field, ra, rb, m, K, n, 0);
+    }
+}
+
+u64 zech_reads_device(DeviceFieldCache& F, const GfqField& field, const uint32_t* A, const uint32_t* B, u64 m, u64 K,
+                      u64 n, cudaStream_t s) {
+    if (m == 0 || n == 0 || K == 0) return 0;
+    if (field.k() > qpk::kMaxCountK) throw std::invalid_argument("qpack-b200 counters: k <= 8");
+    const std::vector<u32>& lo = detail::FieldAccess::low(field);
+    const std::vector<u32>& hi = detail::FieldAccess::high(field);
+    const std::vector<u32>& z = detail::FieldAccess::zech(field);
+    if (!F.lh_reps.ptr) {
+        std::vector<uint32_t> host(lo.begin(), lo.end());
+        host.insert(host.end(), hi.begin(), hi.end());
+        host.insert(host.end(), z.begin(), z.end());
+        F.lh_reps.ensure(host.size() * 4);
+        check(cudaMemcpy(F.lh_reps.ptr, host.data(), host.size() * 4, cudaMemcpyHostToDevice), "counter tables upload");
+        F.counter.ensure(8);
+        detail::settle_uploads();
+    }
+    qpk::GfqCountParams P{};
+    P.p = static_cast<uint32_t>(field.p());
+    P.k = field.k();
+    P.group = static_cast<uint32_t>(field.order() - 1);
+    P.lh_radix = static_cast<uint32_t>(detail::FieldAccess::lh_radix(field));
+    const u64 q = detail::FieldAccess::q(field);
+    P.qbits = is_pow2(q) ? bit_width_u128(q) - 1 : 0;
+    P.n_q = field.params().n_q;
+    u64 qi = 1;
+    for (u32 i = 0; i < 2 * field.k() - 1; ++i, qi *= q) P.qpow[i] = qi;
+    P.fval = F.fval.as<double>();
+    P.low = F.lh_reps.as<uint32_t>();
+    P.high = P.low + lo.size();
+    P.zech = P.high + hi.size();
+    auto* total = F.counter.as<unsigned long long>();
+    check(cudaMemsetAsync(total, 0, 8, s), "counter clear");
+    check(qpk::launch_gfq_count(P, A, B, m, K, n, total, s), "gfq counter launch");
+    unsigned long long v = 0;
+    check(cudaMemcpyAsync(&v, total, 8, cudaMemcpyDeviceToHost, s), "counter read");
+    check(cudaStreamSynchronize(s), "counter sync");
+    return v;
 }
 
 CostReport matmul_cost(const GfqField& field, u64 m, u64 K, u64 n) {
     // reference grouping (gfq.cpp:346-385): ceil(K/n_q) groups per entry;
-    // table_accesses counts the operand and L/H lookups, not the Zech adds
-    // whose count depends on intermediate zeros
+    // table_accesses here counts the operand and L/H lookups; the Zech reads
+    // of the two additions per group depend on the data: callers that report
+    // counters add zech_reads_device (K7)
     const u64 groups = K ? (K + field.params().n_q - 1) / field.params().n_q : 0;
     CostReport c;
     c.mul_add = m * n * K;
@@ -905,7 +961,7 @@ void gfq_gemv_device(DeviceFieldCache& F, const GfqField& field, const uint32_t*
 }
 
 void gfq_gemv_host(DeviceFieldCache& F, const GfqField& field, const uint32_t* A, const uint32_t* x, u64 m, u64 K,
-                   uint32_t* y_rep, uint8_t* y_coeff) {
+                   uint32_t* y_rep, uint8_t* y_coeff, u64* zech_reads) {
     std::lock_guard<std::mutex> lock(F.mu);
     auto* da = static_cast<uint32_t*>(F.io_a.ensure(std::max<u64>(m * K, 1) * 4));
     auto* dx = static_cast<uint32_t*>(F.io_b.ensure(std::max<u64>(K, 1) * 4));
@@ -918,6 +974,7 @@ void gfq_gemv_host(DeviceFieldCache& F, const GfqField& field, const uint32_t* A
     if (y_rep) check(cudaMemcpy(y_rep, dr, m * 4, cudaMemcpyDeviceToHost), "D2H");
     if (y_coeff) check(cudaMemcpy(y_coeff, dc, m * field.k(), cudaMemcpyDeviceToHost), "D2H");
     raise_field_status(take_field_status(F, 0));
+    if (zech_reads) *zech_reads = zech_reads_device(F, field, da, dx, m, K, 1, 0);
 }
 
 CostReport gemv_cost(const GfqField& field, u64 m, u64 K) {
@@ -935,9 +992,14 @@ void gfq_gemv(std::span<const GfqElt> A, std::span<const GfqElt> x, std::size_t 
         for (const GfqElt& e : v)
             if (e.rep >= field.order()) throw std::out_of_range("gfq_gemv: rep outside the field");
     static_assert(sizeof(GfqElt) == 4, "GfqElt is one u32 rep");
+    u64 zech = 0;
     gfq_gemv_host(detail::device_field(field), field, reinterpret_cast<const uint32_t*>(A.data()),
-                  reinterpret_cast<const uint32_t*>(x.data()), m, K, reinterpret_cast<uint32_t*>(y.data()), nullptr);
-    if (cost) *cost += gemv_cost(field, m, K);
+                  reinterpret_cast<const uint32_t*>(x.data()), m, K, reinterpret_cast<uint32_t*>(y.data()), nullptr,
+                  cost ? &zech : nullptr);
+    if (cost) {
+        *cost += gemv_cost(field, m, K);
+        cost->table_accesses += zech;
+    }
 }
 
 GfqElt fgdp_dot(std::span<const GfqElt> v1, std::span<const GfqElt> v2, const GfqField& field, CostReport* cost) {
@@ -953,9 +1015,13 @@ void gfq_matmul_coeffs(std::span<const std::uint8_t> A, std::span<const std::uin
     const u64 k = field.k();
     if (A.size() != m * K * k || B.size() != K * n * k || C.size() < m * n * k)
         throw std::invalid_argument("gfq_matmul_coeffs: span sizes do not match m x K x k / K x n x k / m x n x k");
+    u64 zech = 0;
     gfq_matmul_host(detail::device_field(field), field, A.data(), B.data(), m, K, n, chunk, C.data(), false,
-                    static_cast<std::uint32_t>(repack));
-    if (cost) *cost += matmul_cost(field, m, K, n);
+                    static_cast<std::uint32_t>(repack), cost ? &zech : nullptr);
+    if (cost) {
+        *cost += matmul_cost(field, m, K, n);
+        cost->table_accesses += zech;
+    }
 }
 
 }  // namespace qpack::gpu
@@ -970,9 +1036,13 @@ GfqMatrix gfq_matmul(const GfqMatrix& a, const GfqMatrix& b, const GfqField& fie
     for (const auto* mtx : {&a, &b})
         for (const GfqElt& e : mtx->data)
             if (e.rep >= field.order()) throw std::out_of_range("gfq_matmul: rep outside the field");
+    u64 zech = 0;
     gpu::gfq_matmul_host(detail::device_field(field), field, a.data.data(), b.data.data(), a.rows, a.cols, b.cols, 0,
-                         c.data.data(), true);
-    if (cost) *cost += gpu::matmul_cost(field, a.rows, a.cols, b.cols);
+                         c.data.data(), true, qpk::kRepackRedq, cost ? &zech : nullptr);
+    if (cost) {
+        *cost += gpu::matmul_cost(field, a.rows, a.cols, b.cols);
+        cost->table_accesses += zech;  // the reference's Zech reads, replayed on the device (K7)
+    }
     return c;
 }
 

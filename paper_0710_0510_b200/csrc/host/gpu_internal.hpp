@@ -61,14 +61,19 @@ uint32_t resolve_chunk(const detail::DeviceFieldCache& F, const GfqField& field,
                        uint32_t repack = 0);
 void gfq_matmul_device(detail::DeviceFieldCache& F, const GfqField& field, const void* A, const void* B, u64 m, u64 K,
                        u64 n, uint32_t chunk, void* C, bool reps, cudaStream_t s, uint32_t repack = 0);
+// zech_reads: when given, also the reference's data-dependent counter part (K7)
 void gfq_matmul_host(detail::DeviceFieldCache& F, const GfqField& field, const void* A, const void* B, u64 m, u64 K,
-                     u64 n, uint32_t chunk, void* C, bool reps, uint32_t repack = 0);
+                     u64 n, uint32_t chunk, void* C, bool reps, uint32_t repack = 0, u64* zech_reads = nullptr);
 CostReport matmul_cost(const GfqField& field, u64 m, u64 K, u64 n);
+// fgdp_dot's data-dependent Zech reads summed over C = A*B (K7), A and B
+// device rep arrays (m x K, K x n); synchronous on stream s
+u64 zech_reads_device(detail::DeviceFieldCache& F, const GfqField& field, const uint32_t* A, const uint32_t* B, u64 m,
+                      u64 K, u64 n, cudaStream_t s);
 
 void gfq_gemv_device(detail::DeviceFieldCache& F, const GfqField& field, const uint32_t* A, const uint32_t* x, u64 m,
                      u64 K, uint32_t* y_rep, uint8_t* y_coeff, cudaStream_t s);
 void gfq_gemv_host(detail::DeviceFieldCache& F, const GfqField& field, const uint32_t* A, const uint32_t* x, u64 m,
-                   u64 K, uint32_t* y_rep, uint8_t* y_coeff);
+                   u64 K, uint32_t* y_rep, uint8_t* y_coeff, u64* zech_reads = nullptr);
 CostReport gemv_cost(const GfqField& field, u64 m, u64 K);
 
 }  // namespace qpack::gpu

@@ -122,6 +122,18 @@ struct GfqGemvParams {
     uint32_t* status;     // the field's error word: kErrRep for reps >= order (read as zero)
 };
 
+// K7: fgdp_dot's data-dependent Zech reads, replayed per gfq_matmul output.
+constexpr uint32_t kMaxCountK = 8;
+struct GfqCountParams {
+    uint32_t p, k, group, lh_radix, qbits;  // qbits: log2 q for q = 2^b, else 0
+    uint64_t n_q;
+    uint64_t qpow[2 * kMaxCountK - 1];      // q^i
+    const double* fval;                     // rep -> q-adic evaluation
+    const uint32_t* low;                    // lh^k reps (GfqField low table)
+    const uint32_t* high;                   // lh^k reps
+    const uint32_t* zech;                   // order reps (plus-one table)
+};
+
 // Chunked FQT product of two long polynomials (K6, fqt_mul polymul.cpp:81-147).
 struct FqtParams {
     RedqParams rq;  // fqt_reduction_plan: d = 2k-2 (ND = 2k-1 <= 15)
@@ -225,6 +237,11 @@ cudaError_t launch_gen_words(uint64_t seed, uint64_t first, uint64_t n, uint64_t
 // record pairs: a[i] = draws 2k*i+1..2k*i+k, b[i] = the next k
 cudaError_t launch_gen_pairs(uint64_t seed, uint64_t n, uint32_t k, uint32_t bound, uint8_t* a, uint8_t* b,
                              cudaStream_t s);
+
+// total (added atomically) += Zech-table reads of fgdp_dot(A[i,:], B[:,j]) over
+// all outputs; A m x K and B K x n reps, row-major
+cudaError_t launch_gfq_count(const GfqCountParams& P, const uint32_t* A, const uint32_t* B, uint64_t m, uint64_t K,
+                             uint64_t n, unsigned long long* total, cudaStream_t s);
 
 // fp64 peak probes (roofline denominators): returns flop count per launch
 cudaError_t launch_probe_dfma(double* sink, int iters, uint64_t* flops, cudaStream_t s);
