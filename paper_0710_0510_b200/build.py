@@ -30,7 +30,7 @@ NVCC_FLAGS = f"{ARCH} -lineinfo -O3 -std=c++17 -Xcompiler -fPIC -I{CSRC} -I{ROOT
 CXX_FLAGS = f"-std=c++20 -O2 -fPIC -Wall -Wextra -I{CSRC} -I{ROOT}/include -I{CUDA}/include"
 
 CU_UNITS = [("stream_main.cu", None), ("gfq_matmul_main.cu", None), ("gfq_gemv.cu", None), ("fqt_conv.cu", None),
-            ("probe.cu", None), ("gfq_count.cu", None)]
+            ("probe.cu", None), ("gfq_count.cu", None), ("gfq_wide.cu", None)]
 CU_UNITS += [("stream_inst.cu", i) for i in range(1, 9)]
 CU_UNITS += [("fqt_conv_inst.cu", nd) for nd in range(1, 16, 2)]
 CU_UNITS += [("gfq_matmul_inst.cu", (k, 0)) for k in range(1, 5)] + [("gfq_matmul_inst.cu", (k, 1)) for k in (2, 3)]

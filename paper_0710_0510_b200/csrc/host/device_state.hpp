@@ -114,6 +114,11 @@ struct DeviceFieldCache {
     gpu::DevBuf zech;    // plus-one table (GfqField::add), uploaded on first use
     gpu::DevBuf status;  // data-error flag of the rep ops (inverse of zero)
     gpu::DevBuf lh_reps; // low | high as reps, for the K7 counter (uploaded on first use)
+    // fields outside the byte-packed form (k > 4 or p > 255): rep-domain
+    // kernels (gfq_wide.cu) over log | antilog | low | high | zech
+    bool wide = false;
+    gpu::DevBuf wide_tabs;
+    qpk::GfqWideParams wp{};
     gpu::DevBuf counter; // K7 total
     qpk::GfqElemParams elem{};
     qpk::GfqMatmulParams mm{};

@@ -193,6 +193,60 @@ CostReport redq_batch_cost(const RedqPlan& plan, u64 n) {
     return c;
 }
 
+// GF(p^k) outside the byte-packed form (k > 4 or p > 255): the rep-domain
+// tables of gfq_wide.cu in global memory (they may exceed shared memory)
+std::shared_ptr<DeviceFieldCache> build_wide_field(const GfqField& f) {
+    const u64 p = f.p(), q = FieldAccess::q(f), order = f.order();
+    const u32 k = f.k();
+    if (k > qpk::kMaxWideK) throw std::invalid_argument("qpack-b200 GF(p^k): k <= 8 (every field with q^(2k-1) < 2^53)");
+    auto c = std::make_shared<DeviceFieldCache>();
+    c->wide = true;
+    std::vector<uint32_t> host;
+    const std::vector<u32>& lg = FieldAccess::log(f);
+    const std::vector<u64>& al = FieldAccess::antilog(f);
+    const std::vector<u32>& lo = FieldAccess::low(f);
+    const std::vector<u32>& hi = FieldAccess::high(f);
+    const std::vector<u32>& z = FieldAccess::zech(f);
+    host.insert(host.end(), lg.begin(), lg.end());
+    for (const u64 v : al) host.push_back(static_cast<uint32_t>(v));
+    host.insert(host.end(), lo.begin(), lo.end());
+    host.insert(host.end(), hi.begin(), hi.end());
+    host.insert(host.end(), z.begin(), z.end());
+    c->wide_tabs.ensure(host.size() * 4);
+    check(cudaMemcpy(c->wide_tabs.ptr, host.data(), host.size() * 4, cudaMemcpyHostToDevice), "field tables upload");
+    c->fval.ensure(order * 8);
+    check(cudaMemcpy(c->fval.ptr, FieldAccess::fval(f).data(), order * 8, cudaMemcpyHostToDevice), "fval upload");
+    c->status.ensure(4);
+    check(cudaMemset(c->status.ptr, 0, 4), "status init");
+    settle_uploads();
+    qpk::GfqWideParams& W = c->wp;
+    W.p = static_cast<uint32_t>(p);
+    W.k = k;
+    W.order = static_cast<uint32_t>(order);
+    W.group = static_cast<uint32_t>(order - 1);
+    W.lh_radix = static_cast<uint32_t>(FieldAccess::lh_radix(f));
+    W.qbits = is_pow2(q) ? bit_width_u128(q) - 1 : 0;
+    W.chunk = static_cast<uint32_t>(f.params().n_q);
+    u64 qi = 1;
+    for (u32 i = 0; i < 2 * k - 1; ++i, qi *= q) W.qpow[i] = qi;
+    W.qpow[1] = q;  // also for k = 1 (the DQT pack reads it)
+    W.fval = c->fval.as<double>();
+    const uint32_t* t = c->wide_tabs.as<uint32_t>();
+    W.log = t;
+    W.antilog = t + order;
+    W.low = t + 2 * order;
+    W.high = W.low + lo.size();
+    W.zech = W.high + hi.size();
+    W.status = c->status.as<uint32_t>();
+    // the generic helpers (coefficient records -> reps, rep ops) read these
+    c->elem.p = W.p;
+    c->elem.k = k;
+    c->elem.order = W.order;
+    c->elem.group = W.group;
+    c->elem.log = W.log;
+    return c;
+}
+
 DeviceFieldCache& device_field(const GfqField& f) {
     std::lock_guard<std::mutex> lock(g_mirror_mu);
     auto& slot = FieldAccess::device(f);
@@ -200,8 +254,10 @@ DeviceFieldCache& device_field(const GfqField& f) {
     gpu::require_device();
     const u64 p = f.p();
     const u32 k = f.k();
-    if (p > 255 || k > static_cast<u32>(qpk::kMaxGfqK))
-        throw std::invalid_argument("qpack-b200 GF(p^k): device path needs p < 256 and k <= 4");
+    if (p > 255 || k > static_cast<u32>(qpk::kMaxGfqK)) {
+        slot = build_wide_field(f);
+        return *slot;
+    }
     auto c = std::make_shared<DeviceFieldCache>();
     const u64 lh = FieldAccess::lh_radix(f);
     u64 nlh = 1;
@@ -661,11 +717,23 @@ void polymul_batch(std::span<const std::uint8_t> a, std::span<const std::uint8_t
 }
 
 // ------------------------------------------------------------------ GF(p^k)
+// coefficient records hold one byte per coefficient
+void require_byte_coeffs(const DeviceFieldCache& F) {
+    if (F.elem.p > 255)
+        throw std::invalid_argument("qpack-b200 GF(p^k): coefficient records are bytes (p < 256); p = " +
+                                    std::to_string(F.elem.p) + " takes the rep entry points");
+}
+
 void gfq_mul_device(DeviceFieldCache& F, const uint8_t* a, const uint8_t* b, u64 n, uint8_t* out, int path,
                     cudaStream_t s) {
-    qpk::GfqElemParams E = F.elem;
     if (path < qpk::kGfqPacked || path > qpk::kGfqLinear)
         throw std::invalid_argument("gfq_mul: path must be 0 (packed), 1 (dlog) or 2 (linear)");
+    require_byte_coeffs(F);
+    if (F.wide) {
+        check(qpk::launch_gfq_wide_mul(F.wp, a, b, n, out, path, s), "gfq_mul (rep domain) launch");
+        return;
+    }
+    qpk::GfqElemParams E = F.elem;
     E.mode = path;
     check(qpk::launch_gfq_elem(E, a, b, n, out, s), "gfq_mul launch");
 }
@@ -813,13 +881,26 @@ void gfq_matmul_by_columns(DeviceFieldCache& F, const GfqField& field, const voi
         gfq_gemv_device(F, field, ar, wbt.as<uint32_t>() + j * K, m, K, wct.as<uint32_t>() + j * m, nullptr, s);
     uint32_t* cr = reps ? static_cast<uint32_t*>(C) : wc.as<uint32_t>();
     check(qpk::launch_transpose_u32(wct.as<uint32_t>(), n, m, cr, s), "transpose C");
-    if (!reps)
-        check(qpk::launch_reps_to_coeffs(E.k, E.alog, cr, m * n, static_cast<uint8_t*>(C), s), "reps -> coeffs");
+    if (!reps) {
+        if (F.wide)
+            check(qpk::launch_gfq_wide_reps_to_coeffs(F.wp, cr, m * n, static_cast<uint8_t*>(C), s), "reps -> coeffs");
+        else
+            check(qpk::launch_reps_to_coeffs(E.k, E.alog, cr, m * n, static_cast<uint8_t*>(C), s), "reps -> coeffs");
+    }
 }
 
 void gfq_matmul_device(DeviceFieldCache& F, const GfqField& field, const void* A, const void* B, u64 m, u64 K, u64 n,
                        uint32_t chunk, void* C, bool reps, cudaStream_t s, uint32_t repack) {
     if (m == 0 || n == 0) return;
+    if (!reps) require_byte_coeffs(F);
+    if (F.wide) {
+        // rep-domain GEMVs over B's columns (the fp64 MMA kernels pack at most
+        // four byte coefficients per word)
+        if (repack != qpk::kRepackRedq)
+            throw std::invalid_argument("gfq_matmul: the fold re-pack is provided for GF(3^3) at q = 2^10 only");
+        gfq_matmul_by_columns(F, field, A, B, m, K, n, C, reps, s);
+        return;
+    }
     {
         const u64 p = field.p(), unit = field.k() * (p - 1) * (p - 1), q = field.params().q;
         const u64 safe = unit ? (q - 1 - (p - 1)) / unit : K;
@@ -945,6 +1026,12 @@ CostReport matmul_cost(const GfqField& field, u64 m, u64 K, u64 n) {
 void gfq_gemv_device(DeviceFieldCache& F, const GfqField& field, const uint32_t* A, const uint32_t* x, u64 m, u64 K,
                      uint32_t* y_rep, uint8_t* y_coeff, cudaStream_t s) {
     if (m == 0) return;
+    if (y_coeff) require_byte_coeffs(F);
+    if (F.wide) {
+        StreamBuf ws(qpk::gfq_wide_workspace_bytes(m, K), s);
+        check(qpk::launch_gfq_wide_gemv(F.wp, A, x, m, K, ws.ptr, y_rep, y_coeff, s), "gfq_gemv (rep domain) launch");
+        return;
+    }
     uint32_t splits = qpk::gemv_splits(m, K);
     if (const char* e = std::getenv("QPK_GEMV_SPLITS")) splits = static_cast<uint32_t>(std::max(1, std::atoi(e)));  // dev knob
     // products one lane accumulates: a split is rounded up to 128 elements,

@@ -122,6 +122,32 @@ struct GfqGemvParams {
     uint32_t* status;     // the field's error word: kErrRep for reps >= order (read as zero)
 };
 
+// GF(p^k) outside the byte-packed fast form (k > 4 or p > 255), rep domain
+// throughout (gfq_wide.cu).
+constexpr uint32_t kMaxWideK = 8;  // q^(2k-1) < 2^53 with q > k (p-1)^2 allows k <= 8
+struct GfqWideParams {
+    uint32_t p, k, order, group, lh_radix, qbits;  // qbits: log2 q for q = 2^b, else 0
+    uint32_t chunk;                                // products per lane per REDQ group (n_q)
+    uint64_t qpow[2 * kMaxWideK - 1];              // q^i
+    const double* fval;                            // rep -> q-adic evaluation
+    const uint32_t* log;                           // polynomial index -> rep
+    const uint32_t* antilog;                       // rep -> polynomial index
+    const uint32_t* low;                           // lh^k reps
+    const uint32_t* high;                          // lh^k reps
+    const uint32_t* zech;                          // order reps (plus-one table)
+    uint32_t* status;                              // kErrRep
+};
+// elementwise products of k-byte coefficient records (p < 256); path kGfqDlog
+// or the DQT/REDQ/L-H pipeline (kGfqPacked, kGfqLinear)
+cudaError_t launch_gfq_wide_mul(const GfqWideParams& P, const uint8_t* a, const uint8_t* b, uint64_t n, uint8_t* out,
+                                int path, cudaStream_t s);
+// y = A x on reps; ws: gfq_wide_workspace_bytes
+uint64_t gfq_wide_workspace_bytes(uint64_t m, uint64_t K);
+cudaError_t launch_gfq_wide_gemv(const GfqWideParams& P, const uint32_t* A, const uint32_t* x, uint64_t m, uint64_t K,
+                                 void* ws, uint32_t* out_rep, uint8_t* out_coeff, cudaStream_t s);
+cudaError_t launch_gfq_wide_reps_to_coeffs(const GfqWideParams& P, const uint32_t* reps, uint64_t n, uint8_t* out,
+                                           cudaStream_t s);
+
 // K7: fgdp_dot's data-dependent Zech reads, replayed per gfq_matmul output.
 constexpr uint32_t kMaxCountK = 8;
 struct GfqCountParams {
