@@ -56,11 +56,13 @@ def measured_peaks():
 
 
 def ncu_traffic(kernel_key):
-    """dram bytes per launch of `kernel_key` from the committed ncu summary."""
+    """dram bytes per launch (read + write) of `kernel_key` from the committed
+    ncu summary (profiles/ncu_summary.json: the round-2 captures first)."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
             s = json.load(f)
-        return s[kernel_key]["dram_bytes_per_launch"]
+        entry = s.get("round2", {}).get(kernel_key) or s[kernel_key]
+        return entry["dram_bytes_per_launch"]
     except Exception:
         return None
 
@@ -409,10 +411,10 @@ def measure_configs(Q, torch, dev, peak_hbm):
         return {"value": rate_all, "unit": unit, "cores": threads if use_ref else 1, "one_thread": rate_one,
                 "kind": "reference" if use_ref else "port", "sample": sample}
 
-    def hbm_roof(bytes_per_launch, ms, kernel):
+    def hbm_roof(bytes_per_launch, ms, kernel, ncu_key):
         a = bytes_per_launch / (ms * 1e-3) / 1e9
         return {"bound": "hbm", "achieved": a, "peak": peak_hbm, "unit": "GB/s", "frac": a / peak_hbm,
-                "algorithmic_bytes_per_launch": bytes_per_launch, "kernel": kernel}
+                "traffic": ncu_traffic(ncu_key), "algorithmic_bytes_per_launch": bytes_per_launch, "kernel": kernel}
 
     # ---------------------------------------------------------------- C1
     # 2^20 pairs of degree-<4 polynomials over F_3, q = 2^5: 15 B per pair
@@ -447,7 +449,7 @@ def measure_configs(Q, torch, dev, peak_hbm):
                  "metric": "polymul_pairs_per_s", "unit": "pairs/s", "value": n1 / (ms * 1e-3), "ms": ms,
                  "timing": "CUDA graph of 24 launches over rotating buffer sets (377 MB > L2), per launch",
                  "ms_hot": ms_hot, "ms_single_launch_flushed": ms_single,
-                 "roofline": hbm_roof(15 * n1, ms, "stream_direct_kernel<PolymulOp<4,4,CtConst<3,5>>>"),
+                 "roofline": hbm_roof(15 * n1, ms, "stream_direct_kernel<PolymulOp<4,4,CtConst<3,5>>>", "c1_polymul"),
                  "e2e": {"value": n1 / t_e2e, "unit": "pairs/s", "h2d_bytes_per_step": 8 * n1,
                          "d2h_bytes_per_step": 7 * n1, "path": "qpk_polymul_batch_host (pinned host buffers)"},
                  "cpu_baseline": cpu}
@@ -487,7 +489,8 @@ def measure_configs(Q, torch, dev, peak_hbm):
                      "metric": "gf_products_per_s", "unit": "products/s", "value": n3 / (ms * 1e-3), "ms": ms,
                      "timing": "CUDA graph of 12 launches over 3 rotating buffer sets (453 MB > L2), per launch",
                      "ms_single_launch_flushed": single,
-                     "roofline": hbm_roof(9 * n3, ms, f"stream_tma_kernel<GfqElemOp<3,CtConst<7,8>,{path}>>"),
+                     "roofline": hbm_roof(9 * n3, ms, f"stream_tma_kernel<GfqElemOp<3,CtConst<7,8>,{path}>>",
+                                          {0: "c3_redq", 1: "c3_dlog", 2: "c3_linear"}[path]),
                      "e2e": {"value": n3 / t_e2e, "unit": "products/s", "h2d_bytes_per_step": 6 * n3,
                              "d2h_bytes_per_step": 3 * n3,
                              "path": f"qpk_gfq_mul_batch_host path {path} (pinned host buffers)"},
@@ -544,6 +547,7 @@ def measure_configs(Q, torch, dev, peak_hbm):
                      "metric": "gf_ops_per_s", "unit": "GF ops/s", "value": 2 * nn ** 3 / (ms * 1e-3), "ms": ms,
                      "roofline": {"bound": "tensor", "achieved": tf, "peak": fp64_peak, "unit": "TFLOP/s",
                                   "frac": tf / fp64_peak, "peak_source": "fp64 DMMA probe (this run)",
+                                  "traffic": ncu_traffic(f"matmul_c{cfg.cid}"),
                                   "frac_of_nominal_37": tf / 37.0, "kernel": "gfq_matmul_kernel (DMMA) + K1 pack"},
                      "e2e": e2e, "cpu_baseline": cpu, "repack": "redq"}
         if cfg.cid == 5:

@@ -158,7 +158,10 @@ __device__ __forceinline__ double pack_word(const C& c, double qd, const uint32_
         uint64_t v = 0;
 #pragma unroll
         for (int i = K_ - 1; i >= 0; --i) v = (v << c.qbits()) | cf[i];
-        return static_cast<double>(v);
+        // exact as a double below 2^52: a magic add instead of an I2F.F64
+        // conversion (quarter-rate pipe)
+        if constexpr (C::kSafe) return __longlong_as_double(static_cast<long long>(v | 0x4330000000000000ull)) - kTwo52;
+        else return static_cast<double>(v);
     } else {
         double v = 0.0;
 #pragma unroll
@@ -211,11 +214,23 @@ struct PolymulOp {
         const K c{P.rq};
         const double qd = static_cast<double>(P.rq.q);
         uint64_t rec[R];
+        // one range check for the whole run (bytes >= p are reduced mod p,
+        // DensePoly, record by record on the slow path)
+        bool clean = false;
+        if constexpr (K::kSafe) {
+            if constexpr ((R * K_) % 4 == 0 && K::kP < 128)
+                clean = all_bytes_below<R * K_ / 4>(a, c.p()) && all_bytes_below<R * K_ / 4>(b, c.p());
+        }
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             uint32_t ca[K_], cb[K_];
-            record_coeffs<K_>(c, P.rq.mod_magic, a, r, ca);
-            record_coeffs<K_>(c, P.rq.mod_magic, b, r, cb);
+            if (clean) {
+#pragma unroll
+                for (int i = 0; i < K_; ++i) ca[i] = run_byte(a, r * K_ + i), cb[i] = run_byte(b, r * K_ + i);
+            } else {
+                record_coeffs<K_>(c, P.rq.mod_magic, a, r, ca);
+                record_coeffs<K_>(c, P.rq.mod_magic, b, r, cb);
+            }
             // exact: q^(2k-1) < 2^53 (validated)
             rec[r] = redq_record<ND, W>(c, pack_word<K_>(c, qd, ca) * pack_word<K_>(c, qd, cb), tab);
         }
@@ -455,7 +470,10 @@ struct GfqElemOp {
 #ifndef QPK_GFE_DS
 #define QPK_GFE_DS 1
 #endif
-    static constexpr bool kDirectStore = kLanePriv && QPK_GFE_DS;
+#ifndef QPK_GFE_LIN_DS
+#define QPK_GFE_LIN_DS 0
+#endif
+    static constexpr bool kDirectStore = (kLanePriv && QPK_GFE_DS) || (kFast && MODE == kGfqLinear && QPK_GFE_LIN_DS);
     GfqElemParams P;
     __host__ __device__ bool fast() const { return kFast && P.fast_off != 0; }
     __host__ __device__ __forceinline__ int mode() const {
