@@ -217,6 +217,73 @@ def cpu_baseline_leg():
                       "one_thread: 2^22 words on 1 thread"}
 
 
+def cpu_legs():
+    """Every config's reference CPU path (oracle/_ref: the unmodified
+    sources) on the host cores, in a process of its own -- CUDA and torch
+    initialised in the same process measured the same reference call 1.6x
+    slower (scripts/cpu_leg_probe.py) -- with the reference arm's protocol:
+    warm-up, mean over calls, outputs preallocated, all threads and one
+    thread.  Inputs: the configs' seeded streams regenerated on the host."""
+    import numpy as np
+
+    import oracle as O
+    th = host_threads()
+    out = {"C2": cpu_baseline_leg()}
+    if O.ref() is None:
+        return out
+    model = cpu_model()
+
+    def entry(rate_all, rate_one, unit, sample):
+        return {"value": rate_all, "unit": unit, "cores": th, "one_thread": rate_one, "kind": "reference",
+                "cpu_model": model, "sample": sample}
+
+    # C1: fqt_mul per pair (the whole 2^20-pair workload per call)
+    n1 = 1 << 20
+    d = O.draws(0x07100510 + 1, 8 * n1, 3).reshape(n1, 8)
+    a, b = np.ascontiguousarray(d[:, :4]), np.ascontiguousarray(d[:, 4:])
+    o = np.empty((n1, 7), np.uint8)
+    rate = lambda t, n: n / time_cpu(lambda: O.ref_polymul_batch(3, 3, a[:n], b[:n], algo=0, threads=t,
+                                                                 out=o[:n])[1] * 1e-9, 3, 1)
+    out["C1"] = entry(rate(th, n1), rate(1, 1 << 18), "pairs/s",
+                      f"the full {n1}-pair C1 workload per call (fqt_mul per pair, qadic_for_degree(3,3,53)); "
+                      "mean of 3 after 1 warm-up; one_thread: 2^18 pairs")
+    # C3: 2^22 products of the stream per call, both reference paths
+    nc = 1 << 22
+    d = O.draws(0x07100510 + 3, 6 * nc, 7).reshape(nc, 6)
+    a, b = np.ascontiguousarray(d[:, :3]), np.ascontiguousarray(d[:, 3:])
+    o = np.empty((nc, 3), np.uint8)
+    rf = O.RefField(7, 3, 256)
+    for name, algo, what in (("C3_redq", 0, "fgdp_dot on length-1 vectors"), ("C3_dlog", 1, "GfqField::mul"),
+                             ("C3_linear", 0, "fgdp_dot on length-1 vectors")):
+        rate = lambda t, n, al=algo: n / time_cpu(lambda: rf.mul_batch(a[:n], b[:n], algo=al, threads=t,
+                                                                      out=o[:n])[1] * 1e-9, 3, 1)
+        out[name] = entry(rate(th, nc), rate(1, 1 << 20), "products/s",
+                          f"2^22 products of the C3 stream per call ({what}); mean of 3 after 1 warm-up; "
+                          "one_thread: 2^20 products")
+    # C4 / C5: gfq_matmul (as shipped) on a row slab, rate extrapolated
+    for cid, k, q, nn in ((4, 2, 1 << 16, 4096), (5, 3, 1 << 10, 8192)):
+        rows = max(16, th)
+        A = O.draws(0x07100510 + cid, rows * nn * k, 3).reshape(rows, nn, k)
+        B = O.draws(0x07100510 + cid, nn * nn * k, 3, start=nn * nn * k).reshape(nn, nn, k)
+        rfm = O.RefField(3, k, q)
+        cb = np.empty((rows, nn, k), np.uint8)
+        rate = lambda t, r: 2 * r * nn * nn / time_cpu(
+            lambda: rfm.matmul(A[:r], B, 0, r, algo=0, threads=t, out=cb[:r])[1] * 1e-9, 1, 0)
+        out[f"C{cid}"] = entry(rate(th, rows), rate(1, 2), "GF ops/s",
+                               f"{rows} rows x {nn} x {nn} of C{cid} per call (gfq_matmul as shipped, row slabs over "
+                               "threads), rate extrapolated; one_thread: 2 rows")
+    return out
+
+
+def cpu_legs_subprocess():
+    r = subprocess.run([sys.executable, os.path.abspath(__file__), "--cpu-legs"], capture_output=True, text=True,
+                       timeout=1800)
+    lines = [x for x in r.stdout.splitlines() if x.startswith("{")]
+    if r.returncode != 0 or not lines:
+        raise RuntimeError("cpu legs failed: " + r.stderr[-2000:])
+    return json.loads(lines[-1])
+
+
 # ---------------------------------------------------------------------- ours
 def run_ours(args, rank, world, local_rank):
     import numpy as np
@@ -346,8 +413,6 @@ def measure_configs(Q, torch, dev, peak_hbm):
 
     import oracle as O
     res = {}
-    threads = host_threads()
-    use_ref = O.ref() is not None
     fp64_peak = Q.probe_fp64(1, 8192)
     dfma_peak = Q.probe_fp64(0, 8192)
     res["fp64_peaks_tflops"] = {"dmma_probe": fp64_peak, "dfma_probe": dfma_peak, "nominal": 37.0,
@@ -407,10 +472,6 @@ def measure_configs(Q, torch, dev, peak_hbm):
     def pinned(shape, dtype):
         return torch.empty(shape, dtype=dtype, pin_memory=True).numpy()
 
-    def cpu_entry(rate_all, rate_one, unit, sample):
-        return {"value": rate_all, "unit": unit, "cores": threads if use_ref else 1, "one_thread": rate_one,
-                "kind": "reference" if use_ref else "port", "sample": sample}
-
     def hbm_roof(bytes_per_launch, ms, kernel, ncu_key):
         a = bytes_per_launch / (ms * 1e-3) / 1e9
         return {"bound": "hbm", "achieved": a, "peak": peak_hbm, "unit": "GB/s", "frac": a / peak_hbm,
@@ -437,14 +498,7 @@ def measure_configs(Q, torch, dev, peak_hbm):
     t_e2e = time_host(lambda: pm(ha, hb, out=ho), steps=20)
     assert np.array_equal(ho, sets1[0][2].cpu().numpy()), "C1 e2e output differs from the device output"
     del sets1
-    cpu = None
-    if use_ref:
-        out = np.empty((n1, 7), np.uint8)
-        rate = lambda th, n: n / time_cpu(lambda: O.ref_polymul_batch(3, 3, ha[:n], hb[:n], algo=0, threads=th,
-                                                                      out=out[:n])[1] * 1e-9, 3, 1)
-        cpu = cpu_entry(rate(threads, n1), rate(1, 1 << 18), "pairs/s",
-                        f"the full {n1}-pair C1 workload per call (fqt_mul per pair, qadic_for_degree(3,3,53)); "
-                        "mean of 3 after 1 warm-up; one_thread: 2^18 pairs")
+    cpu = None  # filled from the fresh-process CPU legs (cpu_legs)
     res["C1"] = {"workload": "C1 F_3 polymul: 2^20 pairs of degree-<4 polys, q=2^5 -> 7 residues/pair",
                  "metric": "polymul_pairs_per_s", "unit": "pairs/s", "value": n1 / (ms * 1e-3), "ms": ms,
                  "timing": "CUDA graph of 24 launches over rotating buffer sets (377 MB > L2), per launch",
@@ -467,9 +521,6 @@ def measure_configs(Q, torch, dev, peak_hbm):
     ha, hb, ho = pinned((n3, 3), torch.uint8), pinned((n3, 3), torch.uint8), pinned((n3, 3), torch.uint8)
     ha[:] = sets3[0][0].view(n3, 3).cpu().numpy()
     hb[:] = sets3[0][1].view(n3, 3).cpu().numpy()
-    rf = O.RefField(7, 3, 256) if use_ref else None
-    nc = 1 << 22
-    oc = np.empty((nc, 3), np.uint8)
     for path, name, what, algo in ((0, "C3_redq", "DQT pack, fp64 product, REDQ, L/H tables (fgdp_dot on length-1 "
                                                   "vectors)", 0),
                                    (1, "C3_dlog", "dlog/Zech (GfqField::mul)", 1),
@@ -479,12 +530,6 @@ def measure_configs(Q, torch, dev, peak_hbm):
         t_e2e = time_host(lambda pth=path: f3.mul_batch(ha, hb, pth, out=ho))
         assert np.array_equal(ho, sets3[0][2].cpu().numpy()), f"{name} e2e output differs from the device output"
         cpu = None
-        if use_ref:
-            rate = lambda th, n, al=algo: n / time_cpu(
-                lambda: rf.mul_batch(ha[:n], hb[:n], algo=al, threads=th, out=oc[:n])[1] * 1e-9, 3, 1)
-            cpu = cpu_entry(rate(threads, nc), rate(1, 1 << 20), "products/s",
-                            f"2^22 products of the C3 stream per call ({'fgdp_dot on length-1 vectors' if algo == 0 else 'GfqField::mul'}"
-                            "); mean of 3 after 1 warm-up; one_thread: 2^20 products")
         res[name] = {"workload": f"C3 GF(7^3) elementwise: 2^24 products, q=2^8, path {path}: {what}",
                      "metric": "gf_products_per_s", "unit": "products/s", "value": n3 / (ms * 1e-3), "ms": ms,
                      "timing": "CUDA graph of 12 launches over 3 rotating buffer sets (453 MB > L2), per launch",
@@ -532,15 +577,6 @@ def measure_configs(Q, torch, dev, peak_hbm):
                            "path": "qpk_gfq_matmul_rep_host = gfq_matmul(GfqMatrix, GfqMatrix, GfqField) (reps; "
                                    "the reference's chunk n_q)"}}
         cpu = None
-        if use_ref:
-            rows = max(16, threads)
-            rf = O.RefField(3, k, cfg.q)
-            cb = np.empty((rows, nn, k), np.uint8)
-            rate = lambda th, r: 2 * r * nn * nn / time_cpu(
-                lambda: rf.matmul(hA[:r], hB, 0, r, algo=0, threads=th, out=cb[:r])[1] * 1e-9, 1, 0)
-            cpu = cpu_entry(rate(threads, rows), rate(1, 2), "GF ops/s",
-                            f"{rows} rows x {nn} x {nn} of C{cfg.cid} per call (gfq_matmul as shipped, row slabs over "
-                            "threads), rate extrapolated; one_thread: 2 rows")
         name = f"C{cfg.cid}"
         res[name] = {"workload": f"C{cfg.cid} GF(3^{k}) matmul {nn}^3, q=2^{cfg.q.bit_length() - 1}"
                                  + (f", delayed REDQ re-pack every {cfg.chunk}" if cfg.chunk else ""),
@@ -648,7 +684,11 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-legs", action="store_true", help=argparse.SUPPRESS)  # internal: fresh-process CPU legs
     args = ap.parse_args()
+    if args.cpu_legs:
+        print(json.dumps(cpu_legs()))
+        return
     args.warmup = max(args.warmup, 3)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -668,9 +708,11 @@ def main():
     line = run_ours(args, rank, world, local_rank)
     if rank == 0:
         if world == 1 and not args.no_cpu_baseline:
-            line["cpu_baseline"] = cpu_baseline_leg()
-            if "configs" in line:
-                line["configs"]["C2"]["cpu_baseline"] = line["cpu_baseline"]
+            legs = cpu_legs_subprocess()
+            line["cpu_baseline"] = legs["C2"]
+            for name, leg in legs.items():
+                if name in line.get("configs", {}):
+                    line["configs"][name]["cpu_baseline"] = leg
         if "configs" in line:
             line["summary"] = summary(line)  # last key: survives a truncated stdout tail
         print(json.dumps(line))
