@@ -4,6 +4,7 @@ import os
 import socket
 
 import numpy as np
+import pytest
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
@@ -53,3 +54,30 @@ def test_two_ranks_gloo(tmp_path, orc):
         w = w * np.uint64(128) + dr[:, j]
     assert (got == orc.redq_f64(5, 128, 6, w.astype(np.float64), float_mode=True, window=4)).all()
     assert all(float(np.load(tmp_path / f"max{r}.npy")[0]) == 3.0 for r in range(world))
+
+
+@pytest.mark.gpu
+def test_rank_shards_on_the_device_tile_the_stream(qpk, orc, torch_cuda):
+    """The per-rank work of bench.py's multi-GPU path on the product itself:
+    each rank of a world of 4 generates its shard of the seeded C2 stream on
+    the device (gen_words at the rank's first word) and reduces it with the
+    library's REDQ kernel; concatenated, the shards equal the single-process
+    stream's residues (the ranks run one after another on this GPU: they
+    never wait on one another, and the only collectives of the real run are
+    the timing barrier and the max-over-ranks of the elapsed time)."""
+    torch = torch_cuda
+    world, n = 4, 70001
+    plan = qpk.RedqPlan(5, 128, 6, qpk.FLOAT_PREMUL).attach_correction(4)
+    parts = []
+    for rank in range(world):
+        first, count = weak_shard(rank, n)
+        w = torch.empty(count, dtype=torch.float64, device="cuda")
+        qpk.gen_words(qpk.C2.seed, count, 128, 6, w, first=first)
+        parts.append(plan.residues(w).cpu().numpy())
+    plan.sync()
+    got = np.concatenate(parts)
+    dr = orc.draws(qpk.C2.seed, world * n * 7, 128).reshape(world * n, 7).astype(np.uint64)
+    w = np.zeros(world * n, np.uint64)
+    for j in range(7):
+        w = w * np.uint64(128) + dr[:, j]
+    assert (got == orc.redq_f64(5, 128, 6, w.astype(np.float64), float_mode=True, window=4)).all()
