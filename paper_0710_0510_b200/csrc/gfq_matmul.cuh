@@ -62,10 +62,6 @@ __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double
                  : "d"(a), "d"(b));
 }
 
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
-}
-
 // REDQ + re-pack: the word whose digit i is (digit i of r) mod p, as an
 // exact double (digits mu_i via the direct correction, then assembled)
 template <int ND, class K>

@@ -53,9 +53,11 @@ struct PolymulParams {
 // q = 2^8 (BASELINE config 3).  Its dlog path reads the antilog table from
 // kDlogCopies interleaved copies (entry e, copy c at word e*kDlogCopies + c;
 // lane l reads copy l mod kDlogCopies, so only the 32/kDlogCopies lanes of
-// one copy share its banks).
+// one copy share its banks).  16 copies (44 KB, two lanes per copy) with the
+// producer-warp pipeline measured 27.0-27.2 us for C3 dlog against 27.6-27.8
+// with 8 (scripts/c3_sweep.py, round 2).
 #ifndef QPK_DLOG_COPIES
-#define QPK_DLOG_COPIES 8
+#define QPK_DLOG_COPIES 16
 #endif
 constexpr uint32_t kDlogCopies = QPK_DLOG_COPIES;
 constexpr bool gfq_fast_field(uint64_t p, uint32_t k, uint64_t q) { return p == 7 && k == 3 && q == 256; }

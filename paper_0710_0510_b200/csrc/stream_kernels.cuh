@@ -415,33 +415,35 @@ __device__ __forceinline__ uint32_t dlog_product(const C&, uint32_t ia, uint32_t
 #endif
 // MODE: kGfqPacked / kGfqDlog / kGfqLinear as a compile-time choice (fast
 // paths), -1 = P.mode
-// ... and of the fast field's REDQ/L-H (PK) and dlog (DL) paths: 66 KB of
-// lane-private tables, outputs stored straight from registers (kDirectStore),
-// 16-record runs x 2 stages keep two CTAs per SM.  Measured (C3, 2^24
-// products, scripts/c3_sweep.py): bulk-stored output tiles 34.2 / 29.4 us
-// (PK / DL, 8-record runs x 2 stages); direct stores 32.4 / 27.2 us, x 3
-// stages 32.4 / 25.1, 16-record runs x 2 stages 31.2 / 24.6 us; one CTA of
-// 512 or 1024 threads per SM and 4-record runs measured slower.
+// ... and of the fast field's REDQ/L-H (PK) and dlog (DL) paths: 66 / 88 KB
+// of lane-private tables, outputs stored straight from registers (kDirectStore),
+// one CTA of 512 consumer threads (+ the producer warp) per SM, 8-record
+// runs x 4 stages.  Measured over rotating buffers larger than L2 (C3, 2^24
+// products, scripts/c3_sweep.py, PK / DL): two CTAs of 256 threads, 16-record
+// runs x 2 stages, CTA-barrier pipeline 31.3 / 28.1 us; with the producer
+// warp 30.7 / 28.1; one CTA of 512, 8-record runs x 4 stages 29.8 / 27.0
+// (16 antilog copies); x 5-6 stages, 4-record runs x 8 stages, 16-record
+// runs x 2 stages and 768 threads all measured slower.
 #ifndef QPK_GFE_PK_RR
 #define QPK_GFE_PK_RR 1
 #endif
 #ifndef QPK_GFE_PK_R
-#define QPK_GFE_PK_R 16
+#define QPK_GFE_PK_R 8
 #endif
 #ifndef QPK_GFE_PK_S
-#define QPK_GFE_PK_S 2
+#define QPK_GFE_PK_S 4
 #endif
 #ifndef QPK_GFE_PK_T
-#define QPK_GFE_PK_T 256
+#define QPK_GFE_PK_T 512
 #endif
 #ifndef QPK_GFE_DL_R
-#define QPK_GFE_DL_R 16
+#define QPK_GFE_DL_R 8
 #endif
 #ifndef QPK_GFE_DL_S
-#define QPK_GFE_DL_S 2
+#define QPK_GFE_DL_S 4
 #endif
 #ifndef QPK_GFE_DL_T
-#define QPK_GFE_DL_T 256
+#define QPK_GFE_DL_T 512
 #endif
 template <int K_, class K, int MODE = -1>
 struct GfqElemOp {
@@ -457,8 +459,8 @@ struct GfqElemOp {
         else return 0u;
     }();
     static constexpr uint32_t kP3 = kP * kP * kP;
-    // its REDQ/L-H and dlog paths stage 66 KB of tables (32 lane-private
-    // copies, kernels.hpp fast_off): smaller tiles keep two CTAs per SM
+    // its REDQ/L-H and dlog paths stage 66 / 88 KB of tables (lane-private
+    // copies, kernels.hpp fast_off) beside 4 input stages of 24 KB
     static constexpr bool kLanePriv = kFast && (MODE == kGfqPacked || MODE == kGfqDlog);
     static constexpr int RR = kLanePriv ? QPK_GFE_PK_RR : QPK_GFE_RR;
     static constexpr int S = kFastDlog ? QPK_GFE_DL_S : kLanePriv ? QPK_GFE_PK_S : QPK_GFE_S;
@@ -676,18 +678,28 @@ struct op_direct_store : std::false_type {};
 template <class Op>
 struct op_direct_store<Op, std::enable_if_t<Op::kDirectStore>> : std::true_type {};
 
+#ifndef QPK_DS_PRODUCER
+#define QPK_DS_PRODUCER 1
+#endif
+
 template <class Op>
 struct Geometry {
     static constexpr int R = Op::R, RR = Op::RR, S = Op::S;
     static constexpr int THREADS = op_threads<Op>::value;
     static constexpr bool DS = op_direct_store<Op>::value;
+    // direct-store ops with a producer warp: one extra warp keeps the input
+    // stages in flight, released per consumer warp through "empty"
+    // mbarriers, so the consumer warps never meet at a CTA barrier
+    static constexpr bool WS = DS && QPK_DS_PRODUCER;
+    static constexpr int BLOCK = THREADS + (WS ? 32 : 0);  // launched threads
     static constexpr int TILE = THREADS * R * RR;  // records per tile
     static constexpr uint32_t B0 = Op::IN0 * TILE, B1 = Op::IN1 * TILE, BO = Op::OUT * TILE;
     static constexpr int W0 = R * Op::IN0 / 4, W1 = R * Op::IN1 / 4, WO = R * Op::OUT / 4;
     static_assert((R * Op::IN0) % 4 == 0 && (R * Op::IN1) % 4 == 0 && (R * Op::OUT) % 4 == 0, "u32 runs");
     static_assert(B0 % 16 == 0 && B1 % 16 == 0 && BO % 16 == 0, "bulk copies move multiples of 16 bytes");
-    // stage buffers | output double buffer | S mbarriers | (16-aligned) tables
-    static constexpr size_t tab_off = (size_t(S) * (B0 + B1) + (DS ? 0 : 2 * size_t(BO)) + S * 8 + 15) / 16 * 16;
+    // stage buffers | output double buffer | S (2S with WS) mbarriers | (16-aligned) tables
+    static constexpr size_t tab_off =
+        (size_t(S) * (B0 + B1) + (DS ? 0 : 2 * size_t(BO)) + (WS ? 2 : 1) * S * 8 + 15) / 16 * 16;
     static constexpr size_t smem_pipe = tab_off;
 };
 
@@ -770,7 +782,7 @@ __device__ __forceinline__ void stage_op_tables(const Op& op, uint32_t* dst) {
 }
 
 template <class Op>
-__global__ void __launch_bounds__(op_threads<Op>::value) stream_tma_kernel(const Op op, const uint8_t* __restrict__ in0,
+__global__ void __launch_bounds__(Geometry<Op>::BLOCK) stream_tma_kernel(const Op op, const uint8_t* __restrict__ in0,
                                                               const uint8_t* __restrict__ in1,
                                                               uint8_t* __restrict__ out, uint64_t n_tiles,
                                                               uint32_t* status) {
@@ -798,6 +810,8 @@ __global__ void __launch_bounds__(op_threads<Op>::value) stream_tma_kernel(const
     // copies complete
     if (tid == 0) {
         for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
+        if constexpr (G::WS)
+            for (int s = 0; s < S; ++s) mbar_init(&bars[S + s], G::THREADS / 32);
         fence_mbar_init();
         policy = policy_evict_first();
     }
@@ -821,6 +835,40 @@ __global__ void __launch_bounds__(op_threads<Op>::value) stream_tma_kernel(const
 
     uint32_t err = 0;
     uint32_t it = 0;
+    if constexpr (G::WS) {
+        const int warp = tid >> 5, lane = tid & 31;
+        if (warp == G::THREADS / 32) {
+            // producer: refill stage s once every consumer warp released it
+            if (lane == 0) {
+                policy = policy_evict_first();
+                for (uint64_t tile = blockIdx.x + uint64_t(S) * gridDim.x; tile < n_tiles; tile += gridDim.x, ++it) {
+                    const int s = it % S;
+                    mbar_wait(&bars[S + s], (it / S) & 1);
+                    issue(s, tile);
+                }
+            }
+            return;
+        }
+        for (uint64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++it) {
+            const int s = it % S;
+            const uint8_t* src = s_in + size_t(s) * (G::B0 + G::B1);
+            mbar_wait(&bars[s], (it / S) & 1);
+#pragma unroll
+            for (int rr = 0; rr < G::RR; ++rr) {
+                const int run = rr * G::THREADS + tid;
+                uint32_t a[G::W0 > 0 ? G::W0 : 1], b[G::W1 > 0 ? G::W1 : 1];
+                lds_run<G::W0>(src + run * (G::R * Op::IN0), a);
+                lds_run<G::W1>(src + G::B0 + run * (G::R * Op::IN1), b);
+                uint32_t ow[G::WO];
+                op.apply(a, b, ow, tab, err);
+                stg_run<G::WO>(out + tile * G::BO + size_t(run) * (G::R * Op::OUT), ow);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bars[S + s]);
+        }
+        report(err, status);
+        return;
+    }
     for (uint64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++it) {
         const int s = it % S;
         const uint8_t* src = s_in + size_t(s) * (G::B0 + G::B1);
@@ -1023,14 +1071,14 @@ cudaError_t run_stream(const Op& op, const uint8_t* in0, const uint8_t* in1, uin
         cudaGetDevice(&dev);
         if (occ_smem != smem || occ_dev != dev) {
             int v = 0;
-            cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, stream_tma_kernel<Op>, G::THREADS, smem);
+            cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, stream_tma_kernel<Op>, G::BLOCK, smem);
             if (e != cudaSuccess) return e;
             occ_smem = smem;
             occ_dev = dev;
             occ_per_sm = std::max(v, 1);
         }
         const uint64_t grid = std::min<uint64_t>(n_tiles, uint64_t(sms) * occ_per_sm);
-        const cudaError_t e = launch_pdl(stream_tma_kernel<Op>, dim3(static_cast<unsigned>(grid)), dim3(G::THREADS),
+        const cudaError_t e = launch_pdl(stream_tma_kernel<Op>, dim3(static_cast<unsigned>(grid)), dim3(G::BLOCK),
                                          smem, s, op, in0, in1, out, n_tiles, status);
         if (e != cudaSuccess) return e;
     }
