@@ -143,12 +143,15 @@ __device__ __forceinline__ uint32_t byte_of(uint32_t w, int i) { return (w >> (8
 // before pdl_wait (barrier setup, constant plan tables uploaded before the
 // predecessor ran) overlap the previous kernel's tail.  A PDL kernel touches
 // no data buffer before pdl_wait.  No kernel triggers its dependents early
-// (griddepcontrol.launch_dependents): measured, the early
+// (griddepcontrol.launch_dependents) except the producer-warp stream
+// pipeline at its CTAs' last tile (stream_kernels.cuh, one CTA per SM whose
+// shared memory leaves no room for a waiting dependent): measured, an early
 // trigger cost C2 0.1588 -> 0.1604 ms per step, C1 6.8 -> 7.3 us and K5
 // 48.0 -> 50.2 us -- the dependents' waiting CTAs take SM slots (and
 // launch work) while the primary still runs; the implicit trigger at exit
 // keeps the overlap without that.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 // host: launch with programmatic stream serialization (the kernel's prologue
 // overlaps the previous kernel's tail; its data accesses follow pdl_wait)

@@ -681,6 +681,12 @@ struct op_direct_store<Op, std::enable_if_t<Op::kDirectStore>> : std::true_type 
 #ifndef QPK_DS_PRODUCER
 #define QPK_DS_PRODUCER 1
 #endif
+// measured C3 REDQ/L-H 29.7 -> 28.4 us, dlog 27.0 -> 26.6; the same trigger
+// in the bulk-store pipeline left C3 linear unchanged and cost C2 2%
+#ifndef QPK_WS_TRIGGER
+#define QPK_WS_TRIGGER 1
+#endif
+
 
 template <class Op>
 struct Geometry {
@@ -852,6 +858,12 @@ __global__ void __launch_bounds__(Geometry<Op>::BLOCK) stream_tma_kernel(const O
         for (uint64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++it) {
             const int s = it % S;
             const uint8_t* src = s_in + size_t(s) * (G::B0 + G::B1);
+#if QPK_WS_TRIGGER
+            // the CTA's last tile: the next kernel may launch (its CTAs land
+            // on the SMs this grid leaves and stage their tables during its
+            // tail; their data accesses still follow pdl_wait)
+            if (tile + gridDim.x >= n_tiles) pdl_trigger();
+#endif
             mbar_wait(&bars[s], (it / S) & 1);
 #pragma unroll
             for (int rr = 0; rr < G::RR; ++rr) {
@@ -867,61 +879,61 @@ __global__ void __launch_bounds__(Geometry<Op>::BLOCK) stream_tma_kernel(const O
             if (lane == 0) mbar_arrive(&bars[S + s]);
         }
         report(err, status);
-        return;
-    }
-    for (uint64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++it) {
-        const int s = it % S;
-        const uint8_t* src = s_in + size_t(s) * (G::B0 + G::B1);
-        if constexpr (G::DS) {
-            // every thread waits on the stage's mbarrier (the TMA writes are
-            // visible to it); one barrier per tile frees the stage
+    } else {
+        for (uint64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++it) {
+            const int s = it % S;
+            const uint8_t* src = s_in + size_t(s) * (G::B0 + G::B1);
+            if constexpr (G::DS) {
+                // every thread waits on the stage's mbarrier (the TMA writes are
+                // visible to it); one barrier per tile frees the stage
+                mbar_wait(&bars[s], (it / S) & 1);
+#pragma unroll
+                for (int rr = 0; rr < G::RR; ++rr) {
+                    const int run = rr * G::THREADS + tid;
+                    uint32_t a[G::W0 > 0 ? G::W0 : 1], b[G::W1 > 0 ? G::W1 : 1];
+                    lds_run<G::W0>(src + run * (G::R * Op::IN0), a);
+                    lds_run<G::W1>(src + G::B0 + run * (G::R * Op::IN1), b);
+                    uint32_t ow[G::WO];
+                    op.apply(a, b, ow, tab, err);
+                    stg_run<G::WO>(out + tile * G::BO + size_t(run) * (G::R * Op::OUT), ow);
+                }
+                __syncthreads();
+                if (tid == 0) {
+                    const uint64_t next = tile + uint64_t(S) * gridDim.x;
+                    if (next < n_tiles) issue(s, next);
+                }
+                continue;
+            }
+            const int os = it & 1;
+            if (tid == 0) bulk_wait_read<1>();  // output buffer `os` (two tiles ago) drained
             mbar_wait(&bars[s], (it / S) & 1);
+            __syncthreads();
+
+            uint32_t* obuf = reinterpret_cast<uint32_t*>(s_out + size_t(os) * G::BO);
 #pragma unroll
             for (int rr = 0; rr < G::RR; ++rr) {
-                const int run = rr * G::THREADS + tid;
+                const int run = rr * G::THREADS + tid;  // R consecutive records
                 uint32_t a[G::W0 > 0 ? G::W0 : 1], b[G::W1 > 0 ? G::W1 : 1];
                 lds_run<G::W0>(src + run * (G::R * Op::IN0), a);
                 lds_run<G::W1>(src + G::B0 + run * (G::R * Op::IN1), b);
                 uint32_t ow[G::WO];
                 op.apply(a, b, ow, tab, err);
-                stg_run<G::WO>(out + tile * G::BO + size_t(run) * (G::R * Op::OUT), ow);
+#pragma unroll
+                for (int i = 0; i < G::WO; ++i) obuf[run * G::WO + i] = ow[i];
             }
+            fence_proxy_async_smem();
             __syncthreads();
+
             if (tid == 0) {
+                bulk_s2g(out + tile * G::BO, s_out + size_t(os) * G::BO, G::BO);
+                bulk_commit();
                 const uint64_t next = tile + uint64_t(S) * gridDim.x;
                 if (next < n_tiles) issue(s, next);
             }
-            continue;
         }
-        const int os = it & 1;
-        if (tid == 0) bulk_wait_read<1>();  // output buffer `os` (two tiles ago) drained
-        mbar_wait(&bars[s], (it / S) & 1);
-        __syncthreads();
-
-        uint32_t* obuf = reinterpret_cast<uint32_t*>(s_out + size_t(os) * G::BO);
-#pragma unroll
-        for (int rr = 0; rr < G::RR; ++rr) {
-            const int run = rr * G::THREADS + tid;  // R consecutive records
-            uint32_t a[G::W0 > 0 ? G::W0 : 1], b[G::W1 > 0 ? G::W1 : 1];
-            lds_run<G::W0>(src + run * (G::R * Op::IN0), a);
-            lds_run<G::W1>(src + G::B0 + run * (G::R * Op::IN1), b);
-            uint32_t ow[G::WO];
-            op.apply(a, b, ow, tab, err);
-#pragma unroll
-            for (int i = 0; i < G::WO; ++i) obuf[run * G::WO + i] = ow[i];
-        }
-        fence_proxy_async_smem();
-        __syncthreads();
-
-        if (tid == 0) {
-            bulk_s2g(out + tile * G::BO, s_out + size_t(os) * G::BO, G::BO);
-            bulk_commit();
-            const uint64_t next = tile + uint64_t(S) * gridDim.x;
-            if (next < n_tiles) issue(s, next);
-        }
+        if (tid == 0) bulk_wait_all<0>();
+        report(err, status);
     }
-    if (tid == 0) bulk_wait_all<0>();
-    report(err, status);
 }
 
 // Small batches (one wave of CTAs): every thread loads its runs straight
