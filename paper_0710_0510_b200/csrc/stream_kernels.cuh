@@ -445,6 +445,21 @@ __device__ __forceinline__ uint32_t dlog_product(const C&, uint32_t ia, uint32_t
 #ifndef QPK_GFE_DL_T
 #define QPK_GFE_DL_T 512
 #endif
+// the fast field's linear path (no tables): measured (c3_sweep) 26.5 us with
+// the generic geometry; direct stores + producer warp at 512 x 8 x 6 stages
+// 26.7-27.2, 256 x 16 x 4 28.7-29.1, bulk stores at 256 x 8 x 2 x 4 34.5
+#ifndef QPK_GFE_LN_R
+#define QPK_GFE_LN_R QPK_GFE_R
+#endif
+#ifndef QPK_GFE_LN_RR
+#define QPK_GFE_LN_RR QPK_GFE_RR
+#endif
+#ifndef QPK_GFE_LN_S
+#define QPK_GFE_LN_S QPK_GFE_S
+#endif
+#ifndef QPK_GFE_LN_T
+#define QPK_GFE_LN_T kThreads
+#endif
 template <int K_, class K, int MODE = -1>
 struct GfqElemOp {
     static constexpr int ND = 2 * K_ - 1;
@@ -452,7 +467,9 @@ struct GfqElemOp {
     static constexpr bool kFast = K_ == 3 && ct_fast_field<K>();
     static constexpr bool kFastDlog = kFast && MODE == kGfqDlog;
     static constexpr int IN0 = K_, IN1 = K_, OUT = K_;
-    static constexpr int R = kFastDlog ? QPK_GFE_DL_R : (kFast && MODE == kGfqPacked) ? QPK_GFE_PK_R : QPK_GFE_R;
+    static constexpr bool kFastLin = kFast && MODE == kGfqLinear;
+    static constexpr int R = kFastDlog ? QPK_GFE_DL_R : (kFast && MODE == kGfqPacked) ? QPK_GFE_PK_R
+                             : kFastLin ? QPK_GFE_LN_R : QPK_GFE_R;
     static_assert(!kFast || R % 4 == 0, "the fast path handles groups of 4 records");
     static constexpr uint32_t kP = [] {
         if constexpr (kFast) return K::kP;
@@ -462,9 +479,9 @@ struct GfqElemOp {
     // its REDQ/L-H and dlog paths stage 66 / 88 KB of tables (lane-private
     // copies, kernels.hpp fast_off) beside 4 input stages of 24 KB
     static constexpr bool kLanePriv = kFast && (MODE == kGfqPacked || MODE == kGfqDlog);
-    static constexpr int RR = kLanePriv ? QPK_GFE_PK_RR : QPK_GFE_RR;
-    static constexpr int S = kFastDlog ? QPK_GFE_DL_S : kLanePriv ? QPK_GFE_PK_S : QPK_GFE_S;
-    static constexpr int THREADS = kFastDlog ? QPK_GFE_DL_T : kLanePriv ? QPK_GFE_PK_T : kThreads;
+    static constexpr int RR = kLanePriv ? QPK_GFE_PK_RR : kFastLin ? QPK_GFE_LN_RR : QPK_GFE_RR;
+    static constexpr int S = kFastDlog ? QPK_GFE_DL_S : kLanePriv ? QPK_GFE_PK_S : kFastLin ? QPK_GFE_LN_S : QPK_GFE_S;
+    static constexpr int THREADS = kFastDlog ? QPK_GFE_DL_T : kLanePriv ? QPK_GFE_PK_T : kFastLin ? QPK_GFE_LN_T : kThreads;
     // block words: L16 | H | LOG | ALOG copies
     static constexpr uint32_t kLWords = (kP3 + 1) / 2, kHOff = kLWords, kLogOff = kLWords + kP3,
                               kAlogOff = (kLWords + 2 * kP3 + 3) / 4 * 4;  // 16-byte aligned
