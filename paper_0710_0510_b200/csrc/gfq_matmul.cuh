@@ -131,6 +131,56 @@ __device__ __forceinline__ double redq_repack_swar3(double acc) {
     return __longlong_as_double(static_cast<long long>(mu | kBiasBits));  // 2^52 + sum mu_i q^i
 }
 
+// The canonical re-pack for p = 3, q = 2^10, five digits (GF(3^3), C5), as
+// lane folds on two 32-bit registers: digit i of the output is c_i mod 3, the
+// same word redq_repack_swar3 and redq + assemble (redq.cpp:178-182) return
+// whenever every digit c_i is below q (the chunk bound).  Every integer
+// instruction issued between the MMAs costs the tensor pipe about one
+// dispatch slot (measured with timing-only variants of this kernel, DESIGN
+// section 5: ~0.2 ms of C5 per instruction per accumulator, IMAD.HI four
+// times that), so the count is what matters: 24 instructions, no IMAD.HI,
+// against 33 with two IMAD.HI for the SWAR REDQ with div3_u64.
+//  * align: L = bits 0..29 (digits 0-2, bits 30-31 ride along and are masked
+//    at the end), H = bits 30..49 (digits 3-4 at 0 and 10; the 2^52 bias
+//    bits ride above bit 22 and come out as the bias of the result);
+//  * 2^6 == 2^4 == 1 (mod 3): c -> (c & 63) + (c >> 6) <= 78, then
+//    x -> (x & 15) + (x >> 4) <= 19, each as x - (2^s - 1) (x >> s) on all
+//    lanes of a register at once (no lane borrows);
+//  * x <= 19: floor(x/3) = (11 x) >> 5 (11 x <= 209 stays inside the lane),
+//    x - 3 floor(x/3) is the canonical residue.
+__host__ __device__ __forceinline__ uint64_t repack_canon3_bits(uint64_t bits) {
+    const uint32_t lo = static_cast<uint32_t>(bits), hi = static_cast<uint32_t>(bits >> 32);
+    constexpr uint32_t kH6 = 0x00F03C0Fu, kH4 = 0x00701C07u;  // (c >> 6), (x >> 4) and floor(x/3) lane masks
+#ifdef __CUDA_ARCH__
+    uint32_t xh = __funnelshift_l(lo, hi, 2);
+#else
+    uint32_t xh = (hi << 2) | (lo >> 30);
+#endif
+    uint32_t h = (lo >> 6) & kH6;
+    uint32_t xl = lo - 63u * h;
+    h = (xh >> 6) & (kH6 & 0xFFFFFu);
+    xh -= 63u * h;
+    h = (xl >> 4) & kH4;
+    xl -= 15u * h;
+    h = (xh >> 4) & (kH4 & 0xFFFFFu);
+    xh -= 15u * h;
+    h = ((xl * 11u) >> 5) & kH4;
+    xl -= 3u * h;
+    h = ((xh * 11u) >> 5) & (kH4 & 0xFFFFFu);
+    xh -= 3u * h;
+    // H carried (0x43300000 << 2) mod 2^32 = 0x0CC00000 untouched: >> 2 gives 0x03300000
+    const uint32_t out_lo = (xl & 0x3FFFFFFFu) | (xh << 30);
+#ifdef __CUDA_ARCH__
+    const uint32_t out_hi = __funnelshift_r(xh, 1u, 2);  // (xh >> 2) | 0x40000000 in one SHF
+#else
+    const uint32_t out_hi = (xh >> 2) + 0x40000000u;
+#endif
+    return (static_cast<uint64_t>(out_hi) << 32) | out_lo;
+}
+__device__ __forceinline__ double redq_repack_canon3(double acc) {
+    return __longlong_as_double(static_cast<long long>(repack_canon3_bits(dbits(acc))));
+}
+
 // Lane fold (repack mode QPK_REPACK_FOLD), p = 3 and q = 2^B: every digit
 // c_i = l_i + 2^S h_i (l_i < 2^S) is replaced by l_i + h_i, which is
 // congruent mod 3 because 2^S == 1 (mod 3) for even S.  Digits drop from
@@ -149,6 +199,10 @@ __device__ __forceinline__ double repack_fold3(double acc) {
     const uint64_t f = (rb & ML) + ((rb >> S) & MH);
     return __longlong_as_double(static_cast<long long>(f | kBiasBits));
 }
+
+#if defined(QPK_MM_EXP)
+#include "../../scripts/mm_exp_repack.cuh"  // development: timing-only re-pack variants (scripts/mm_exp.sh)
+#endif
 
 // fold split S: the largest even S <= B - S + 2 (balances l_i and h_i)
 template <uint32_t B>
@@ -171,9 +225,14 @@ struct mm_biased {
 
 template <int ND, class K, bool FOLD>
 __device__ __forceinline__ double repack_one(const K& c, double r) {
+#if defined(QPK_MM_EXP)
+    if constexpr (is_swar3<K>::value && !FOLD) return mm_exp_repack<ND, K::kQbits>(r);
+#endif
     if constexpr (is_swar3<K>::value) {
         if constexpr (FOLD)
             return repack_fold3<ND, K::kQbits, kFoldShift<K::kQbits>>(r);
+        else if constexpr (ND == 5 && K::kQbits == 10)
+            return redq_repack_canon3(r);
         else
             return redq_repack_swar3<ND, K::kQbits>(r);
     } else {
@@ -369,6 +428,16 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
 
     // ------------------------- epilogue ------------------------------------
+#if defined(QPK_MM_EXP)
+    if constexpr (is_swar3<K>::value && !FOLD) {  // timing-only variants: keep the table indices in range
+#pragma unroll
+        for (int i = 0; i < MT; ++i)
+#pragma unroll
+            for (int j = 0; j < NT; ++j)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) acc[i][j][h] = redq_repack_swar3<ND, K::kQbits>(acc[i][j][h]);
+    }
+#endif
     const uint32_t lc_s = smem_addr(tabs), hc_s = lc_s + 4 * nlh, lg_s = lc_s + 8 * nlh;
 #pragma unroll
     for (int i = 0; i < MT; ++i) {
