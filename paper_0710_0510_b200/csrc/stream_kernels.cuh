@@ -55,8 +55,8 @@ __device__ __forceinline__ void pack_records(const uint64_t (&rec)[R], uint32_t 
 __device__ __forceinline__ uint32_t run_byte(const uint32_t* w, int i) { return byte_of(w[i >> 2], i & 3); }
 
 // residues mu_0..mu_{ND-1} of one word, packed one per byte
-template <int ND, int W, class K>
-__device__ __forceinline__ uint64_t redq_record(const K& c, double r, uint32_t tab_saddr) {
+template <int ND, int W, class K, class TabLoad>
+__device__ __forceinline__ uint64_t redq_record(const K& c, double r, TabLoad tab_load) {
     uint32_t u[ND];
     redq_raw_digits<ND>(c, r, u);
     constexpr int D = ND - 1;
@@ -73,7 +73,7 @@ __device__ __forceinline__ uint64_t redq_record(const K& c, double r, uint32_t t
                 uint32_t idx = 0;
 #pragma unroll
                 for (int j = W - 1; j >= 0; --j) idx = idx * c.radix() + (s + j <= D ? u[s + j] : 0u);
-                const uint32_t e = lds_u32(tab_saddr + 4 * idx);
+                const uint32_t e = tab_load(idx);
                 const int keep = (a == A - 1) ? (D - s + 1) : (W - 1);  // bytes of this window kept
                 const uint32_t mask = keep >= 4 ? 0xffffffffu : ((1u << (8 * keep)) - 1);
                 rec |= static_cast<uint64_t>(e & mask) << (8 * s);
@@ -87,6 +87,11 @@ __device__ __forceinline__ uint64_t redq_record(const K& c, double r, uint32_t t
 #pragma unroll
     for (int j = 0; j < ND; ++j) rec |= static_cast<uint64_t>(mu[j]) << (8 * j);
     return rec;
+}
+// ... with the table staged in shared memory at byte address tab_saddr
+template <int ND, int W, class K>
+__device__ __forceinline__ uint64_t redq_record(const K& c, double r, uint32_t tab_saddr) {
+    return redq_record<ND, W>(c, r, [tab_saddr](uint32_t idx) { return lds_u32(tab_saddr + 4 * idx); });
 }
 
 // ----------------------------------------------------------------- ops
@@ -202,12 +207,69 @@ __device__ __forceinline__ uint32_t record_int(const uint32_t* w, int r) {
 #ifndef QPK_PM_S
 #define QPK_PM_S 2
 #endif
+// C1's field on byte lanes: F_3[X] products of degree < 4 at q = 2^5 (seven
+// digits), the config's pipeline -- DQT pack (dqt.cpp:23-37), fp64 product,
+// REDQ with the Lemma-1 floor (redq.cpp:31-60) and the mod-p correction
+// (redq.cpp:63-65; neg_q = 1) -- with every step on all lanes of a register
+// at once.  The generic path spends ~100 instructions per pair, most of them
+// on the 16-lane ALU pipe (ncu r02 c1: ALU the busiest pipe, 102
+// thread-instructions per pair); this one ~40, split between the ALU and FMA
+// pipes.  xa, xb: the four coefficient bytes of each operand, all below 3
+// (checked by the caller for the whole run).  Returns residue bytes 0-3 and
+// (by reference) bytes 4-6.
+//  * pack: moving a byte field left by s is x + (2^s - 1)(x & field): two
+//    multiply-adds put byte i at bit 5i + 9, and the double with exponent
+//    2^43 whose low mantissa word that is equals 2^43 + A exactly;
+//  * u_i = floor(r/q^i) - 3 floor(rop/q^i) lies in [0, 2] and is fixed mod 4
+//    by the low two bits of lane i of r and of rop (-3 == 1 mod 4); lane 6
+//    starts at bit 30, so all seven 2-bit fields sit in the low words;
+//  * mu_i = (u_i + u_{i+1}) mod 3 (mu_6 = u_6): v = u + (u >> 5) <= 4,
+//    minus 3 where v >= 3;
+//  * the 2-bit fields at 5i are spread to bytes by the same multiply-adds.
+__device__ __forceinline__ uint32_t polymul_f3q32(double inv_p, uint32_t xa, uint32_t xb, uint32_t& hi3) {
+    constexpr uint32_t kM1 = 0x42108421u, kM3 = 3u * kM1;  // bit 0 / bits 0-1 of every 5-bit lane
+    const uint32_t ya = xa + 7u * (xa & 0x00030003u);      // bytes 0, 2 up by 3: fields at 3, 8, 19, 24
+    const uint32_t yb = xb + 7u * (xb & 0x00030003u);
+    const uint32_t pa = ya + 63u * (ya & 0x0000ffffu);     // low pair up by 6: fields at 9, 14, 19, 24
+    const uint32_t pb = yb + 63u * (yb & 0x0000ffffu);
+    const double da = __hiloint2double(0x42a00000, static_cast<int>(pa)) - 8796093022208.0;  // 2^43 + A - 2^43
+    const double db = __hiloint2double(0x42a00000, static_cast<int>(pb)) - 8796093022208.0;
+    const double r = da * db;  // exact, < 2^35
+    const uint32_t rl = static_cast<uint32_t>(dbits(r + kTwo52));
+    const uint32_t ol = static_cast<uint32_t>(dbits(__dadd_rz(__dmul_ru(r, inv_p), kTwo52)));
+    const uint32_t u = ((rl & kM3) + (ol & kM3)) & kM3;
+    const uint32_t v = u + (u >> 5);
+    const uint32_t g = ((v + kM1) >> 2) & kM1;
+    const uint32_t mu = v - 3u * g;
+    uint32_t lo = mu & 0x00018c63u;          // residues 0-3 at 0, 5, 10, 15
+    lo += 63u * (lo & 0x00018c00u);          // 2, 3 up by 6: 0, 5, 16, 21
+    lo += 7u * (lo & 0x00600060u);           // 1, 3 up by 3: 0, 8, 16, 24
+    uint32_t hi = mu >> 20;                  // residues 4-6 at 0, 5, 10
+    hi += 63u * (hi & 0x00000c00u);          // 6 up by 6: 0, 5, 16
+    hi += 7u * (hi & 0x00000060u);           // 5 up by 3: 0, 8, 16
+    hi3 = hi;
+    return lo;
+}
+
+template <class K>
+constexpr bool is_f3_q32() {
+    if constexpr (K::kSafe) return K::kP == 3 && K::kQbitsCt == 5;
+    else return false;
+}
+
 template <int K_, int W, class K>
 struct PolymulOp {
     static constexpr int ND = 2 * K_ - 1;
     static constexpr int IN0 = K_, IN1 = K_, OUT = ND, R = QPK_PM_R, RR = QPK_PM_RR, S = QPK_PM_S;
     PolymulParams P;
-    __host__ __device__ uint32_t tables_words() const { return W ? P.rq.n_entries : 0u; }
+    // F_3, q = 2^5, k = 4 (C1): runs of clean bytes take polymul_f3q32, which
+    // needs no table; the record-by-record path then reads the window table
+    // from global memory, so no launch stages it (the staging and its CTA
+    // barrier cost 0.26 us of a 4.8 us launch) and the one-wave direct kernel
+    // is held to 7 CTAs per SM (32 registers: all 1024 CTAs of C1 resident)
+    static constexpr bool kF3Q32 = K_ == 4 && R == 4 && W > 0 && is_f3_q32<K>();
+    static constexpr int kDirectMinBlocks = kF3Q32 ? 7 : 1;
+    __host__ __device__ uint32_t tables_words() const { return W && !kF3Q32 ? P.rq.n_entries : 0u; }
     __host__ __device__ const uint32_t* tables_src() const { return P.rq.table; }
     __device__ __forceinline__ void apply(const uint32_t* a, const uint32_t* b, uint32_t (&ow)[R * OUT / 4],
                                           uint32_t tab, uint32_t&) const {
@@ -220,6 +282,22 @@ struct PolymulOp {
         if constexpr (K::kSafe) {
             if constexpr ((R * K_) % 4 == 0 && K::kP < 128)
                 clean = all_bytes_below<R * K_ / 4>(a, c.p()) && all_bytes_below<R * K_ / 4>(b, c.p());
+            if constexpr (kF3Q32) {
+                if (clean) {
+                    uint32_t lo[R], hi[R];
+#pragma unroll
+                    for (int r = 0; r < R; ++r) lo[r] = polymul_f3q32(P.rq.inv_p, a[r], b[r], hi[r]);
+                    // four 7-byte records as seven words
+                    ow[0] = lo[0];
+                    ow[1] = __byte_perm(hi[0], lo[1], 0x4210);
+                    ow[2] = __byte_perm(lo[1], hi[1], 0x4321);
+                    ow[3] = __byte_perm(hi[1], lo[2], 0x5421);
+                    ow[4] = __byte_perm(lo[2], hi[2], 0x5432);
+                    ow[5] = __byte_perm(hi[2], lo[3], 0x6542);
+                    ow[6] = __byte_perm(lo[3], hi[3], 0x6543);
+                    return;
+                }
+            }
         }
 #pragma unroll
         for (int r = 0; r < R; ++r) {
@@ -232,7 +310,13 @@ struct PolymulOp {
                 record_coeffs<K_>(c, P.rq.mod_magic, b, r, cb);
             }
             // exact: q^(2k-1) < 2^53 (validated)
-            rec[r] = redq_record<ND, W>(c, pack_word<K_>(c, qd, ca) * pack_word<K_>(c, qd, cb), tab);
+            const double word = pack_word<K_>(c, qd, ca) * pack_word<K_>(c, qd, cb);
+            if constexpr (kF3Q32) {
+                const uint32_t* gtab = P.rq.table;
+                rec[r] = redq_record<ND, W>(c, word, [gtab](uint32_t idx) { return __ldg(gtab + idx); });
+            } else {
+                rec[r] = redq_record<ND, W>(c, word, tab);
+            }
         }
         pack_records<R, OUT>(rec, ow);
     }
@@ -786,6 +870,25 @@ __device__ __forceinline__ void stg_run(uint8_t* base, const uint32_t (&w)[N]) {
     }
 }
 
+// The same 32 runs of one warp (N words each, N not a multiple of 4: a
+// thread's own stores are 4 bytes wide and N * 4 bytes apart across lanes,
+// 7+ cache lines per instruction) written as 16-byte chunks of the warp's
+// contiguous output range, transposed through a per-warp shared buffer
+// (stride N words: conflict-free for odd N).  `warp_out` is 16-byte aligned.
+template <int N>
+__device__ __forceinline__ void stg_run_warp(uint8_t* warp_out, uint32_t* wbuf, const uint32_t (&w)[N], int lane) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) wbuf[lane * N + i] = w[i];
+    __syncwarp();
+    constexpr int V = 32 * N / 4;
+#pragma unroll
+    for (int j = 0; j < (V + 31) / 32; ++j) {
+        const int ch = j * 32 + lane;
+        if (ch < V) reinterpret_cast<uint4*>(warp_out)[ch] = reinterpret_cast<const uint4*>(wbuf)[ch];
+    }
+    __syncwarp();
+}
+
 template <class Op, class = void>
 struct has_custom_stage : std::false_type {};
 template <class Op>
@@ -979,8 +1082,14 @@ __device__ __forceinline__ void ldg_run(const uint8_t* base, uint32_t (&w)[N > 0
     }
 }
 
+template <class Op, class = void>
+struct op_direct_min_blocks : std::integral_constant<int, 1> {};
 template <class Op>
-__global__ void __launch_bounds__(kThreads) stream_direct_kernel(const Op op, const uint8_t* __restrict__ in0,
+struct op_direct_min_blocks<Op, std::enable_if_t<(Op::kDirectMinBlocks > 1)>>
+    : std::integral_constant<int, Op::kDirectMinBlocks> {};
+
+template <class Op>
+__global__ void __launch_bounds__(kThreads, op_direct_min_blocks<Op>::value) stream_direct_kernel(const Op op, const uint8_t* __restrict__ in0,
                                                                  const uint8_t* __restrict__ in1,
                                                                  uint8_t* __restrict__ out, uint64_t n_runs,
                                                                  uint32_t* status) {
@@ -995,15 +1104,24 @@ __global__ void __launch_bounds__(kThreads) stream_direct_kernel(const Op op, co
         ldg_run<G::W0>(in0 + run * (G::R * Op::IN0), a);
         ldg_run<G::W1>(in1 + run * (G::R * Op::IN1), b);
     }
-    stage_op_tables<Op, false>(op, s_tab);
-    __syncthreads();
+    if (op.tables_words() > 0) {  // CTA-uniform
+        stage_op_tables<Op, false>(op, s_tab);
+        __syncthreads();
+    }
     const uint32_t tab = smem_addr(s_tab);
     uint32_t err = 0;
     const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+    constexpr bool kWarpStore = G::WO % 4 != 0;
+    __shared__ __align__(16) uint32_t s_wout[kWarpStore ? kThreads * G::WO : 4];
+    const int lane = threadIdx.x & 31;
+    const bool out_aligned = (reinterpret_cast<uintptr_t>(out) & 15) == 0;
     for (; run < n_runs; run += stride) {
         uint32_t ow[G::WO];
         op.apply(a, b, ow, tab, err);
-        stg_run<G::WO>(out + run * (G::R * Op::OUT), ow);
+        if (kWarpStore && out_aligned && run - lane + 31 < n_runs)  // warp-uniform: all 32 runs exist
+            stg_run_warp<G::WO>(out + (run - lane) * (G::R * Op::OUT), s_wout + (threadIdx.x - lane) * G::WO, ow, lane);
+        else
+            stg_run<G::WO>(out + run * (G::R * Op::OUT), ow);
         if (run + stride < n_runs) {
             ldg_run<G::W0>(in0 + (run + stride) * (G::R * Op::IN0), a);
             ldg_run<G::W1>(in1 + (run + stride) * (G::R * Op::IN1), b);
