@@ -280,6 +280,6 @@ int num_sms();  // of the current device
 // Raise `kernel`'s dynamic shared-memory limit to at least `bytes` on the
 // current device (a per-device function attribute: recorded per (kernel,
 // device), thread-safe; a no-op below the 48 KB default).
-cudaError_t ensure_dyn_smem(const void* kernel, size_t bytes);
+cudaError_t ensure_dyn_smem(const void* kernel, size_t bytes, size_t static_bytes = 0);
 
 }  // namespace qpk

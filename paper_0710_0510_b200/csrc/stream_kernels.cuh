@@ -1191,7 +1191,9 @@ cudaError_t run_stream(const Op& op, const uint8_t* in0, const uint8_t* in1, uin
     // small batches: the direct kernel over whole runs, then the tail
     if (aligned && n < kDirectMax && n >= uint64_t(G::R)) {
         const uint64_t n_runs = n / G::R;
-        if (cudaError_t e = ensure_dyn_smem(reinterpret_cast<const void*>(stream_direct_kernel<Op>), tab_bytes);
+        // (the direct kernel's static buffer of the warp-transposed stores counts against the 48 KB default)
+        constexpr size_t kStatic = G::WO % 4 != 0 ? size_t(kThreads) * G::WO * 4 : 16;
+        if (cudaError_t e = ensure_dyn_smem(reinterpret_cast<const void*>(stream_direct_kernel<Op>), tab_bytes, kStatic);
             e != cudaSuccess)
             return e;
         const uint64_t grid = std::min<uint64_t>((n_runs + kThreads - 1) / kThreads, uint64_t(sms) * 16);

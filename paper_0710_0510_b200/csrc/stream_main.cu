@@ -235,8 +235,9 @@ int num_sms() {
     return v;
 }
 
-cudaError_t ensure_dyn_smem(const void* kernel, size_t bytes) {
-    if (bytes <= 48 * 1024) return cudaSuccess;
+cudaError_t ensure_dyn_smem(const void* kernel, size_t bytes, size_t static_bytes) {
+    // the 48 KB a launch gets without the attribute covers static + dynamic
+    if (bytes + static_bytes <= 48 * 1024) return cudaSuccess;
     static std::mutex mu;
     static std::map<std::pair<const void*, int>, size_t> done;
     int dev = 0;
