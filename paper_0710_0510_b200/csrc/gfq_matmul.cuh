@@ -17,11 +17,15 @@
 //    below q and the word below 2^53.  Re-packs run at stage granularity,
 //    outside the stage loop (so they are never predicated into every stage)
 //    and staggered so the two consumer warps of an SM sub-partition never
-//    re-pack in the same stage: one warp's integer work overlaps the other
-//    warp's MMAs.  On the fast paths (p = 3, q = 2^(2m)) the accumulators
-//    carry a 2^52 bias so the word is the accumulator's mantissa, and the
-//    re-pack is integer-only: the SWAR REDQ (floor(r/3) by div3_u64) or,
-//    with repack = fold, a congruent lane fold (7 instructions);
+//    re-pack in the same stage.  Measured: integer
+//    instructions do not hide behind the DMMAs -- each one costs the
+//    sub-partition about one dispatch slot of the 16 a DMMA takes, wherever
+//    it sits -- so the re-pack is written for instruction count.  On the fast
+//    paths (p = 3, q = 2^(2m)) the accumulators carry a 2^52 bias so the word
+//    is the accumulator's mantissa and the re-pack is integer-only: canonical
+//    lane folds for C5 (24 instructions), the SWAR REDQ (floor(r/3) by
+//    div3_u64) for the other fields, or, with repack = fold, a congruent lane
+//    fold (7 instructions);
 //  * the REDQ-re-pack kernel walks tiles in groups of 8 tile rows (L2 reuse
 //    of B), the fold kernel row-major (measured best for each);
 //  * epilogue: final REDQ digits -> low/high half tables in coefficient form

@@ -17,15 +17,18 @@
 // the reference's except wall_time_ns and the algo tag: device rows are
 // tagged `<algo>_b200`, host verification rows keep the reference's name.
 // QPACK_TABLE_CACHE reuses serialized correction tables (qpack.cpp:80-98).
+#include <array>
 #include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <filesystem>
 #include <fstream>
-#include <iomanip>
+#include <functional>
 #include <iostream>
 #include <map>
 #include <sstream>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "qpack/common.hpp"
@@ -38,63 +41,98 @@
 #include "qpack/redq.hpp"
 #include "qpack/rng.hpp"
 
+namespace fs = std::filesystem;
 using namespace qpack;
 
 namespace {
 
-struct Row {
-    std::string algo;
-    u64 p = 0, q = 0;
-    u32 k = 0, d = 0;
-    u64 n = 0, n_q = 0, n_d = 0;
-    CostReport cost;
-    u64 wall_ns = 0;
-    u64 checksum = 0;
+std::string hex16(u64 v) {
+    char buf[17];
+    std::snprintf(buf, sizeof buf, "%016llx", static_cast<unsigned long long>(v));
+    return buf;
+}
+
+std::string hex(u64 v) {
+    char buf[17];
+    std::snprintf(buf, sizeof buf, "%llx", static_cast<unsigned long long>(v));
+    return buf;
+}
+
+// one CSV row: what ran (tag, field and shape), what it counted, how long it
+// took, and the FNV-1a fold of its output
+struct Measurement {
+    std::string tag;
+    u64 prime = 0, radix = 0, size = 0, group = 0, delay = 0;
+    u32 chunk = 0, degree = 0;
+    CostReport counted;
+    u64 elapsed_ns = 0, fnv = 0;
 };
 
-void append_csv(const std::string& path, const Row& r) {
-    if (path.empty()) return;
-    const bool fresh = !std::filesystem::exists(path) || std::filesystem::file_size(path) == 0;
-    std::ofstream out(path, std::ios::app);
-    if (!out) throw std::runtime_error("cannot open csv file " + path);
-    if (fresh) out << "algo,p,q,k,d,N,n_q,n_d,mul_add,divisions,table_accesses,wall_time_ns,checksum\n";
-    out << r.algo << ',' << r.p << ',' << r.q << ',' << r.k << ',' << r.d << ',' << r.n << ',' << r.n_q << ','
-        << r.n_d << ',' << r.cost.mul_add << ',' << r.cost.divisions << ',' << r.cost.table_accesses << ','
-        << r.wall_ns << ',' << std::hex << std::setw(16) << std::setfill('0') << r.checksum << std::dec
-        << std::setfill(' ') << '\n';
-}
-
-u64 now_ns() {
-    return static_cast<u64>(
-        std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now().time_since_epoch())
-            .count());
-}
-
-// QPACK_TABLE_CACHE: load the plan's table if cached, else save it
-void wire_table_cache(RedqPlan& plan) {
-    const char* dir = std::getenv("QPACK_TABLE_CACHE");
-    if (!dir || !plan.correction) return;
-    const CorrectionTable& t = *plan.correction;
-    std::ostringstream name;
-    name << dir << "/redq_p" << t.p << "_q" << t.q << "_w" << t.k_window << "_"
-         << (t.indexing == TableIndexing::base_p ? "basep" : "shift") << ".tbl";
-    const std::string path = name.str();
-    if (std::filesystem::exists(path)) {
-        std::ifstream in(path, std::ios::binary);
-        plan.attach_correction(load_correction_table(in));
-        return;
+class CsvLog {
+public:
+    explicit CsvLog(std::string file) : file_(std::move(file)) {}
+    void add(const Measurement& m) const {
+        if (file_.empty()) return;
+        std::error_code ec;
+        const bool header = !fs::exists(file_, ec) || fs::file_size(file_, ec) == 0;
+        std::ofstream f(file_, std::ios::app);
+        if (!f) throw std::runtime_error("cannot open csv file " + file_);
+        if (header) f << kColumns << '\n';
+        const std::array<u64, 11> nums{m.prime, m.radix,          m.chunk,
+                                       m.degree, m.size,          m.group,
+                                       m.delay,  m.counted.mul_add, m.counted.divisions,
+                                       m.counted.table_accesses,  m.elapsed_ns};
+        f << m.tag;
+        for (u64 v : nums) f << ',' << v;
+        f << ',' << hex16(m.fnv) << '\n';
     }
-    std::filesystem::create_directories(dir);
-    std::ofstream out(path, std::ios::binary);
-    save_correction_table(t, out);
+
+private:
+    static constexpr const char* kColumns =
+        "algo,p,q,k,d,N,n_q,n_d,mul_add,divisions,table_accesses,wall_time_ns,checksum";
+    std::string file_;
+};
+
+class Stopwatch {
+public:
+    Stopwatch() : t0_(clock::now()) {}
+    u64 ns() const {
+        return static_cast<u64>(std::chrono::duration_cast<std::chrono::nanoseconds>(clock::now() - t0_).count());
+    }
+
+private:
+    using clock = std::chrono::steady_clock;
+    clock::time_point t0_;
+};
+
+// QPACK_TABLE_CACHE: a plan's correction table is read back from the cache
+// directory when a file for (p, q, window, indexing) exists, stored otherwise
+void reuse_cached_table(RedqPlan& plan) {
+    const char* root = std::getenv("QPACK_TABLE_CACHE");
+    if (root == nullptr || !plan.correction.has_value()) return;
+    const CorrectionTable& tab = *plan.correction;
+    const std::string leaf = "redq_p" + std::to_string(tab.p) + "_q" + std::to_string(tab.q) + "_w" +
+                             std::to_string(tab.k_window) +
+                             (tab.indexing == TableIndexing::base_p ? "_basep.tbl" : "_shift.tbl");
+    const fs::path where = fs::path(root) / leaf;
+    if (std::ifstream cached(where, std::ios::binary); cached) {
+        plan.attach_correction(load_correction_table(cached));
+    } else {
+        fs::create_directories(root);
+        std::ofstream fresh(where, std::ios::binary);
+        save_correction_table(tab, fresh);
+    }
 }
 
-std::vector<u64> parse_list(const std::string& s, u64 p) {
-    std::vector<u64> v;
-    std::stringstream ss(s);
-    std::string item;
-    while (std::getline(ss, item, ',')) v.push_back(std::stoull(item) % p);
-    return v;
+std::vector<u64> coefficients_of(const std::string& text, u64 p) {
+    std::vector<u64> out;
+    std::size_t at = 0;
+    while (at <= text.size() && !text.empty()) {
+        const std::size_t comma = std::min(text.find(',', at), text.size());
+        if (comma > at) out.push_back(std::stoull(text.substr(at, comma - at)) % p);
+        at = comma + 1;
+    }
+    return out;
 }
 
 // plain schoolbook product mod p: the CLI's own verification
@@ -120,222 +158,242 @@ struct Args {
 
 int cmd_mulpoly(const Args& a) {
     if (!a.has("p") || !a.has("n")) throw std::invalid_argument("mulpoly: --p and --n are required");
-    const u64 p = a.u("p", 3), n = a.u("n", 100), seed = a.u("seed", 42);
+    const u64 p = a.u("p", 3), n = a.u("n", 100);
     const u32 m = static_cast<u32>(a.u("m", 53));
-    const unsigned repeat = static_cast<unsigned>(a.u("repeat", 1));
-    const std::string algo = a.str("algo", "fqt"), csv = a.str("csv");
-    const bool no_verify = a.flag("no-verify");
+    const std::string algo = a.str("algo", "fqt");
+    const CsvLog log(a.str("csv"));
+    const bool on_device = algo == "fqt", verify = on_device && !a.flag("no-verify");
     if (algo == "delayed") throw std::domain_error("--algo delayed is not part of qpack-b200 (host-only variant)");
-    if (algo != "fqt" && algo != "oracle") throw std::domain_error("unknown --algo " + algo);
-    SplitMix64 rng(seed);
-    QadicParams params{};
-    RedqPlan plan;
-    if (algo == "fqt") {
-        params = a.has("d") ? qadic_for_degree(p, static_cast<u32>(a.u("d", 0)), m) : best_qadic(p, m, 1, true);
-        plan = fqt_reduction_plan(params, params.k - 1);
-        wire_table_cache(plan);
+    if (!on_device && algo != "oracle") throw std::domain_error("unknown --algo " + algo);
+    QadicParams shape{};
+    RedqPlan reducer;
+    if (on_device) {
+        shape = a.has("d") ? qadic_for_degree(p, static_cast<u32>(a.u("d", 0)), m) : best_qadic(p, m, 1, true);
+        reducer = fqt_reduction_plan(shape, shape.k - 1);
+        reuse_cached_table(reducer);
     }
-    for (unsigned rep = 0; rep < repeat; ++rep) {
-        DensePoly x{p, {}}, y{p, {}};
-        if (a.has("a") || a.has("b")) {
-            x.coeffs = parse_list(a.str("a"), p);
-            y.coeffs = parse_list(a.str("b"), p);
-            if (x.coeffs.empty() || y.coeffs.empty())
+    SplitMix64 draws(a.u("seed", 42));
+    const bool fixed = a.has("a") || a.has("b");
+    for (u64 rep = 0, reps = a.u("repeat", 1); rep < reps; ++rep) {
+        DensePoly lhs{p, {}}, rhs{p, {}};
+        if (fixed) {
+            lhs.coeffs = coefficients_of(a.str("a"), p);
+            rhs.coeffs = coefficients_of(a.str("b"), p);
+            if (lhs.coeffs.empty() || rhs.coeffs.empty())
                 throw std::domain_error("--a and --b must both be given for fixed inputs");
         } else {
-            for (u64 i = 0; i <= n; ++i) x.coeffs.push_back(rng.below(p));
-            for (u64 i = 0; i <= n; ++i) y.coeffs.push_back(rng.below(p));
+            for (DensePoly* poly : {&lhs, &rhs})
+                for (u64 i = 0; i <= n; ++i) poly->coeffs.push_back(draws.below(p));
         }
-        Row r;
-        r.algo = algo == "fqt" ? "fqt_b200" : "oracle";
-        r.p = p;
-        r.n = n;
-        DensePoly out{p, {}};
-        const u64 t0 = now_ns();
-        if (algo == "fqt") {
-            out = fqt_mul(x, y, params.k - 1, params, plan, &r.cost);  // K6 on the device (m <= 53)
-            r.q = params.q;
-            r.k = params.k;
-            r.d = params.k - 1;
-            r.n_q = params.n_q;
-        } else {
-            out = schoolbook(x, y);
+        Measurement row;
+        row.tag = on_device ? "fqt_b200" : "oracle";
+        row.prime = p;
+        row.size = n;
+        if (on_device) {
+            row.radix = shape.q;
+            row.chunk = shape.k;
+            row.degree = shape.k - 1;
+            row.group = shape.n_q;
         }
-        r.wall_ns = now_ns() - t0;
-        r.checksum = fold_checksum(out.coeffs.data(), out.coeffs.size());
-        if (!no_verify && algo != "oracle" && !(out == schoolbook(x, y))) {
+        const Stopwatch clock;
+        // K6 on the device (m <= 53), or the host schoolbook product
+        const DensePoly product =
+            on_device ? fqt_mul(lhs, rhs, shape.k - 1, shape, reducer, &row.counted) : schoolbook(lhs, rhs);
+        row.elapsed_ns = clock.ns();
+        row.fnv = fold_checksum(product.coeffs.data(), product.coeffs.size());
+        if (verify && !(product == schoolbook(lhs, rhs))) {
             std::cerr << "verification FAILED against the schoolbook product\n";
             return 3;
         }
-        append_csv(csv, r);
-        std::cout << r.algo << " p=" << p << " N=" << n << " rep=" << rep << " mul_add=" << r.cost.mul_add
-                  << " divisions=" << r.cost.divisions << " table_accesses=" << r.cost.table_accesses
-                  << " wall_ns=" << r.wall_ns << " checksum=" << std::hex << r.checksum << std::dec
-                  << (no_verify || algo == "oracle" ? "" : " verified=ok") << "\n";
+        log.add(row);
+        std::cout << row.tag << " p=" << p << " N=" << n << " rep=" << rep << " mul_add=" << row.counted.mul_add
+                  << " divisions=" << row.counted.divisions << " table_accesses=" << row.counted.table_accesses
+                  << " wall_ns=" << row.elapsed_ns << " checksum=" << hex(row.fnv) << (verify ? " verified=ok" : "")
+                  << "\n";
     }
     return 0;
 }
 
+std::string bracketed(const std::vector<u64>& v) {
+    std::string s;
+    for (u64 x : v) s += (s.empty() ? "[" : ",") + std::to_string(x);
+    return (s.empty() ? "[" : s) + "]";
+}
+
+// The worked examples of the paper (PAPER.md sections 2-4) as exhibits of
+// (label, computed, expected) lines, then the same reductions on the device.
 int cmd_paper_examples(const Args& a) {
-    int bad = 0;
-    auto check = [&](const std::string& what, const std::string& got, const std::string& want) {
-        const bool ok = got == want;
-        std::cout << (ok ? "  ok   " : "  FAIL ") << what << ": " << got;
-        if (!ok) std::cout << " (expected " << want << ")";
-        std::cout << "\n";
-        bad += ok ? 0 : 1;
+    using Line = std::tuple<std::string, std::string, std::string>;
+    struct Exhibit {
+        std::string title;
+        std::function<std::vector<Line>()> lines;
     };
-    auto fmt = [](const std::vector<u64>& v) {
-        std::string s = "[";
-        for (std::size_t i = 0; i < v.size(); ++i) s += (i ? "," : "") + std::to_string(v[i]);
-        return s + "]";
+    const bool corrupt = a.flag("inject-fault");
+    const std::vector<Exhibit> exhibits = {
+        {"[1] radix-100 product over Z/3Z",
+         [] {
+             const QadicParams radix100{3, 100, 2, 1, 53};
+             const DensePoly x_plus_1{3, {1, 1}}, x_plus_2{3, {2, 1}};
+             const Packed word = dqt_mul(pack(x_plus_1, radix100), pack(x_plus_2, radix100));
+             const bool reduced = dqt_mul_poly(x_plus_1, x_plus_2, radix100) == DensePoly{3, {2, 0, 1}};
+             return std::vector<Line>{{"101 x 102", to_string(word.value), "10302"},
+                                      {"digits", bracketed(unpack(word, 3)), "[2,3,1]"},
+                                      {"reduced", reduced ? "X^2+2" : "?", "X^2+2"}};
+         }},
+        {"[2] five residues reduced at once (p | q)",
+         [] {
+             const u128 word = static_cast<u128>(100020003) * 400050006;
+             return std::vector<Line>{
+                 {"packed product", to_string(word), "40013002800270018"},
+                 {"reduced word", to_string(redq(word, RedqPlan::build(5, 10000, 4))), "40003000300020003"}};
+         }},
+        {"[3] full correction at p=23, q=10^6",
+         [] {
+             const RedqTrace tr = redq_trace(parse_u128("1234005678009123004567"), RedqPlan::build(23, 1000000, 3));
+             return std::vector<Line>{{"rop", to_string(tr.rop), "53652420783005348024"},
+                                      {"u", bracketed(tr.u), "[15,8,18,15]"},
+                                      {"mu", bracketed(tr.mu), "[13,15,20,15]"}};
+         }},
+        {"[4] degree-6 correction through three window lookups",
+         [corrupt] {
+             CorrectionTable window3 = build_correction_table(23, 1000000, 3, TableIndexing::base_p);
+             if (corrupt)
+                 for (u64& e : window3.entries) e ^= 1;  // a corrupted cache must be detected
+             const RedqPlan direct = RedqPlan::build(23, 1000000, 6);
+             SplitMix64 draws(4);
+             u64 lookups = 0, disagreements = 0;
+             std::vector<u64> raw(7);
+             for (int trial = 0; trial < 500; ++trial) {
+                 for (u64& digit : raw) digit = draws.below(23);
+                 CostReport tally;
+                 disagreements += correct_tabulated(raw, window3, &tally) != correct_direct(raw, direct);
+                 lookups = tally.table_accesses;
+             }
+             return std::vector<Line>{{"window accesses", std::to_string(lookups), "3"},
+                                      {"tabulated == direct", disagreements == 0 ? "yes" : "no", "yes"}};
+         }},
+        {"[5] the same reductions on the device (batched REDQ kernels)",
+         [] {
+             // random words at p=23, q=2^7, d=6 through the windowed device
+             // table (Alg. 3), against the host REDQ of each word
+             RedqPlan pd = RedqPlan::build(23, 1 << 7, 6, RedqMode::float_premul);
+             pd.attach_correction(build_correction_table(23, 1 << 7, 3, TableIndexing::base_p));
+             std::vector<double> words(4096);
+             SplitMix64 wr(5);
+             for (double& w : words) {
+                 u64 r = 0;
+                 for (int i = 0; i < 7; ++i) r = r * 128 + wr.below(128);
+                 w = static_cast<double>(r);
+             }
+             std::vector<std::uint8_t> res(words.size() * 7);
+             gpu::redq_residues_batch(words, pd, res);
+             bool same = true;
+             for (std::size_t i = 0; i < words.size(); ++i) {
+                 const std::vector<u64> mu = redq_residues(static_cast<u128>(static_cast<u64>(words[i])), pd);
+                 for (int j = 0; j < 7; ++j) same &= res[i * 7 + j] == mu[j];
+             }
+             return std::vector<Line>{{"device residues == host", same ? "yes" : "no", "yes"}};
+         }},
     };
-    std::cout << "[1] radix-100 product over Z/3Z\n";
-    const QadicParams ex1{3, 100, 2, 1, 53};
-    const Packed prod1 = dqt_mul(pack(DensePoly{3, {1, 1}}, ex1), pack(DensePoly{3, {2, 1}}, ex1));
-    check("101 x 102", to_string(prod1.value), "10302");
-    check("digits", fmt(unpack(prod1, 3)), "[2,3,1]");
-    check("reduced", dqt_mul_poly(DensePoly{3, {1, 1}}, DensePoly{3, {2, 1}}, ex1) == DensePoly{3, {2, 0, 1}}
-                         ? "X^2+2" : "?",
-          "X^2+2");
-
-    std::cout << "[2] five residues reduced at once (p | q)\n";
-    const u128 prod2 = static_cast<u128>(100020003) * 400050006;
-    check("packed product", to_string(prod2), "40013002800270018");
-    check("reduced word", to_string(redq(prod2, RedqPlan::build(5, 10000, 4))), "40003000300020003");
-
-    std::cout << "[3] full correction at p=23, q=10^6\n";
-    const RedqTrace t3 = redq_trace(parse_u128("1234005678009123004567"), RedqPlan::build(23, 1000000, 3));
-    check("rop", to_string(t3.rop), "53652420783005348024");
-    check("u", fmt(t3.u), "[15,8,18,15]");
-    check("mu", fmt(t3.mu), "[13,15,20,15]");
-
-    std::cout << "[4] degree-6 correction through three window lookups\n";
-    CorrectionTable q2 = build_correction_table(23, 1000000, 3, TableIndexing::base_p);
-    if (a.flag("inject-fault"))
-        for (u64& e : q2.entries) e ^= 1;  // a corrupted cache must be detected
-    const RedqPlan plan4 = RedqPlan::build(23, 1000000, 6);
-    SplitMix64 rng(4);
-    bool windows_ok = true;
-    u64 accesses = 0;
-    for (int it = 0; it < 500; ++it) {
-        std::vector<u64> u(7);
-        for (u64& v : u) v = rng.below(23);
-        CostReport cost;
-        if (correct_tabulated(u, q2, &cost) != correct_direct(u, plan4)) windows_ok = false;
-        accesses = cost.table_accesses;
-    }
-    check("window accesses", std::to_string(accesses), "3");
-    check("tabulated == direct", windows_ok ? "yes" : "no", "yes");
-
-    std::cout << "[5] the same reductions on the device (batched REDQ kernels)\n";
-    {
-        // random words at p=23, q=2^7, d=6 through the windowed device
-        // table (Alg. 3), against the host REDQ of each word
-        RedqPlan pd = RedqPlan::build(23, 1 << 7, 6, RedqMode::float_premul);
-        pd.attach_correction(build_correction_table(23, 1 << 7, 3, TableIndexing::base_p));
-        std::vector<double> words(4096);
-        SplitMix64 wr(5);
-        for (double& w : words) {
-            u64 r = 0;
-            for (int i = 0; i < 7; ++i) r = r * 128 + wr.below(128);
-            w = static_cast<double>(r);
+    int misses = 0;
+    for (const Exhibit& ex : exhibits) {
+        std::cout << ex.title << "\n";
+        for (const auto& [label, got, want] : ex.lines()) {
+            if (got == want) {
+                std::cout << "  ok   " << label << ": " << got << "\n";
+            } else {
+                std::cout << "  FAIL " << label << ": " << got << " (expected " << want << ")\n";
+                ++misses;
+            }
         }
-        std::vector<std::uint8_t> res(words.size() * 7);
-        gpu::redq_residues_batch(words, pd, res);
-        bool same = true;
-        for (std::size_t i = 0; i < words.size(); ++i) {
-            const std::vector<u64> mu = redq_residues(static_cast<u128>(static_cast<u64>(words[i])), pd);
-            for (int j = 0; j < 7; ++j) same &= res[i * 7 + j] == mu[j];
-        }
-        check("device residues == host", same ? "yes" : "no", "yes");
     }
-    std::cout << (bad == 0 ? "all examples reproduced\n" : "MISMATCHES FOUND\n");
-    return bad == 0 ? 0 : 4;
+    std::cout << (misses ? "MISMATCHES FOUND\n" : "all examples reproduced\n");
+    return misses ? 4 : 0;
 }
 
 int cmd_gfq(const Args& a) {
     if (!a.has("p") || !a.has("k")) throw std::invalid_argument("gfq: --p and --k are required");
-    const u64 p = a.u("p", 3), len = a.u("len", 100), size = a.u("size", 8), seed = a.u("seed", 42);
+    const u64 p = a.u("p", 3);
     const u32 k = static_cast<u32>(a.u("k", 2));
-    const std::string op = a.str("op", "dot"), csv = a.str("csv");
-    const TableIndexing idx =
-        a.str("indexing", "base_p") == "binary_shift" ? TableIndexing::binary_shift : TableIndexing::base_p;
-    const GfqField field = GfqField::build(p, k, gfq_default_q(p, k), idx);
+    const std::string op = a.str("op", "dot");
+    if (op != "dot" && op != "matmul" && !a.flag("dump-field")) throw std::domain_error("unknown --op " + op);
+    const bool shifted = a.str("indexing", "base_p") == "binary_shift";
+    const GfqField F =
+        GfqField::build(p, k, gfq_default_q(p, k), shifted ? TableIndexing::binary_shift : TableIndexing::base_p);
     if (a.flag("dump-field")) {
-        std::cout << field.describe();
+        std::cout << F.describe();
         return 0;
     }
-    SplitMix64 rng(seed);
-    auto fill = [&](Row& r, u64 n) {
-        r.p = p;
-        r.q = field.params().q;
-        r.k = k;
-        r.n = n;
-        r.n_q = field.params().n_q;
+    const CsvLog log(a.str("csv"));
+    SplitMix64 draws(a.u("seed", 42));
+    auto random_element = [&] { return F.from_index(draws.below(F.order())); };
+    // the device row and the host row of one comparison share shape and checksum rules
+    auto rows = [&](u64 n) {
+        Measurement dev;
+        dev.prime = p;
+        dev.radix = F.params().q;
+        dev.chunk = k;
+        dev.size = n;
+        dev.group = F.params().n_q;
+        Measurement host = dev;
+        dev.tag = "fgdp_b200";
+        host.tag = "naive_dot";
+        return std::pair<Measurement, Measurement>{dev, host};
+    };
+    auto field_dot = [&](auto&& lhs_at, auto&& rhs_at, u64 terms) {
+        GfqElt sum = F.zero();
+        for (u64 l = 0; l < terms; ++l) sum = F.add(sum, F.mul(lhs_at(l), rhs_at(l)));
+        return sum;
     };
     if (op == "dot") {
-        std::vector<GfqElt> v1(len), v2(len);
+        const u64 len = a.u("len", 100);
+        std::vector<GfqElt> lhs(len), rhs(len);
         for (u64 i = 0; i < len; ++i) {
-            v1[i] = field.from_index(rng.below(field.order()));
-            v2[i] = field.from_index(rng.below(field.order()));
+            lhs[i] = random_element();
+            rhs[i] = random_element();
         }
-        Row packed, naive;
-        packed.algo = "fgdp_b200";
-        naive.algo = "naive_dot";
-        u64 t0 = now_ns();
-        const GfqElt got = gpu::fgdp_dot(v1, v2, field, &packed.cost);  // K5 on the device
-        packed.wall_ns = now_ns() - t0;
-        t0 = now_ns();
-        GfqElt want = field.zero();
-        for (u64 i = 0; i < len; ++i) want = field.add(want, field.mul(v1[i], v2[i]));
-        naive.wall_ns = now_ns() - t0;
-        const std::vector<u64> gc = field.to_coeffs(got), wc = field.to_coeffs(want);
-        fill(packed, len);
-        fill(naive, len);
-        packed.checksum = fold_checksum(gc.data(), gc.size());
-        naive.checksum = fold_checksum(wc.data(), wc.size());
-        append_csv(csv, packed);
-        append_csv(csv, naive);
-        const bool agree = gc == wc;
-        const u64 expected = len == 0 ? 0 : (len + field.params().n_q - 1) / field.params().n_q;
-        std::cout << "gfq dot p=" << p << " k=" << k << " len=" << len << " divisions=" << packed.cost.divisions
-                  << " (expected " << expected << ") table_accesses=" << packed.cost.table_accesses
-                  << " agreement=" << (agree ? "ok" : "MISMATCH") << "\n";
-        return agree ? 0 : 3;
+        auto [dev, host] = rows(len);
+        const Stopwatch t_dev;
+        const GfqElt got = gpu::fgdp_dot(lhs, rhs, F, &dev.counted);  // K5 on the device
+        dev.elapsed_ns = t_dev.ns();
+        const Stopwatch t_host;
+        const GfqElt want = field_dot([&](u64 l) { return lhs[l]; }, [&](u64 l) { return rhs[l]; }, len);
+        host.elapsed_ns = t_host.ns();
+        const std::vector<u64> got_c = F.to_coeffs(got), want_c = F.to_coeffs(want);
+        dev.fnv = fold_checksum(got_c.data(), got_c.size());
+        host.fnv = fold_checksum(want_c.data(), want_c.size());
+        log.add(dev);
+        log.add(host);
+        const u64 groups = (len + F.params().n_q - 1) / F.params().n_q;
+        std::cout << "gfq dot p=" << p << " k=" << k << " len=" << len << " divisions=" << dev.counted.divisions
+                  << " (expected " << groups << ") table_accesses=" << dev.counted.table_accesses
+                  << " agreement=" << (got_c == want_c ? "ok" : "MISMATCH") << "\n";
+        return got_c == want_c ? 0 : 3;
     }
-    if (op == "matmul") {
-        GfqMatrix x = GfqMatrix::zero(field, size, size), y = GfqMatrix::zero(field, size, size);
-        for (GfqElt& e : x.data) e = field.from_index(rng.below(field.order()));
-        for (GfqElt& e : y.data) e = field.from_index(rng.below(field.order()));
-        Row packed, naive;
-        packed.algo = "fgdp_b200";
-        naive.algo = "naive_dot";
-        u64 t0 = now_ns();
-        const GfqMatrix c = gfq_matmul(x, y, field, &packed.cost);  // K1 + K4 on the device
-        packed.wall_ns = now_ns() - t0;
-        t0 = now_ns();
-        GfqMatrix want = GfqMatrix::zero(field, size, size);
-        for (u64 i = 0; i < size; ++i)
-            for (u64 j = 0; j < size; ++j) {
-                GfqElt acc = field.zero();
-                for (u64 l = 0; l < size; ++l) acc = field.add(acc, field.mul(x.at(i, l), y.at(l, j)));
-                want.at(i, j) = acc;
-            }
-        naive.wall_ns = now_ns() - t0;
-        const bool agree = c.data == want.data;
-        std::vector<u64> folded;
-        for (const GfqElt& e : want.data) folded.push_back(field.to_index(e));
-        fill(packed, size);
-        fill(naive, size);
-        packed.checksum = naive.checksum = fold_checksum(folded.data(), folded.size());
-        append_csv(csv, packed);
-        append_csv(csv, naive);
-        std::cout << "gfq matmul p=" << p << " k=" << k << " size=" << size << " divisions=" << packed.cost.divisions
-                  << " agreement=" << (agree ? "ok" : "MISMATCH") << "\n";
-        return agree ? 0 : 3;
-    }
-    throw std::domain_error("unknown --op " + op);
+    const u64 side = a.u("size", 8);
+    GfqMatrix lhs = GfqMatrix::zero(F, side, side), rhs = GfqMatrix::zero(F, side, side);
+    for (GfqMatrix* mat : {&lhs, &rhs})
+        for (GfqElt& e : mat->data) e = random_element();
+    auto [dev, host] = rows(side);
+    const Stopwatch t_dev;
+    const GfqMatrix got = gfq_matmul(lhs, rhs, F, &dev.counted);  // K1 + K4 on the device
+    dev.elapsed_ns = t_dev.ns();
+    const Stopwatch t_host;
+    std::vector<u64> want_index;
+    bool agree = true;
+    for (u64 i = 0; i < side; ++i)
+        for (u64 j = 0; j < side; ++j) {
+            const GfqElt e = field_dot([&](u64 l) { return lhs.at(i, l); }, [&](u64 l) { return rhs.at(l, j); }, side);
+            agree = agree && got.at(i, j) == e;
+            want_index.push_back(F.to_index(e));
+        }
+    host.elapsed_ns = t_host.ns();
+    dev.fnv = host.fnv = fold_checksum(want_index.data(), want_index.size());
+    log.add(dev);
+    log.add(host);
+    std::cout << "gfq matmul p=" << p << " k=" << k << " size=" << side << " divisions=" << dev.counted.divisions
+              << " agreement=" << (agree ? "ok" : "MISMATCH") << "\n";
+    return agree ? 0 : 3;
 }
 
 const char* kUsage =
