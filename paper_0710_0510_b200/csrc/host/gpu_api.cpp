@@ -579,7 +579,12 @@ void polymul_host(PolymulPlan& pl, const uint8_t* a, const uint8_t* b, u64 n, ui
     std::lock_guard<std::mutex> lock(dp.mu);
     if (!dp.staging) dp.staging = std::make_unique<Staging>();
     Staging& S = *dp.staging;
-    const u64 k = pl.params.k, ko = 2 * k - 1, chunk = u64(1) << 22;
+    // up to 2^22 pairs per chunk; a batch smaller than four such chunks is cut
+    // in four (64 Ki granules) so the D2H of one quarter still overlaps the
+    // H2D of the next (C1's 2^20 pairs: one serial H2D + kernel + D2H before)
+    const u64 k = pl.params.k, ko = 2 * k - 1;
+    u64 chunk = std::clamp<u64>((n / 4 + 0xffff) & ~u64(0xffff), u64(1) << 16, u64(1) << 22);
+    if (const char* e = std::getenv("QPK_PM_CHUNK_LOG2")) chunk = u64(1) << std::clamp(std::atoi(e), 12, 22);  // dev knob
     for (int sl = 0; sl < Staging::kSlots; ++sl) {
         S.in0[sl].ensure(chunk * k);
         S.in1[sl].ensure(chunk * k);
