@@ -38,6 +38,10 @@ constexpr int kGemvThreads = 256;
 #define QPK_GEMV_UNROLL 4
 #endif
 constexpr int kGemvUnroll = QPK_GEMV_UNROLL;  // 16-byte loads of A in flight per lane
+#ifndef QPK_GEMV_UNROLL_X
+#define QPK_GEMV_UNROLL_X 4
+#endif
+constexpr int kGemvUnrollX = QPK_GEMV_UNROLL_X;  // ... of A and of x each, when x is streamed too (few rows)
 constexpr uint32_t kReplMax = 64;  // replicate the value table up to this order (8 KB)
 constexpr uint64_t kXrepRows = 4;  // up to this many rows x is looked up per use
 
@@ -142,10 +146,10 @@ __global__ void __launch_bounds__(kGemvThreads) gfq_gemv_kernel(const GfqGemvPar
                 acc = 0;
                 cnt = 0;
             };
-            auto four = [&](const uint4& a, uint64_t j) {
+            // XREP: b = the x vector of the same position, streamed like A
+            auto four = [&](const uint4& a, uint64_t j, const uint4& b) {
                 V xs[4];
                 if constexpr (XREP) {
-                    const uint4 b = ldg_stream(xr + j);  // few rows: x is streamed too
                     seen(b);
                     xs[0] = val(b.x), xs[1] = val(b.y), xs[2] = val(b.z), xs[3] = val(b.w);
                 } else if constexpr (INT) {
@@ -169,29 +173,46 @@ __global__ void __launch_bounds__(kGemvThreads) gfq_gemv_kernel(const GfqGemvPar
                 }
             };
             if constexpr (VEC) {
+                constexpr int U = XREP ? kGemvUnrollX : kGemvUnroll;
                 // k0 and Kd are multiples of 4: every 16-byte vector is whole.
-                // Software pipelined: the next kGemvUnroll vectors of A are in
+                // Software pipelined: the next U vectors of A are in
                 // flight while the current ones are multiplied.
-                constexpr uint64_t kStep = 128 * kGemvUnroll;
+                constexpr uint64_t kStep = 128 * U;
                 uint64_t j = k0 + 4 * lane;
+                // (few rows: x is streamed too, one step ahead like A -- loaded at
+                // its use, every step waited a full DRAM round trip for it)
+                constexpr int XU = XREP ? U : 1;
+                const uint4 none = make_uint4(0, 0, 0, 0);
                 if (j + kStep - 128 < k1) {
-                    uint4 cur[kGemvUnroll];
+                    uint4 cur[U], xcur[XU];
 #pragma unroll
-                    for (int u = 0; u < kGemvUnroll; ++u) cur[u] = ldg_stream(arow + j + 128 * u);
+                    for (int u = 0; u < U; ++u) cur[u] = ldg_stream(arow + j + 128 * u);
+                    if constexpr (XREP) {
+#pragma unroll
+                        for (int u = 0; u < U; ++u) xcur[u] = ldg_stream(xr + j + 128 * u);
+                    }
                     for (; j + 2 * kStep - 128 < k1; j += kStep) {
-                        uint4 nxt[kGemvUnroll];
+                        uint4 nxt[U], xnxt[XU];
 #pragma unroll
-                        for (int u = 0; u < kGemvUnroll; ++u) nxt[u] = ldg_stream(arow + j + kStep + 128 * u);
+                        for (int u = 0; u < U; ++u) nxt[u] = ldg_stream(arow + j + kStep + 128 * u);
+                        if constexpr (XREP) {
 #pragma unroll
-                        for (int u = 0; u < kGemvUnroll; ++u) four(cur[u], j + 128 * u);
+                            for (int u = 0; u < U; ++u) xnxt[u] = ldg_stream(xr + j + kStep + 128 * u);
+                        }
 #pragma unroll
-                        for (int u = 0; u < kGemvUnroll; ++u) cur[u] = nxt[u];
+                        for (int u = 0; u < U; ++u) four(cur[u], j + 128 * u, XREP ? xcur[u] : none);
+#pragma unroll
+                        for (int u = 0; u < U; ++u) cur[u] = nxt[u];
+                        if constexpr (XREP) {
+#pragma unroll
+                            for (int u = 0; u < U; ++u) xcur[u] = xnxt[u];
+                        }
                     }
 #pragma unroll
-                    for (int u = 0; u < kGemvUnroll; ++u) four(cur[u], j + 128 * u);
+                    for (int u = 0; u < U; ++u) four(cur[u], j + 128 * u, XREP ? xcur[u] : none);
                     j += kStep;
                 }
-                for (; j < k1; j += 128) four(ldg_stream(arow + j), j);
+                for (; j < k1; j += 128) four(ldg_stream(arow + j), j, XREP ? ldg_stream(xr + j) : none);
             } else {
                 for (uint64_t j = k0 + lane; j < k1; j += 32) {
                     emax = max(emax, arow[j]);
