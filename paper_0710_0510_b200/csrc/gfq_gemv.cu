@@ -43,7 +43,10 @@ constexpr int kGemvUnroll = QPK_GEMV_UNROLL;  // 16-byte loads of A in flight pe
 #endif
 constexpr int kGemvUnrollX = QPK_GEMV_UNROLL_X;  // ... of A and of x each, when x is streamed too (few rows)
 constexpr uint32_t kReplMax = 64;  // replicate the value table up to this order (8 KB)
-constexpr uint64_t kXrepRows = 4;  // up to this many rows x is looked up per use
+#ifndef QPK_XREP_ROWS
+#define QPK_XREP_ROWS 4
+#endif
+constexpr uint64_t kXrepRows = QPK_XREP_ROWS;  // up to this many rows x is looked up per use
 
 __device__ __forceinline__ uint4 ldg_stream(const uint32_t* p) {
     uint4 v;
