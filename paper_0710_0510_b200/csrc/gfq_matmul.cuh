@@ -284,7 +284,7 @@ __device__ __forceinline__ uint32_t acc_to_coeffs(const K& c, uint32_t lh_radix,
 #endif
 // (9 warps: one SM sub-partition holds 3 of them, so 16384 / (3 * 32) caps
 // the kernel at 168 registers per thread)
-template <int KR, class K, bool REDQ_STAGE, int NST, bool FOLD>
+template <int KR, class K, bool REDQ_STAGE, int NST, bool FOLD, bool PAIR>
 __global__ void __launch_bounds__(THREADS, 1)
     gfq_matmul_kernel(const GfqMatmulParams P, const double* __restrict__ at, const double* __restrict__ bm,
                       uint64_t m, uint64_t n, uint64_t K_pad, uint64_t m_pad, uint64_t n_pad,
@@ -370,14 +370,31 @@ __global__ void __launch_bounds__(THREADS, 1)
             }
     };
     // 4 MMA k-steps of one stage; per step 8 A and 4 B fragments -> 32 DMMA
+    // PAIR: the workspaces hold a thread's fragments 2t, 2t+1 next to each
+    // other (kernels.hpp mm_col_a / mm_col_b): one 16-byte load for two
     auto mma_kstep = [&](const double* sa, const double* sb, int kk) {
-        const double* pa = sa + (kk * 4 + lc4) * LDS_ + wm + lr;
-        const double* pb = sb + (kk * 4 + lc4) * LDS_ + wn + lr;
         double af[MT], bf[NT];
+        if constexpr (PAIR) {
+            const double2* pa = reinterpret_cast<const double2*>(sa + (kk * 4 + lc4) * LDS_ + wm + 2 * lr);
+            const double2* pb = reinterpret_cast<const double2*>(sb + (kk * 4 + lc4) * LDS_ + wn + 2 * lr);
 #pragma unroll
-        for (int i = 0; i < MT; ++i) af[i] = pa[i * 8];
+            for (int t = 0; t < MT / 2; ++t) {
+                const double2 v = pa[8 * t];
+                af[2 * t] = v.x, af[2 * t + 1] = v.y;
+            }
 #pragma unroll
-        for (int j = 0; j < NT; ++j) bf[j] = pb[j * 8];
+            for (int t = 0; t < NT / 2; ++t) {
+                const double2 v = pb[8 * t];
+                bf[2 * t] = v.x, bf[2 * t + 1] = v.y;
+            }
+        } else {
+            const double* pa = sa + (kk * 4 + lc4) * LDS_ + wm + lr;
+            const double* pb = sb + (kk * 4 + lc4) * LDS_ + wn + lr;
+#pragma unroll
+            for (int i = 0; i < MT; ++i) af[i] = pa[i * 8];
+#pragma unroll
+            for (int j = 0; j < NT; ++j) bf[j] = pb[j * 8];
+        }
 #pragma unroll
         for (int i = 0; i < MT; ++i)
 #pragma unroll
@@ -471,26 +488,21 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
 }
 
-template <int KR, class K, bool REDQ_STAGE, int NST = 4, bool FOLD = false>
+template <int KR, class K, bool REDQ_STAGE, int NST = 4, bool FOLD = false, bool PAIR = false>
 cudaError_t run_matmul_t(const GfqMatmulParams& P, const double* at, const double* b, uint64_t m, uint64_t n,
                          uint64_t K_pad, uint64_t m_pad, uint64_t n_pad, uint8_t* oc, uint32_t* orp, cudaStream_t s) {
     uint32_t nlh = 1;
     for (int i = 0; i < KR; ++i) nlh *= P.lh_radix;
     const size_t smem = smem_bytes(NST) + size_t(2 * nlh + P.order) * 4;
     if (smem > 227 * 1024) return cudaErrorInvalidValue;
-    if (cudaError_t e = ensure_dyn_smem(reinterpret_cast<const void*>(gfq_matmul_kernel<KR, K, REDQ_STAGE, NST, FOLD>),
+    if (cudaError_t e = ensure_dyn_smem(reinterpret_cast<const void*>(gfq_matmul_kernel<KR, K, REDQ_STAGE, NST, FOLD, PAIR>),
                                         smem);
         e != cudaSuccess)
         return e;
     dim3 grid(static_cast<unsigned>(n_pad / BN), static_cast<unsigned>(m_pad / BM));
-    gfq_matmul_kernel<KR, K, REDQ_STAGE, NST, FOLD><<<grid, THREADS, smem, s>>>(P, at, b, m, n, K_pad, m_pad, n_pad,
+    gfq_matmul_kernel<KR, K, REDQ_STAGE, NST, FOLD, PAIR><<<grid, THREADS, smem, s>>>(P, at, b, m, n, K_pad, m_pad, n_pad,
                                                                                 oc, orp);
     return cudaGetLastError();
-}
-
-// a plan is "safe" when every accumulated word stays <= min(r_max, 2^52)
-inline bool mm_plan_safe(const RedqParams& R) {
-    return R.qbits && R.limit <= R.r_max + 1.0 && R.limit <= kTwo52;
 }
 
 // VARIANT 1: compile-time fast paths for the benchmark fields (C4 GF(3^2)
@@ -506,11 +518,15 @@ cudaError_t run_matmul(const GfqMatmulParams& P, const double* at, const double*
                 return run_matmul_t<2, CtConst<3, 16>, true, 6>(P, at, b, m, n, K_pad, m_pad, n_pad, oc, orp, s);
         }
         if constexpr (KR == 3) {
-            if (P.p == 3 && P.rq.qbits == 10 && mm_plan_safe(P.rq) && stage_ok)
+            if (P.p == 3 && P.rq.qbits == 10 && mm_plan_safe(P.rq) && stage_ok) {
+                // the workspaces were packed for the kernel mm_pair_layout names
+                if ((P.repack != kRepackFold) != mm_pair_layout(P)) return cudaErrorInvalidValue;
                 return P.repack == kRepackFold
                            ? run_matmul_t<3, CtConst<3, 10>, true, 6, true>(P, at, b, m, n, K_pad, m_pad, n_pad, oc,
                                                                             orp, s)
-                           : run_matmul_t<3, CtConst<3, 10>, true, 6>(P, at, b, m, n, K_pad, m_pad, n_pad, oc, orp, s);
+                           : run_matmul_t<3, CtConst<3, 10>, true, 6, false, true>(P, at, b, m, n, K_pad, m_pad, n_pad,
+                                                                                   oc, orp, s);
+            }
         }
         return cudaErrorNotSupported;
     } else {

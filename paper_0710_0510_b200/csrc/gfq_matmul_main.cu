@@ -69,7 +69,7 @@ __global__ void reps_to_coeffs_kernel(uint32_t k, const uint32_t* __restrict__ a
 // vector loads).
 template <int KR>
 __global__ void pack_coeffs_kernel(uint32_t p, double qd, const uint8_t* __restrict__ src, uint64_t rows,
-                                   uint64_t cols, double* __restrict__ dst, uint64_t ld, bool transpose) {
+                                   uint64_t cols, double* __restrict__ dst, uint64_t ld, bool transpose, bool pair) {
     __shared__ double tile[32][33];
     const uint64_t r0 = uint64_t(blockIdx.y) * 32, c0 = uint64_t(blockIdx.x) * 32;
     const int tx = threadIdx.x, ty = threadIdx.y;
@@ -125,17 +125,17 @@ __global__ void pack_coeffs_kernel(uint32_t p, double qd, const uint8_t* __restr
     for (int i = ty; i < 32; i += 8) {
         if (transpose) {
             const uint64_t c = c0 + i, r = r0 + tx;
-            if (r < rows && c < cols) dst[c * ld + r] = tile[tx][i];
+            if (r < rows && c < cols) dst[c * ld + (pair ? mm_col_a(r) : r)] = tile[tx][i];
         } else {
             const uint64_t r = r0 + i, c = c0 + tx;
-            if (r < rows && c < cols) dst[r * ld + c] = tile[i][tx];
+            if (r < rows && c < cols) dst[r * ld + (pair ? mm_col_b(c) : c)] = tile[i][tx];
         }
     }
 }
 
 __global__ void pack_reps_kernel(const double* __restrict__ fval, uint32_t order, const uint32_t* __restrict__ src,
                                  uint64_t rows, uint64_t cols, double* __restrict__ dst, uint64_t ld, bool transpose,
-                                 uint32_t* status) {
+                                 bool pair, uint32_t* status) {
     extern __shared__ double s_fval[];
     __shared__ double tile[32][33];
     for (uint32_t i = threadIdx.y * 32 + threadIdx.x; i < order; i += 256) s_fval[i] = fval[i];
@@ -158,10 +158,10 @@ __global__ void pack_reps_kernel(const double* __restrict__ fval, uint32_t order
     for (int i = ty; i < 32; i += 8) {
         if (transpose) {
             const uint64_t c = c0 + i, r = r0 + tx;
-            if (r < rows && c < cols) dst[c * ld + r] = tile[tx][i];
+            if (r < rows && c < cols) dst[c * ld + (pair ? mm_col_a(r) : r)] = tile[tx][i];
         } else {
             const uint64_t r = r0 + i, c = c0 + tx;
-            if (r < rows && c < cols) dst[r * ld + c] = tile[i][tx];
+            if (r < rows && c < cols) dst[r * ld + (pair ? mm_col_b(c) : c)] = tile[i][tx];
         }
     }
 }
@@ -212,28 +212,29 @@ cudaError_t launch_reps_to_coeffs(uint32_t k, const uint32_t* alog, const uint32
 }
 
 cudaError_t launch_pack_coeffs(uint32_t p, uint32_t k, double qd, const uint8_t* src, uint64_t rows, uint64_t cols,
-                               double* dst, uint64_t ld, bool transpose, cudaStream_t s) {
+                               double* dst, uint64_t ld, bool transpose, bool pair_layout, cudaStream_t s) {
     if (rows == 0 || cols == 0) return cudaSuccess;
     dim3 grid(static_cast<unsigned>((cols + 31) / 32), static_cast<unsigned>((rows + 31) / 32));
     switch (k) {
-        case 1: pack_coeffs_kernel<1><<<grid, dim3(32, 8), 0, s>>>(p, qd, src, rows, cols, dst, ld, transpose); break;
-        case 2: pack_coeffs_kernel<2><<<grid, dim3(32, 8), 0, s>>>(p, qd, src, rows, cols, dst, ld, transpose); break;
-        case 3: pack_coeffs_kernel<3><<<grid, dim3(32, 8), 0, s>>>(p, qd, src, rows, cols, dst, ld, transpose); break;
-        case 4: pack_coeffs_kernel<4><<<grid, dim3(32, 8), 0, s>>>(p, qd, src, rows, cols, dst, ld, transpose); break;
+        case 1: pack_coeffs_kernel<1><<<grid, dim3(32, 8), 0, s>>>(p, qd, src, rows, cols, dst, ld, transpose, pair_layout); break;
+        case 2: pack_coeffs_kernel<2><<<grid, dim3(32, 8), 0, s>>>(p, qd, src, rows, cols, dst, ld, transpose, pair_layout); break;
+        case 3: pack_coeffs_kernel<3><<<grid, dim3(32, 8), 0, s>>>(p, qd, src, rows, cols, dst, ld, transpose, pair_layout); break;
+        case 4: pack_coeffs_kernel<4><<<grid, dim3(32, 8), 0, s>>>(p, qd, src, rows, cols, dst, ld, transpose, pair_layout); break;
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();
 }
 
 cudaError_t launch_pack_reps(const double* fval, uint32_t order, const uint32_t* src, uint64_t rows, uint64_t cols,
-                             double* dst, uint64_t ld, bool transpose, uint32_t* status, cudaStream_t s) {
+                             double* dst, uint64_t ld, bool transpose, bool pair_layout, uint32_t* status,
+                             cudaStream_t s) {
     if (rows == 0 || cols == 0) return cudaSuccess;
     dim3 grid(static_cast<unsigned>((cols + 31) / 32), static_cast<unsigned>((rows + 31) / 32));
     const size_t smem = size_t(order) * 8;
     if (smem > 200 * 1024) return cudaErrorInvalidValue;
     if (cudaError_t e = ensure_dyn_smem(reinterpret_cast<const void*>(pack_reps_kernel), smem); e != cudaSuccess)
         return e;
-    pack_reps_kernel<<<grid, dim3(32, 8), smem, s>>>(fval, order, src, rows, cols, dst, ld, transpose, status);
+    pack_reps_kernel<<<grid, dim3(32, 8), smem, s>>>(fval, order, src, rows, cols, dst, ld, transpose, pair_layout, status);
     return cudaGetLastError();
 }
 

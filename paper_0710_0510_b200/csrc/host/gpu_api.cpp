@@ -925,21 +925,26 @@ void gfq_matmul_device(DeviceFieldCache& F, const GfqField& field, const void* A
     auto* bt = wb.as<double>();
     if (mp != m || kp != K) check(cudaMemsetAsync(at, 0, kp * mp * 8, s), "memset");
     if (np != n || kp != K) check(cudaMemsetAsync(bt, 0, kp * np * 8, s), "memset");
-    if (reps) {
-        uint32_t* st = F.status.as<uint32_t>();
-        check(qpk::launch_pack_reps(F.mm.fval, F.mm.order, static_cast<const uint32_t*>(A), m, K, at, mp, true, st, s),
-              "pack A");
-        check(qpk::launch_pack_reps(F.mm.fval, F.mm.order, static_cast<const uint32_t*>(B), K, n, bt, np, false, st, s),
-              "pack B");
-    } else {
-        check(qpk::launch_pack_coeffs(F.mm.p, F.mm.k, F.mm.qd, static_cast<const uint8_t*>(A), m, K, at, mp, true, s),
-              "pack A");
-        check(qpk::launch_pack_coeffs(F.mm.p, F.mm.k, F.mm.qd, static_cast<const uint8_t*>(B), K, n, bt, np, false, s),
-              "pack B");
-    }
     qpk::GfqMatmulParams M = F.mm;
     M.chunk = resolve_chunk(F, field, K, chunk, repack);
     M.repack = M.chunk ? repack : qpk::kRepackRedq;
+    const bool pair = qpk::mm_pair_layout(M);  // the column order the kernel this launch selects reads
+    if (reps) {
+        uint32_t* st = F.status.as<uint32_t>();
+        check(qpk::launch_pack_reps(F.mm.fval, F.mm.order, static_cast<const uint32_t*>(A), m, K, at, mp, true, pair,
+                                    st, s),
+              "pack A");
+        check(qpk::launch_pack_reps(F.mm.fval, F.mm.order, static_cast<const uint32_t*>(B), K, n, bt, np, false, pair,
+                                    st, s),
+              "pack B");
+    } else {
+        check(qpk::launch_pack_coeffs(F.mm.p, F.mm.k, F.mm.qd, static_cast<const uint8_t*>(A), m, K, at, mp, true, pair,
+                                      s),
+              "pack A");
+        check(qpk::launch_pack_coeffs(F.mm.p, F.mm.k, F.mm.qd, static_cast<const uint8_t*>(B), K, n, bt, np, false,
+                                      pair, s),
+              "pack B");
+    }
     check(qpk::launch_gfq_matmul(M, at, bt, m, n, kp, mp, np, reps ? nullptr : static_cast<uint8_t*>(C),
                                  reps ? static_cast<uint32_t*>(C) : nullptr, s),
           "gfq_matmul launch");

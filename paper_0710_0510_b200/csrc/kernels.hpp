@@ -191,8 +191,11 @@ cudaError_t launch_gfq_mul_rep(uint32_t group, const uint32_t* a, const uint32_t
 // DQT pack of coefficient records into q-adic doubles (K1a): src is
 // rows x cols x k bytes; dst element (r, c) goes to dst[c*ld + r] when
 // `transpose`, else dst[r*ld + c].  dst must be pre-zeroed for padding.
+// pair_layout: K4 fragment column order (mm_col_a for the transposed operand A,
+// mm_col_b for B)
 cudaError_t launch_pack_coeffs(uint32_t p, uint32_t k, double qd, const uint8_t* src, uint64_t rows,
-                               uint64_t cols, double* dst, uint64_t ld, bool transpose, cudaStream_t s);
+                               uint64_t cols, double* dst, uint64_t ld, bool transpose, bool pair_layout,
+                               cudaStream_t s);
 // Zech/dlog tabulated pack (K1b): reps -> float_eval(rep) via a smem table;
 // reps >= order are packed as zero and latch kErrRep in *status.
 // layout helpers of the GEMV-column matmul route (fields whose n_q is below
@@ -204,11 +207,41 @@ cudaError_t launch_coeffs_to_reps(uint32_t p, uint32_t k, const uint32_t* log, c
 cudaError_t launch_reps_to_coeffs(uint32_t k, const uint32_t* alog, const uint32_t* src, uint64_t n, uint8_t* dst,
                                   cudaStream_t s);
 cudaError_t launch_pack_reps(const double* fval, uint32_t order, const uint32_t* src, uint64_t rows,
-                             uint64_t cols, double* dst, uint64_t ld, bool transpose, uint32_t* status,
-                             cudaStream_t s);
+                             uint64_t cols, double* dst, uint64_t ld, bool transpose, bool pair_layout,
+                             uint32_t* status, cudaStream_t s);
+
+// Column order of the K4 operand workspaces when mm_pair_layout(P) holds (the
+// C5 fast path with the canonical re-pack).  A thread of the fp64 MMA takes
+// the elements 8 i + lr of its warp's 64 rows of A^T (i = 0..7) and of its
+// warp's 32 columns of B (i = 0..3).  Inside every 64-block of A^T columns
+// and every 32-block of B columns, element 8 i + lr is stored at
+// 16 (i / 2) + 2 lr + (i % 2): a thread's fragment pairs are adjacent (one
+// 16-byte shared load for two fragments: 6 loads per k-step instead of 12)
+// and the eight lanes of a quarter warp read eight different 16-byte bank
+// groups (row stride 132 doubles == 32 bytes mod 128).  Every instruction
+// next to the DMMAs costs a dispatch slot: C5 37.10 ->
+// 36.54 ms.  Not used by the other K4 kernels: at the 168-register cap the
+// aligned register quads of the 16-byte loads make ptxas spill in the fold
+// kernel (33.0 -> 36.4 ms) and gain nothing for C4.
+__host__ __device__ constexpr uint64_t mm_col_a(uint64_t x) {
+    return (x & ~uint64_t(63)) | (((x >> 4) & 3) << 4) | ((x & 7) << 1) | ((x >> 3) & 1);
+}
+__host__ __device__ constexpr uint64_t mm_col_b(uint64_t x) {
+    return (x & ~uint64_t(31)) | (((x >> 4) & 1) << 4) | ((x & 7) << 1) | ((x >> 3) & 1);
+}
+// a plan is "safe" when every accumulated word stays <= min(r_max, 2^52)
+inline bool mm_plan_safe(const RedqParams& R) {
+    return R.qbits && R.limit <= R.r_max + 1.0 && R.limit <= 4503599627370496.0;
+}
+// the launch that takes the paired column order (P with chunk and repack resolved)
+inline bool mm_pair_layout(const GfqMatmulParams& P) {
+    return P.k == 3 && P.p == 3 && P.rq.qbits == 10 && mm_plan_safe(P.rq) &&
+           (P.chunk == 0 || P.chunk % kMatmulBK == 0) && P.repack != kRepackFold;
+}
 
 // K4: C = A*B on packed operands.  at is K x m_pad (A transposed), b is
-// K x n_pad, both zero padded (m_pad, n_pad multiples of 128, K_pad of 16).
+// K x n_pad, both zero padded (m_pad, n_pad multiples of 128, K_pad of 16),
+// packed with pair_layout = mm_pair_layout(P).
 // Output either coefficient bytes (m x n x k) or reps (m x n u32).
 cudaError_t launch_gfq_matmul(const GfqMatmulParams& P, const double* at, const double* b, uint64_t m,
                               uint64_t n, uint64_t K_pad, uint64_t m_pad, uint64_t n_pad, uint8_t* out_coeffs,
