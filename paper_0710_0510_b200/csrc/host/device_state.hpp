@@ -67,6 +67,8 @@ struct StreamBuf {
 struct Staging {
     static constexpr int kSlots = 4;
     cudaStream_t sh = nullptr, sk = nullptr, sd = nullptr;
+    cudaStream_t sk2 = nullptr;  // second compute stream (row bands of a matrix product alternate)
+    cudaEvent_t ev_aux = nullptr;
     cudaEvent_t ev_in[kSlots] = {}, ev_k[kSlots] = {}, ev_out[kSlots] = {};
     DevBuf in0[kSlots], in1[kSlots], out[kSlots];
     Staging();

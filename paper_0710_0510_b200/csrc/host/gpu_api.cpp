@@ -63,7 +63,9 @@ StreamBuf::~StreamBuf() {
 }
 
 Staging::Staging() {
-    for (cudaStream_t* s : {&sh, &sk, &sd}) check(cudaStreamCreateWithFlags(s, cudaStreamNonBlocking), "cudaStreamCreate");
+    for (cudaStream_t* s : {&sh, &sk, &sd, &sk2})
+        check(cudaStreamCreateWithFlags(s, cudaStreamNonBlocking), "cudaStreamCreate");
+    check(cudaEventCreateWithFlags(&ev_aux, cudaEventDisableTiming), "cudaEventCreate");
     for (int i = 0; i < kSlots; ++i)
         for (cudaEvent_t* e : {&ev_in[i], &ev_k[i], &ev_out[i]})
             check(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "cudaEventCreate");
@@ -73,7 +75,8 @@ Staging::~Staging() {
     for (int i = 0; i < kSlots; ++i)
         for (cudaEvent_t e : {ev_in[i], ev_k[i], ev_out[i]})
             if (e) cudaEventDestroy(e);
-    for (cudaStream_t s : {sh, sk, sd})
+    if (ev_aux) cudaEventDestroy(ev_aux);
+    for (cudaStream_t s : {sh, sk, sd, sk2})
         if (s) cudaStreamDestroy(s);
 }
 
@@ -894,8 +897,47 @@ void gfq_matmul_by_columns(DeviceFieldCache& F, const GfqField& field, const voi
     }
 }
 
+namespace {
+
+// the fp64 MMA route of gfq_matmul (else: rep-domain or per-column GEMVs)
+bool matmul_mma_route(const DeviceFieldCache& F, const GfqField& field, u64 K) {
+    if (F.wide) return false;
+    const u64 p = field.p(), unit = field.k() * (p - 1) * (p - 1), q = field.params().q;
+    const u64 safe = unit ? (q - 1 - (p - 1)) / unit : K;
+    return !(K > field.params().n_q && safe < 4);
+}
+
+// kernel parameters of one launch (chunk and re-pack resolved)
+qpk::GfqMatmulParams matmul_params(const DeviceFieldCache& F, const GfqField& field, u64 K, uint32_t chunk,
+                                   uint32_t repack) {
+    qpk::GfqMatmulParams M = F.mm;
+    M.chunk = resolve_chunk(F, field, K, chunk, repack);
+    M.repack = M.chunk ? repack : qpk::kRepackRedq;
+    return M;
+}
+
+// operand B (K x n records or reps) -> the K4 workspace bt (kp x np doubles)
+void matmul_pack_b(DeviceFieldCache& F, const qpk::GfqMatmulParams& M, const void* B, u64 K, u64 n, bool reps,
+                   double* bt, cudaStream_t s) {
+    const u64 np = round_up(n, 128), kp = round_up(std::max<u64>(K, 1), 16);
+    const bool pair = qpk::mm_pair_layout(M);
+    if (np != n || kp != K) check(cudaMemsetAsync(bt, 0, kp * np * 8, s), "memset");
+    if (reps)
+        check(qpk::launch_pack_reps(F.mm.fval, F.mm.order, static_cast<const uint32_t*>(B), K, n, bt, np, false, pair,
+                                    F.status.as<uint32_t>(), s),
+              "pack B");
+    else
+        check(qpk::launch_pack_coeffs(F.mm.p, F.mm.k, F.mm.qd, static_cast<const uint8_t*>(B), K, n, bt, np, false,
+                                      pair, s),
+              "pack B");
+}
+
+}  // namespace
+
+// packed_b: operand B already in the K4 workspace form (matmul_pack_b with
+// the same field, K, chunk and repack), shared by the row bands of one product
 void gfq_matmul_device(DeviceFieldCache& F, const GfqField& field, const void* A, const void* B, u64 m, u64 K, u64 n,
-                       uint32_t chunk, void* C, bool reps, cudaStream_t s, uint32_t repack) {
+                       uint32_t chunk, void* C, bool reps, cudaStream_t s, uint32_t repack, const double* packed_b) {
     if (m == 0 || n == 0) return;
     if (!reps) require_byte_coeffs(F);
     if (F.wide) {
@@ -920,30 +962,23 @@ void gfq_matmul_device(DeviceFieldCache& F, const GfqField& field, const void* A
         }
     }
     const u64 mp = round_up(m, 128), np = round_up(n, 128), kp = round_up(std::max<u64>(K, 1), 16);
-    StreamBuf wa(kp * mp * 8, s), wb(kp * np * 8, s);
+    StreamBuf wa(kp * mp * 8, s), wb(packed_b ? 0 : kp * np * 8, s);
     auto* at = wa.as<double>();
-    auto* bt = wb.as<double>();
-    if (mp != m || kp != K) check(cudaMemsetAsync(at, 0, kp * mp * 8, s), "memset");
-    if (np != n || kp != K) check(cudaMemsetAsync(bt, 0, kp * np * 8, s), "memset");
-    qpk::GfqMatmulParams M = F.mm;
-    M.chunk = resolve_chunk(F, field, K, chunk, repack);
-    M.repack = M.chunk ? repack : qpk::kRepackRedq;
+    const qpk::GfqMatmulParams M = matmul_params(F, field, K, chunk, repack);
     const bool pair = qpk::mm_pair_layout(M);  // the column order the kernel this launch selects reads
-    if (reps) {
-        uint32_t* st = F.status.as<uint32_t>();
+    if (mp != m || kp != K) check(cudaMemsetAsync(at, 0, kp * mp * 8, s), "memset");
+    if (reps)
         check(qpk::launch_pack_reps(F.mm.fval, F.mm.order, static_cast<const uint32_t*>(A), m, K, at, mp, true, pair,
-                                    st, s),
+                                    F.status.as<uint32_t>(), s),
               "pack A");
-        check(qpk::launch_pack_reps(F.mm.fval, F.mm.order, static_cast<const uint32_t*>(B), K, n, bt, np, false, pair,
-                                    st, s),
-              "pack B");
-    } else {
+    else
         check(qpk::launch_pack_coeffs(F.mm.p, F.mm.k, F.mm.qd, static_cast<const uint8_t*>(A), m, K, at, mp, true, pair,
                                       s),
               "pack A");
-        check(qpk::launch_pack_coeffs(F.mm.p, F.mm.k, F.mm.qd, static_cast<const uint8_t*>(B), K, n, bt, np, false,
-                                      pair, s),
-              "pack B");
+    const double* bt = packed_b;
+    if (!bt) {
+        matmul_pack_b(F, M, B, K, n, reps, wb.as<double>(), s);
+        bt = wb.as<double>();
     }
     check(qpk::launch_gfq_matmul(M, at, bt, m, n, kp, mp, np, reps ? nullptr : static_cast<uint8_t*>(C),
                                  reps ? static_cast<uint32_t*>(C) : nullptr, s),
@@ -957,10 +992,57 @@ void gfq_matmul_host(DeviceFieldCache& F, const GfqField& field, const void* A, 
     auto* da = F.io_a.ensure(m * K * es);
     auto* db = F.io_b.ensure(K * n * es);
     auto* dc = F.io_c.ensure(m * n * es);
-    check(cudaMemcpy(da, A, m * K * es, cudaMemcpyHostToDevice), "H2D");
-    check(cudaMemcpy(db, B, K * n * es, cudaMemcpyHostToDevice), "H2D");
-    gfq_matmul_device(F, field, da, db, m, K, n, chunk, dc, reps, 0, repack);
-    check(cudaMemcpy(C, dc, m * n * es, cudaMemcpyDeviceToHost), "D2H");
+    // Large products on the MMA route run as row bands of A and C: B goes up
+    // and is packed once, then band i's rows of A go up while band i-1
+    // multiplies and band i-2's rows of C come back (streams chained by
+    // events) -- the copies of all but the first and last band hide behind
+    // the contraction.  Consecutive bands run on two alternating compute
+    // streams so a band's last, partly filled wave of tiles overlaps the next
+    // band's first.  Small or other-route products: copy, multiply, copy.
+    const u64 bands = (matmul_mma_route(F, field, K) && K && m >= 1024 && m * K * es >= (u64(16) << 20))
+                          ? std::min<u64>(8, m / 512)
+                          : 1;
+    if (bands > 1) {
+        if (!F.staging) F.staging = std::make_unique<Staging>();
+        Staging& S = *F.staging;
+        const u64 np = round_up(n, 128), kp = round_up(K, 16);
+        const qpk::GfqMatmulParams M = matmul_params(F, field, K, chunk, repack);
+        StreamBuf bt(kp * np * 8, S.sk);
+        check(cudaMemcpyAsync(db, B, K * n * es, cudaMemcpyHostToDevice, S.sh), "H2D");
+        check(cudaEventRecord(S.ev_in[0], S.sh), "event");
+        check(cudaStreamWaitEvent(S.sk, S.ev_in[0], 0), "wait B");
+        matmul_pack_b(F, M, db, K, n, reps, bt.as<double>(), S.sk);
+        check(cudaEventRecord(S.ev_aux, S.sk), "event");
+        check(cudaStreamWaitEvent(S.sk2, S.ev_aux, 0), "wait packed B");
+        const u64 rows_per = round_up((m + bands - 1) / bands, 128);
+        auto* a8 = static_cast<uint8_t*>(da);
+        auto* c8 = static_cast<uint8_t*>(dc);
+        for (u64 r0 = 0, i = 0; r0 < m; r0 += rows_per, ++i) {
+            const u64 rows = std::min(rows_per, m - r0);
+            const int sl = static_cast<int>(i % Staging::kSlots);
+            check(cudaMemcpyAsync(a8 + r0 * K * es, static_cast<const uint8_t*>(A) + r0 * K * es, rows * K * es,
+                                  cudaMemcpyHostToDevice, S.sh),
+                  "H2D");
+            check(cudaEventRecord(S.ev_in[sl], S.sh), "event");
+            const cudaStream_t ks = (i & 1) ? S.sk2 : S.sk;
+            check(cudaStreamWaitEvent(ks, S.ev_in[sl], 0), "wait A band");
+            gfq_matmul_device(F, field, a8 + r0 * K * es, db, rows, K, n, chunk, c8 + r0 * n * es, reps, ks, repack,
+                              bt.as<double>());
+            check(cudaEventRecord(S.ev_k[sl], ks), "event");
+            check(cudaStreamWaitEvent(S.sd, S.ev_k[sl], 0), "wait band");
+            check(cudaMemcpyAsync(static_cast<uint8_t*>(C) + r0 * n * es, c8 + r0 * n * es, rows * n * es,
+                                  cudaMemcpyDeviceToHost, S.sd),
+                  "D2H");
+        }
+        check(cudaStreamSynchronize(S.sd), "sync");
+        check(cudaStreamSynchronize(S.sk), "sync");
+        check(cudaStreamSynchronize(S.sk2), "sync");
+    } else {
+        check(cudaMemcpy(da, A, m * K * es, cudaMemcpyHostToDevice), "H2D");
+        check(cudaMemcpy(db, B, K * n * es, cudaMemcpyHostToDevice), "H2D");
+        gfq_matmul_device(F, field, da, db, m, K, n, chunk, dc, reps, 0, repack);
+        check(cudaMemcpy(C, dc, m * n * es, cudaMemcpyDeviceToHost), "D2H");
+    }
     if (reps) raise_field_status(take_field_status(F, 0));
     if (zech_reads && m && n && K) {
         // the reference's data-dependent counter part (K7), on rep operands

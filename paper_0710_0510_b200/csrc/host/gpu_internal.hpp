@@ -60,7 +60,8 @@ void gfq_rep_op_host(detail::DeviceFieldCache& F, const GfqField& field, int op,
 uint32_t resolve_chunk(const detail::DeviceFieldCache& F, const GfqField& field, u64 K, uint32_t chunk,
                        uint32_t repack = 0);
 void gfq_matmul_device(detail::DeviceFieldCache& F, const GfqField& field, const void* A, const void* B, u64 m, u64 K,
-                       u64 n, uint32_t chunk, void* C, bool reps, cudaStream_t s, uint32_t repack = 0);
+                       u64 n, uint32_t chunk, void* C, bool reps, cudaStream_t s, uint32_t repack = 0,
+                       const double* packed_b = nullptr);
 // zech_reads: when given, also the reference's data-dependent counter part (K7)
 void gfq_matmul_host(detail::DeviceFieldCache& F, const GfqField& field, const void* A, const void* B, u64 m, u64 K,
                      u64 n, uint32_t chunk, void* C, bool reps, uint32_t repack = 0, u64* zech_reads = nullptr);
