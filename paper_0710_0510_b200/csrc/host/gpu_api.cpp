@@ -1008,6 +1008,13 @@ void gfq_matmul_host(DeviceFieldCache& F, const GfqField& field, const void* A, 
         const u64 np = round_up(n, 128), kp = round_up(K, 16);
         const qpk::GfqMatmulParams M = matmul_params(F, field, K, chunk, repack);
         StreamBuf bt(kp * np * 8, S.sk);
+        // every stream drains before bt is released, also when a launch below throws
+        struct Drain {
+            Staging& st;
+            ~Drain() {
+                for (cudaStream_t q : {st.sh, st.sk, st.sk2, st.sd}) cudaStreamSynchronize(q);
+            }
+        } drain{S};
         check(cudaMemcpyAsync(db, B, K * n * es, cudaMemcpyHostToDevice, S.sh), "H2D");
         check(cudaEventRecord(S.ev_in[0], S.sh), "event");
         check(cudaStreamWaitEvent(S.sk, S.ev_in[0], 0), "wait B");
